@@ -1,0 +1,158 @@
+/*
+ * elattn_gpu.h — C ABI of the B200-native EL-attention decode path.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/elattn/attention.hpp).  Plain pointers and
+ * sizes only; no exceptions, no torch types.  Each entry point names the
+ * reference function it replaces.  The C++ wrapper with the reference's exact
+ * signatures (elattn::gpu::el_attention_folded(const Tensor&, ...)) lives in
+ * include/elattn_gpu.hpp and is built on these calls; the Python host mirror is
+ * paper_2105_04779_b200/attention.py.
+ *
+ * Conventions (reference semantics, SURVEY.md §8 "math contract"):
+ *   - all matrices row-major;
+ *   - folded query row   = ((b * g) + k) * h + i   (attention.hpp:296-302);
+ *   - output row         = b * g + k              (attention.hpp:283-288);
+ *   - H of input b lives at H + b * n_stride * d_m and is used as both key and
+ *     value source; it is never projected, copied or beam-expanded;
+ *   - "EL-Q" (q') has the reference meaning (q.Wq_i + bq_i).Wk_i^T WITHOUT the
+ *     1/sqrt(d_k) factor; the decode kernel folds 1/sqrt(d_k)*log2(e) into the
+ *     single FFMA that feeds exp2 in its online softmax;
+ *   - the key-bias scalars s (attention.hpp:192-195) may be passed but are not
+ *     applied: softmax is shift invariant (test_attention.cpp:260-271);
+ *   - element type of every activation buffer (Y, q', H, out) is the params
+ *     dtype: ELATTN_DTYPE_F32 (fp32 storage, FFMA arithmetic) or
+ *     ELATTN_DTYPE_BF16 (bf16 storage, tcgen05 tensor cores, fp32 accumulate).
+ *
+ * Errors: every call returns an elattn_status_t; the message of the last failure
+ * on the calling thread is elattn_gpu_last_error_message().  Status values map
+ * 1:1 onto the reference exception types (errors.hpp:8-31).
+ *
+ * Streams: every compute call is stream-ordered and asynchronous; buffers are
+ * device pointers owned by the caller.  A params handle is immutable after
+ * creation and may be shared read-only across streams.  `workspace` may be
+ * NULL (the library then allocates stream-ordered scratch with
+ * cudaMallocAsync); otherwise it must hold elattn_gpu_workspace_size(...) bytes.
+ */
+#ifndef ELATTN_GPU_H_
+#define ELATTN_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ELATTN_OK = 0,
+    ELATTN_ERR_SHAPE = 1,       /* ShapeError   errors.hpp:8-11  */
+    ELATTN_ERR_PARAM = 2,       /* ParamError   errors.hpp:13-16 */
+    ELATTN_ERR_STATE = 3,       /* StateError   errors.hpp:18-21 */
+    ELATTN_ERR_NUMERIC = 4,     /* NumericError errors.hpp:33-36 */
+    ELATTN_ERR_CUDA = 5,        /* CUDA runtime / launch failure  */
+    ELATTN_ERR_OOM = 6,         /* device allocation failure      */
+    ELATTN_ERR_UNSUPPORTED = 7  /* shape outside the kernels' envelope */
+} elattn_status_t;
+
+typedef enum { ELATTN_DTYPE_F32 = 0, ELATTN_DTYPE_BF16 = 1 } elattn_dtype_t;
+
+typedef struct elattn_gpu_params_s* elattn_gpu_params_t;
+typedef struct CUstream_st* elattn_stream_t; /* == cudaStream_t */
+
+/* Library version and the sm_100a kernels compiled in. */
+const char* elattn_gpu_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* elattn_gpu_last_error_message(void);
+
+/*
+ * Replaces: AttentionParams (attention.hpp:13-81) — validate() + the weights.
+ * Host fp64 arrays in the reference's per-head layout:
+ *   Wq, Wk, Wv: [h][d_m][d_k];  Wo: [h][d_k][d_m];  bq, bk, bv: [h][d_k];  bo: [d_m].
+ * Weights are packed once to device in `dtype` as W_Q^T [h*d_k][d_m],
+ * W_K [h][d_m][d_k], W_V^T [h][d_k][d_m], W_O^T [d_m][h*d_k] (every GEMM operand
+ * K-major), with fp32 biases; bv is zeroed when include_value_bias == 0.
+ * Errors: PARAM (h, d_m, d_k < 1; bad dtype), OOM, CUDA.
+ */
+int elattn_gpu_params_create(int h, int d_m, int d_k, int dtype, int include_key_bias,
+                             int include_value_bias, const double* Wq, const double* Wk,
+                             const double* Wv, const double* Wo, const double* bq,
+                             const double* bk, const double* bv, const double* bo,
+                             elattn_gpu_params_t* out);
+int elattn_gpu_params_destroy(elattn_gpu_params_t params);
+int elattn_gpu_params_info(elattn_gpu_params_t params, int* h, int* d_m, int* d_k, int* dtype);
+
+/*
+ * Replaces: build_el_query (attention.hpp:197-215) for R query rows at once
+ * (g queries of B inputs, R = B*g), already in the folded layout of
+ * fold_el_queries (attention.hpp:293-304).
+ *   Y       [R][d_m]        query rows (dtype)
+ *   qprime  [R*h][d_m]      EL-Q rows, row r*h + i (dtype)
+ *   s       [R*h] float or NULL  key-bias scalars (Q_{r,i} . bk_i; 0 if the flag is off)
+ * Errors: SHAPE (R < 1).
+ */
+int elattn_gpu_build_el_query(elattn_gpu_params_t params, const void* Y, int R, void* qprime,
+                              float* s, void* workspace, size_t workspace_bytes,
+                              elattn_stream_t stream);
+
+/*
+ * Replaces: el_attention_folded (attention.hpp:262-290), batched over B inputs.
+ *   qprime       [B*g*h][d_m]   EL-Q rows (dtype), row ((b*g)+k)*h + i
+ *   s            [B*g*h] float or NULL (accepted, not applied — see above)
+ *   H            [B][n][d_m]    per-input hidden states (dtype)
+ *   n_per_input  device int[B] or NULL: ragged context lengths, 1 <= n_b <= n
+ *                (rows n_b..n-1 of H_b are ignored; an out-of-range n_b writes NaN rows)
+ *   out          [B*g][d_m]     (dtype), row b*g + k
+ * Errors: SHAPE (B, g < 1), STATE (n < 1, the reference's "empty context").
+ */
+int elattn_gpu_el_attention_folded(elattn_gpu_params_t params, const void* qprime, const float* s,
+                                   const void* H, const int* n_per_input, int B, int g, int n,
+                                   void* out, void* workspace, size_t workspace_bytes,
+                                   elattn_stream_t stream);
+
+/*
+ * Replaces: one EL cross-attention sub-layer for a batch of lanes — the
+ * reference's per-lane el_attention(yc, H, cross_attn) calls (model.hpp:373-377,
+ * attention.hpp:239-257) for B inputs x x beams in one stream-ordered pass:
+ *   (1) query expansion  Q = Y.W_Q + b_Q ; q'_{r,i} = Q_{r,i}.W_K,i^T
+ *   (2) fused decode     P = softmax(q'.H_b^T / sqrt(d_k)) ; C = P.H_b  (H read once)
+ *   (3) output proj.     out = concat_i(C_{r,i}.W_V,i + b_V,i).W_O + b_O
+ *   Y [B*x][d_m], H [B][n][d_m], out [B*x][d_m] (dtype).
+ * Errors: SHAPE (B, x < 1), STATE (n < 1).
+ */
+int elattn_gpu_el_attention_step(elattn_gpu_params_t params, const void* Y, const void* H,
+                                 const int* n_per_input, int B, int x, int n, void* out,
+                                 void* workspace, size_t workspace_bytes, elattn_stream_t stream);
+
+/*
+ * Stage (2) alone — the fused flash-style pass of el_attention_folded
+ * (attention.hpp:272-280: scores, softmax, P.H) without the output projection:
+ *   qprime [B*rows][d_m], H [B][n][d_m]  ->  ctx [B*rows][d_m]   (dtype)
+ * rows = query rows per input (g*h).  Exposed for stage-level timing and for
+ * callers that fuse their own projection.
+ */
+int elattn_gpu_el_attention_decode(elattn_gpu_params_t params, const void* qprime, const void* H,
+                                   const int* n_per_input, int B, int rows, int n, void* ctx,
+                                   elattn_stream_t stream);
+
+/* Scratch bytes needed by the calls above for (B inputs, g queries each, n). */
+size_t elattn_gpu_workspace_size(elattn_gpu_params_t params, int B, int g, int n);
+
+/*
+ * Which decode kernel a (params, g) pair dispatches to:
+ *   0 = SIMT (fp32 FFMA, or bf16 storage with fp32 FFMA),
+ *   1 = tcgen05/TMEM/TMA fused decode (bf16, cluster of 2 CTAs per input).
+ */
+int elattn_gpu_decode_kernel_kind(elattn_gpu_params_t params, int g);
+
+/* Device-kernel launches issued by this thread since the last reset (for bench
+ * accounting of gpu_launches). */
+int64_t elattn_gpu_launch_count(void);
+void elattn_gpu_reset_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ELATTN_GPU_H_ */

@@ -1,0 +1,368 @@
+"""Host-side mirror of the reference's EL-attention interface, on the B200 path.
+
+Names, argument meaning, layouts and error types follow
+``/root/reference/proj/include/elattn/attention.hpp`` so reference-style tests
+read the same; the arithmetic runs in ``libelattn_gpu.so`` (sm_100a kernels)
+through the C ABI of ``include/elattn_gpu.h``.  Two layers:
+
+* reference-shaped, host-buffer calls (``build_el_query``, ``fold_el_queries``,
+  ``el_attention``, ``el_attention_folded``) that take/return fp64 numpy arrays
+  exactly like the reference's ``Tensor`` API (H2D/D2H inside the call);
+* the device-resident batched API (:class:`ElAttentionLayer`) that the decoder
+  step and ``bench.py`` use: torch CUDA tensors in HBM, stream-ordered, no host
+  round trip.
+
+torch is used for device memory and streams only (plumbing, not compute).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import capi
+from .capi import DTYPE_BF16, DTYPE_F32, ParamError, ShapeError, StateError
+
+__all__ = [
+    "Rng", "seeded_uniform", "AttentionParams", "ElQuery", "DeviceParams", "ElAttentionLayer",
+    "build_el_query", "fold_el_queries", "el_attention", "el_attention_folded",
+    "DTYPE_F32", "DTYPE_BF16",
+]
+
+_MASK64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+_GAMMA = np.uint64(0x9E3779B97F4A7C15)
+
+
+class Rng:
+    """SplitMix64, bit-identical to ``elattn::Rng`` (tensor.hpp:133-150).
+
+    Vectorised: the k-th output depends only on ``seed + k*gamma``, so a block
+    of draws is one numpy expression instead of a Python loop.
+    """
+
+    def __init__(self, seed: int):
+        self.state = np.uint64(seed & 0xFFFFFFFFFFFFFFFF)
+
+    def next_u64_block(self, count: int) -> np.ndarray:
+        with np.errstate(over="ignore"):
+            k = np.arange(1, count + 1, dtype=np.uint64)
+            z = self.state + k * _GAMMA
+            self.state = self.state + np.uint64(count) * _GAMMA
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            return z ^ (z >> np.uint64(31))
+
+    def next_u64(self) -> int:
+        return int(self.next_u64_block(1)[0])
+
+    def next_double_block(self, count: int) -> np.ndarray:
+        # (u >> 11) * 2^-53 (tensor.hpp:146)
+        return (self.next_u64_block(count) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+    def next_double(self) -> float:
+        return float(self.next_double_block(1)[0])
+
+
+def seeded_uniform(shape: Sequence[int], rng: Rng, lo: float, hi: float) -> np.ndarray:
+    """``seeded_uniform`` (tensor.hpp:236-241): row-major fill ``lo + (hi-lo)*u``."""
+    if not lo < hi:
+        raise ParamError("seeded_uniform: lo must be < hi")
+    shape = tuple(int(s) for s in shape)
+    if not shape or any(s <= 0 for s in shape):
+        raise ShapeError("tensor dimensions must be positive")
+    n = int(np.prod(shape))
+    return (lo + (hi - lo) * rng.next_double_block(n)).reshape(shape)
+
+
+@dataclass
+class AttentionParams:
+    """``AttentionParams`` (attention.hpp:13-81) with per-head tensors stacked.
+
+    Wq, Wk, Wv: [h, d_m, d_k]; Wo: [h, d_k, d_m]; bq, bk, bv: [h, d_k]; bo: [d_m].
+    """
+
+    h: int
+    d_m: int
+    d_k: int
+    Wq: np.ndarray
+    Wk: np.ndarray
+    Wv: np.ndarray
+    Wo: np.ndarray
+    bq: np.ndarray
+    bk: np.ndarray
+    bv: np.ndarray
+    bo: np.ndarray
+    include_key_bias: bool = True
+    include_value_bias: bool = True
+
+    def validate(self) -> None:  # attention.hpp:24-50
+        if self.h < 1 or self.d_m < 1 or self.d_k < 1:
+            raise ParamError("AttentionParams: h, d_m, d_k must be >= 1")
+        want = {"Wq": (self.h, self.d_m, self.d_k), "Wk": (self.h, self.d_m, self.d_k),
+                "Wv": (self.h, self.d_m, self.d_k), "Wo": (self.h, self.d_k, self.d_m),
+                "bq": (self.h, self.d_k), "bk": (self.h, self.d_k), "bv": (self.h, self.d_k),
+                "bo": (self.d_m,)}
+        for name, shape in want.items():
+            if tuple(np.shape(getattr(self, name))) != shape:
+                raise ShapeError(f"AttentionParams: {name} entry has shape {np.shape(getattr(self, name))}")
+
+    @classmethod
+    def random(cls, h: int, d_m: int, d_k: int, rng: Rng, lo: float = -0.1, hi: float = 0.1) -> "AttentionParams":
+        """Draw order Wq[0..h), Wk, Wv, Wo, bq, bk, bv, bo (attention.hpp:52-80)."""
+        if h < 1 or d_m < 1 or d_k < 1:
+            raise ParamError("AttentionParams: h, d_m, d_k must be >= 1")
+        mats = lambda r, c: seeded_uniform((h * r, c), rng, lo, hi).reshape(h, r, c)  # noqa: E731
+        Wq, Wk, Wv, Wo = mats(d_m, d_k), mats(d_m, d_k), mats(d_m, d_k), mats(d_k, d_m)
+        vecs = lambda n: seeded_uniform((h, n), rng, lo, hi)  # noqa: E731
+        bq, bk, bv = vecs(d_k), vecs(d_k), vecs(d_k)
+        bo = seeded_uniform((d_m,), rng, lo, hi)
+        return cls(h, d_m, d_k, Wq, Wk, Wv, Wo, bq, bk, bv, bo)
+
+    def cast(self, dtype: int) -> "AttentionParams":
+        """Copy with every weight rounded to the storage dtype (RNE), as fp64.
+
+        Feeding these to the CPU reference isolates kernel arithmetic error
+        from input rounding (SURVEY.md §8(c) parity protocol)."""
+        f = (lambda a: round_to_dtype(a, dtype))
+        return AttentionParams(self.h, self.d_m, self.d_k, f(self.Wq), f(self.Wk), f(self.Wv),
+                               f(self.Wo), self.bq.astype(np.float32).astype(np.float64),
+                               self.bk.astype(np.float32).astype(np.float64),
+                               self.bv.astype(np.float32).astype(np.float64),
+                               self.bo.astype(np.float32).astype(np.float64),
+                               self.include_key_bias, self.include_value_bias)
+
+
+def round_to_dtype(a: np.ndarray, dtype: int) -> np.ndarray:
+    """Round fp64 values to fp32 or bf16 (round-to-nearest-even) and back to fp64."""
+    a32 = np.ascontiguousarray(a, dtype=np.float32)
+    if dtype == DTYPE_F32:
+        return a32.astype(np.float64)
+    u = a32.view(np.uint32).astype(np.uint64)
+    rounded = ((u + np.uint64(0x7FFF) + ((u >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)) << np.uint64(16)
+    nan = np.isnan(a32)
+    out = rounded.astype(np.uint32).view(np.float32).astype(np.float64)
+    out[nan] = np.nan
+    return out
+
+
+@dataclass
+class ElQuery:
+    """``ElQuery`` (attention.hpp:192-195): elq [h, d_m] and key-bias scalars s [h]."""
+
+    elq: np.ndarray
+    s: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+def _torch():
+    import torch  # plumbing only: device memory + streams
+
+    return torch
+
+
+def _tdtype(dtype: int):
+    torch = _torch()
+    return torch.bfloat16 if dtype == DTYPE_BF16 else torch.float32
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class DeviceParams:
+    """Opaque device weights (``elattn_gpu_params_t``): packed once, K-major, in `dtype`."""
+
+    def __init__(self, p: AttentionParams, dtype: int = DTYPE_BF16):
+        p.validate()
+        self.h, self.d_m, self.d_k, self.dtype = p.h, p.d_m, p.d_k, dtype
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (p.Wq, p.Wk, p.Wv, p.Wo, p.bq, p.bk, p.bv, p.bo)]
+        self._keep = arrs
+        handle = ctypes.c_void_p()
+        L = capi.lib()
+        capi.check(L.elattn_gpu_params_create(p.h, p.d_m, p.d_k, dtype, int(p.include_key_bias),
+                                              int(p.include_value_bias),
+                                              *[a.ctypes.data for a in arrs], ctypes.byref(handle)))
+        self.handle = handle
+        self._keep = None
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            capi.check(capi.lib().elattn_gpu_params_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def workspace_size(self, B: int, g: int, n: int) -> int:
+        return int(capi.lib().elattn_gpu_workspace_size(self.handle, B, g, n))
+
+    def decode_kernel_kind(self, g: int) -> int:
+        return int(capi.lib().elattn_gpu_decode_kernel_kind(self.handle, g))
+
+
+class ElAttentionLayer:
+    """Device-resident batched EL cross-attention sub-layer (one decoder layer).
+
+    ``step(Y, H)`` computes, for B inputs x beams, exactly what the reference
+    computes lane by lane with ``el_attention(yc, H, cross_attn)``
+    (model.hpp:373-377): Y [B*x, d_m], H [B, n, d_m] -> out [B*x, d_m].
+    """
+
+    def __init__(self, params: AttentionParams | DeviceParams, dtype: int = DTYPE_BF16):
+        self.dev = params if isinstance(params, DeviceParams) else DeviceParams(params, dtype)
+        self.dtype = self.dev.dtype
+        self._ws = None
+
+    def workspace(self, B: int, x: int, n: int):
+        torch = _torch()
+        need = self.dev.workspace_size(B, x, n)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+        return self._ws
+
+    def _check(self, t, shape, what):
+        torch = _torch()
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise ParamError(f"{what}: expected a CUDA tensor")
+        if t.dtype != _tdtype(self.dtype) or not t.is_contiguous():
+            raise ParamError(f"{what}: expected contiguous {_tdtype(self.dtype)}")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise ShapeError(f"{what}: shape {tuple(t.shape)} != {tuple(shape)}")
+
+    def step(self, Y, H, n_per_input=None, out=None, stream=None):
+        torch = _torch()
+        if H.dim() != 3:
+            raise ShapeError("H must be [B, n, d_m]")
+        B, n, d_m = H.shape
+        if d_m != self.dev.d_m:
+            raise ShapeError("el_attention: q/H width must equal d_m")
+        if Y.dim() != 2 or Y.shape[1] != d_m or B < 1 or Y.shape[0] % B:
+            raise ShapeError("Y must be [B*x, d_m]")
+        x = Y.shape[0] // B
+        self._check(Y, None, "Y")
+        self._check(H, None, "H")
+        if out is None:
+            out = torch.empty_like(Y)
+        self._check(out, Y.shape, "out")
+        npi = 0
+        if n_per_input is not None:
+            if n_per_input.dtype != torch.int32 or not n_per_input.is_cuda or n_per_input.numel() != B:
+                raise ParamError("n_per_input must be a CUDA int32 tensor of length B")
+            npi = n_per_input.data_ptr()
+        ws = self.workspace(B, x, n)
+        capi.check(capi.lib().elattn_gpu_el_attention_step(
+            self.dev.handle, Y.data_ptr(), H.data_ptr(), npi or None, B, x, n, out.data_ptr(),
+            ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+        return out
+
+    def build_el_query(self, Y, qprime=None, s=None, stream=None):
+        torch = _torch()
+        R = Y.shape[0]
+        self._check(Y, (R, self.dev.d_m), "Y")
+        if qprime is None:
+            qprime = torch.empty(R * self.dev.h, self.dev.d_m, dtype=Y.dtype, device=Y.device)
+        ws = self.workspace(R, 1, 1)
+        capi.check(capi.lib().elattn_gpu_build_el_query(
+            self.dev.handle, Y.data_ptr(), R, qprime.data_ptr(), s.data_ptr() if s is not None else None,
+            ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+        return qprime
+
+    def el_attention_folded(self, qprime, H, g, n_per_input=None, out=None, stream=None):
+        torch = _torch()
+        B, n, d_m = H.shape
+        self._check(qprime, (B * g * self.dev.h, d_m), "queries")
+        self._check(H, None, "H")
+        if out is None:
+            out = torch.empty(B * g, d_m, dtype=H.dtype, device=H.device)
+        ws = self.workspace(B, g, n)
+        npi = n_per_input.data_ptr() if n_per_input is not None else None
+        capi.check(capi.lib().elattn_gpu_el_attention_folded(
+            self.dev.handle, qprime.data_ptr(), None, H.data_ptr(), npi, B, g, n, out.data_ptr(),
+            ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# Reference-shaped host API (fp64 numpy in / out), the drop-in for attention.hpp.
+# ---------------------------------------------------------------------------
+
+def _as_device(a: np.ndarray, dtype: int):
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(
+        device="cuda", dtype=_tdtype(dtype)).contiguous()
+
+
+def _to_host(t) -> np.ndarray:
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def _layer(p, dtype) -> ElAttentionLayer:
+    return ElAttentionLayer(p if isinstance(p, DeviceParams) else DeviceParams(p, dtype))
+
+
+def _params_dims(p):
+    return p.h, p.d_m, p.d_k
+
+
+def build_el_query(q: np.ndarray, p: AttentionParams | DeviceParams, dtype: int = DTYPE_F32) -> ElQuery:
+    """``build_el_query`` (attention.hpp:197-215): q [1, d_m] -> ElQuery{elq [h, d_m], s [h]}."""
+    torch = _torch()
+    h, d_m, _ = _params_dims(p)
+    q = np.asarray(q, dtype=np.float64)
+    if q.ndim != 2 or q.shape != (1, d_m):
+        raise ShapeError("build_el_query: q must be 1 x d_m")
+    layer = _layer(p, dtype)
+    s = torch.empty(h, dtype=torch.float32, device="cuda")
+    elq = layer.build_el_query(_as_device(q, layer.dtype), s=s)
+    torch.cuda.current_stream().synchronize()
+    return ElQuery(_to_host(elq), s.double().cpu().numpy())
+
+
+def fold_el_queries(queries: Sequence[ElQuery], h: int, d_m: int):
+    """``fold_el_queries`` (attention.hpp:293-304): rows b*h + i."""
+    q = np.concatenate([np.asarray(e.elq, dtype=np.float64).reshape(h, d_m) for e in queries], axis=0)
+    s = np.concatenate([np.asarray(e.s, dtype=np.float64).reshape(h) for e in queries], axis=0)
+    return q, s
+
+
+def el_attention_folded(queries: np.ndarray, H: np.ndarray, bias_scalars: np.ndarray,
+                        p: AttentionParams | DeviceParams, dtype: int = DTYPE_F32) -> np.ndarray:
+    """``el_attention_folded`` (attention.hpp:262-290): [(g*h), d_m] x H [n, d_m] -> [g, d_m]."""
+    h, d_m, _ = _params_dims(p)
+    queries = np.asarray(queries, dtype=np.float64)
+    if queries.ndim != 2 or queries.shape[0] % h != 0:
+        raise ShapeError(f"el_attention_folded: query row count {queries.shape[0]} not divisible by h={h}")
+    if np.asarray(bias_scalars).size != queries.shape[0]:
+        raise ShapeError("el_attention_folded: bias scalar count must equal query rows")
+    H = np.asarray(H, dtype=np.float64)
+    if H.size == 0 or H.shape[0] < 1:
+        raise StateError("el_attention_folded: empty context")
+    if queries.shape[1] != d_m or H.ndim != 2 or H.shape[1] != d_m:
+        raise ShapeError("el_attention_folded: width must equal d_m")
+    g = queries.shape[0] // h
+    layer = _layer(p, dtype)
+    out = layer.el_attention_folded(_as_device(queries, layer.dtype), _as_device(H[None], layer.dtype), g)
+    return _to_host(out)
+
+
+def el_attention(q: np.ndarray, H: np.ndarray, p: AttentionParams | DeviceParams,
+                 dtype: int = DTYPE_F32) -> np.ndarray:
+    """``el_attention`` (attention.hpp:239-257): q [1, d_m], H [n, d_m] -> [1, d_m]."""
+    h, d_m, _ = _params_dims(p)
+    H = np.asarray(H, dtype=np.float64)
+    if H.size == 0 or H.shape[0] < 1:
+        raise StateError("el_attention: empty context")
+    q = np.asarray(q, dtype=np.float64)
+    if q.ndim != 2 or q.shape[1] != d_m or H.ndim != 2 or H.shape[1] != d_m:
+        raise ShapeError("el_attention: q/H width must equal d_m")
+    layer = _layer(p, dtype)
+    out = layer.step(_as_device(q, layer.dtype), _as_device(H[None], layer.dtype))
+    return _to_host(out)

@@ -1,0 +1,363 @@
+// capi.cu — the extern "C" boundary (include/elattn_gpu.h).
+//
+// Host-side orchestration of the three hot-path stages, each stream-ordered:
+//   (1) query expansion  (build_el_query, attention.hpp:197-215)
+//   (2) fused decode     (el_attention_folded core, attention.hpp:272-280)
+//   (3) output proj.     (el_attention_folded tail + el_bias_terms, :281-288, :221-231)
+// No CPU compute path exists: every arithmetic step is a device kernel.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+struct elattn_gpu_params_s {
+    int h = 0, d_m = 0, d_k = 0, dtype = 0;
+    int include_key_bias = 1, include_value_bias = 1;
+    // Device buffers, element type `dtype` unless noted.
+    void* WqT = nullptr;  // [h*d_k][d_m]
+    void* Wk = nullptr;   // [h][d_m][d_k]
+    void* WvT = nullptr;  // [h][d_k][d_m]
+    void* WoT = nullptr;  // [d_m][h*d_k]
+    float* bq = nullptr;  // [h*d_k]
+    float* bk = nullptr;  // [h*d_k]
+    float* bv = nullptr;  // [h*d_k] (zero when include_value_bias == 0)
+    float* bo = nullptr;  // [d_m]
+};
+
+namespace elattn_gpu {
+
+namespace {
+thread_local std::string g_last_error;
+thread_local int64_t g_launches = 0;
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches += n; }
+
+namespace {
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return ELATTN_OK;
+    } catch (const Status& s) {
+        g_last_error = s.msg;
+        return s.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return ELATTN_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return ELATTN_ERR_CUDA;
+    }
+}
+
+uint16_t f32_to_bf16_rne(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t((u >> 16) | 0x40);  // NaN stays NaN
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return uint16_t(u >> 16);
+}
+
+// Upload an fp64 host array as `dtype` (fp32 or bf16, RNE).
+void* upload(const std::vector<double>& v, int dtype) {
+    void* d = nullptr;
+    const size_t n = v.size();
+    if (dtype == ELATTN_DTYPE_BF16) {
+        std::vector<uint16_t> h(n);
+        for (size_t i = 0; i < n; ++i) h[i] = f32_to_bf16_rne(float(v[i]));
+        ELA_CHECK_CUDA(cudaMalloc(&d, n * 2));
+        ELA_CHECK_CUDA(cudaMemcpy(d, h.data(), n * 2, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> h(n);
+        for (size_t i = 0; i < n; ++i) h[i] = float(v[i]);
+        ELA_CHECK_CUDA(cudaMalloc(&d, n * 4));
+        ELA_CHECK_CUDA(cudaMemcpy(d, h.data(), n * 4, cudaMemcpyHostToDevice));
+    }
+    return d;
+}
+
+float* upload_f32(const std::vector<double>& v) {
+    return static_cast<float*>(upload(v, ELATTN_DTYPE_F32));
+}
+
+void free_params(elattn_gpu_params_s* p) {
+    if (!p) return;
+    for (void* ptr : {p->WqT, p->Wk, p->WvT, p->WoT, (void*)p->bq, (void*)p->bk, (void*)p->bv,
+                      (void*)p->bo})
+        if (ptr) cudaFree(ptr);
+    delete p;
+}
+
+// Stream-ordered scratch: caller-provided or cudaMallocAsync'd for this call.
+class Scratch {
+   public:
+    Scratch(void* ws, size_t ws_bytes, size_t need, cudaStream_t st) : st_(st) {
+        if (need == 0) return;
+        if (ws) {
+            ELA_REQUIRE(ws_bytes >= need, ELATTN_ERR_PARAM,
+                        "workspace too small: need " + std::to_string(need) + " bytes");
+            base_ = static_cast<char*>(ws);
+        } else {
+            ELA_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base_), need, st));
+            owned_ = true;
+        }
+    }
+    ~Scratch() {
+        if (owned_) cudaFreeAsync(base_, st_);
+    }
+    void* take(size_t bytes) {
+        void* p = base_ + off_;
+        off_ += (bytes + 255) & ~size_t(255);
+        return p;
+    }
+
+   private:
+    char* base_ = nullptr;
+    size_t off_ = 0;
+    bool owned_ = false;
+    cudaStream_t st_;
+};
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// Scratch layout of a full step: Q [R][h*d_k], q' [R*h][d_m], C [R*h][d_m], V [R][h*d_k].
+size_t step_workspace(const elattn_gpu_params_s* p, int64_t R) {
+    const size_t e = dtype_bytes(p->dtype);
+    const size_t hk = size_t(p->h) * p->d_k, hm = size_t(p->h) * p->d_m;
+    return align256(R * hk * e) * 2 + align256(R * hm * e) * 2;
+}
+
+void gemm(const elattn_gpu_params_s* p, const GemmArgs& g, cudaStream_t st) {
+    if (p->dtype == ELATTN_DTYPE_BF16 && tc_gemm_supported(g))
+        launch_tc_gemm(g, st);
+    else
+        launch_simt_gemm(p->dtype, g, st);
+}
+
+// (1a) Q = Y.W_Q + b_Q ; (1b) q'_{r,i} = Q_{r,i}.W_K,i^T   (attention.hpp:205-206)
+void query_expansion(const elattn_gpu_params_s* p, const void* Y, int64_t R, void* Q, void* qp,
+                     cudaStream_t st) {
+    const int h = p->h, d_m = p->d_m, d_k = p->d_k, hk = h * d_k;
+    GemmArgs a{};
+    a.A = Y, a.lda = d_m, a.B = p->WqT, a.ldb = d_m, a.C = Q, a.ldc = hk, a.bias = p->bq;
+    a.M = int(R), a.N = hk, a.K = d_m, a.Z = 1, a.alpha = 1.f;
+    gemm(p, a, st);
+    const size_t e = dtype_bytes(p->dtype);
+    GemmArgs b{};
+    b.A = Q, b.lda = hk, b.sAz = d_k;                         // head i: columns i*d_k..
+    b.B = p->Wk, b.ldb = d_k, b.sBz = int64_t(d_m) * d_k;     // W_K,i [d_m][d_k] is K-major
+    b.C = qp, b.ldc = int64_t(h) * d_m, b.sCz = d_m;          // row r*h + i
+    b.M = int(R), b.N = d_m, b.K = d_k, b.Z = h, b.alpha = 1.f;
+    (void)e;
+    gemm(p, b, st);
+}
+
+// (3a) V_{r,i} = C_{r*h+i}.W_V,i + b_V,i ; (3b) out = V.W_O + b_O   (attention.hpp:283-288)
+void output_projection(const elattn_gpu_params_s* p, const void* C, int64_t R, void* V, void* out,
+                       cudaStream_t st) {
+    const int h = p->h, d_m = p->d_m, d_k = p->d_k, hk = h * d_k;
+    GemmArgs a{};
+    a.A = C, a.lda = int64_t(h) * d_m, a.sAz = d_m;
+    a.B = p->WvT, a.ldb = d_m, a.sBz = int64_t(d_k) * d_m;
+    a.C = V, a.ldc = hk, a.sCz = d_k;
+    a.bias = p->bv, a.sbz = d_k;
+    a.M = int(R), a.N = d_k, a.K = d_m, a.Z = h, a.alpha = 1.f;
+    gemm(p, a, st);
+    GemmArgs b{};
+    b.A = V, b.lda = hk, b.B = p->WoT, b.ldb = hk, b.C = out, b.ldc = d_m, b.bias = p->bo;
+    b.M = int(R), b.N = d_m, b.K = hk, b.Z = 1, b.alpha = 1.f;
+    gemm(p, b, st);
+}
+
+bool use_tc_decode(const elattn_gpu_params_s* p, int rows_per_input) {
+    return p->dtype == ELATTN_DTYPE_BF16 && el_decode_tc_supported(rows_per_input, p->d_m);
+}
+
+// (2) fused decode: C = softmax(q'.H^T / sqrt(d_k)) . H   (attention.hpp:272-280)
+void decode(const elattn_gpu_params_s* p, const void* qp, const void* H, const int* npi, int B,
+            int rows_per_input, int n, void* C, cudaStream_t st) {
+    const float scale = float(1.0 / std::sqrt(double(p->d_k)));
+    if (use_tc_decode(p, rows_per_input))
+        launch_el_decode_tc(qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st);
+    else
+        launch_el_decode_simt(p->dtype, qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st);
+}
+
+void check_handle(const elattn_gpu_params_s* p) {
+    ELA_REQUIRE(p != nullptr, ELATTN_ERR_PARAM, "null params handle");
+}
+
+}  // namespace
+}  // namespace elattn_gpu
+
+using namespace elattn_gpu;
+
+extern "C" {
+
+const char* elattn_gpu_version(void) {
+    return "elattn-b200 0.1 (sm_100a: SIMT fp32/bf16, tcgen05 GEMM, tcgen05 fused EL decode)";
+}
+
+const char* elattn_gpu_last_error_message(void) { return g_last_error.c_str(); }
+
+int64_t elattn_gpu_launch_count(void) { return g_launches; }
+void elattn_gpu_reset_launch_count(void) { g_launches = 0; }
+
+int elattn_gpu_params_create(int h, int d_m, int d_k, int dtype, int include_key_bias,
+                             int include_value_bias, const double* Wq, const double* Wk,
+                             const double* Wv, const double* Wo, const double* bq,
+                             const double* bk, const double* bv, const double* bo,
+                             elattn_gpu_params_t* out) {
+    return guarded([&] {
+        // AttentionParams::validate (attention.hpp:24-50)
+        ELA_REQUIRE(out != nullptr, ELATTN_ERR_PARAM, "null output handle pointer");
+        *out = nullptr;
+        ELA_REQUIRE(h >= 1 && d_m >= 1 && d_k >= 1, ELATTN_ERR_PARAM,
+                    "AttentionParams: h, d_m, d_k must be >= 1");
+        ELA_REQUIRE(dtype == ELATTN_DTYPE_F32 || dtype == ELATTN_DTYPE_BF16, ELATTN_ERR_PARAM,
+                    "unknown dtype");
+        ELA_REQUIRE(Wq && Wk && Wv && Wo && bq && bk && bv && bo, ELATTN_ERR_SHAPE,
+                    "AttentionParams: null weight array");
+        const size_t H_ = size_t(h), M = size_t(d_m), K = size_t(d_k);
+        std::vector<double> wqT(H_ * K * M), wk(H_ * M * K), wvT(H_ * K * M), woT(M * H_ * K);
+        for (size_t i = 0; i < H_; ++i)
+            for (size_t j = 0; j < M; ++j)
+                for (size_t c = 0; c < K; ++c) {
+                    const size_t src = (i * M + j) * K + c;  // [h][d_m][d_k]
+                    wqT[(i * K + c) * M + j] = Wq[src];
+                    wk[src] = Wk[src];
+                    wvT[(i * K + c) * M + j] = Wv[src];
+                }
+        for (size_t i = 0; i < H_; ++i)
+            for (size_t c = 0; c < K; ++c)
+                for (size_t j = 0; j < M; ++j) woT[j * H_ * K + i * K + c] = Wo[(i * K + c) * M + j];
+        std::vector<double> vbq(bq, bq + H_ * K), vbk(bk, bk + H_ * K), vbv(H_ * K, 0.0),
+            vbo(bo, bo + M);
+        if (include_value_bias) vbv.assign(bv, bv + H_ * K);
+        std::unique_ptr<elattn_gpu_params_s, void (*)(elattn_gpu_params_s*)> p(
+            new elattn_gpu_params_s, free_params);
+        p->h = h, p->d_m = d_m, p->d_k = d_k, p->dtype = dtype;
+        p->include_key_bias = include_key_bias != 0;
+        p->include_value_bias = include_value_bias != 0;
+        p->WqT = upload(wqT, dtype);
+        p->Wk = upload(wk, dtype);
+        p->WvT = upload(wvT, dtype);
+        p->WoT = upload(woT, dtype);
+        p->bq = upload_f32(vbq);
+        p->bk = upload_f32(vbk);
+        p->bv = upload_f32(vbv);
+        p->bo = upload_f32(vbo);
+        *out = p.release();
+    });
+}
+
+int elattn_gpu_params_destroy(elattn_gpu_params_t params) {
+    return guarded([&] { free_params(params); });
+}
+
+int elattn_gpu_params_info(elattn_gpu_params_t p, int* h, int* d_m, int* d_k, int* dtype) {
+    return guarded([&] {
+        check_handle(p);
+        if (h) *h = p->h;
+        if (d_m) *d_m = p->d_m;
+        if (d_k) *d_k = p->d_k;
+        if (dtype) *dtype = p->dtype;
+    });
+}
+
+size_t elattn_gpu_workspace_size(elattn_gpu_params_t p, int B, int g, int n) {
+    (void)n;
+    if (!p || B < 1 || g < 1) return 0;
+    return step_workspace(p, int64_t(B) * g);
+}
+
+int elattn_gpu_decode_kernel_kind(elattn_gpu_params_t p, int g) {
+    if (!p || g < 1) return -1;
+    return use_tc_decode(p, g * p->h) ? 1 : 0;
+}
+
+int elattn_gpu_build_el_query(elattn_gpu_params_t p, const void* Y, int R, void* qprime, float* s,
+                              void* ws, size_t ws_bytes, elattn_stream_t stream) {
+    return guarded([&] {
+        check_handle(p);
+        ELA_REQUIRE(R >= 1, ELATTN_ERR_SHAPE, "build_el_query: need at least one query row");
+        ELA_REQUIRE(Y && qprime, ELATTN_ERR_PARAM, "build_el_query: null buffer");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const size_t qbytes = size_t(R) * p->h * p->d_k * dtype_bytes(p->dtype);
+        Scratch scratch(ws, ws_bytes, align256(qbytes), st);
+        void* Q = scratch.take(qbytes);
+        query_expansion(p, Y, R, Q, qprime, st);
+        if (s) {
+            if (p->include_key_bias)
+                launch_key_bias_scalars(p->dtype, Q, p->bk, R, p->h, p->d_k, s, st);
+            else
+                ELA_CHECK_CUDA(cudaMemsetAsync(s, 0, sizeof(float) * size_t(R) * p->h, st));
+        }
+    });
+}
+
+int elattn_gpu_el_attention_folded(elattn_gpu_params_t p, const void* qprime, const float* s,
+                                   const void* H, const int* n_per_input, int B, int g, int n,
+                                   void* out, void* ws, size_t ws_bytes, elattn_stream_t stream) {
+    (void)s;  // shift invariance: see header
+    return guarded([&] {
+        check_handle(p);
+        ELA_REQUIRE(B >= 1 && g >= 1, ELATTN_ERR_SHAPE,
+                    "el_attention_folded: query row count must be a positive multiple of h");
+        ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "el_attention_folded: empty context");
+        ELA_REQUIRE(qprime && H && out, ELATTN_ERR_PARAM, "el_attention_folded: null buffer");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const int64_t R = int64_t(B) * g;
+        const size_t e = dtype_bytes(p->dtype);
+        const size_t cbytes = size_t(R) * p->h * p->d_m * e, vbytes = size_t(R) * p->h * p->d_k * e;
+        Scratch scratch(ws, ws_bytes, align256(cbytes) + align256(vbytes), st);
+        void* C = scratch.take(cbytes);
+        void* V = scratch.take(vbytes);
+        decode(p, qprime, H, n_per_input, B, g * p->h, n, C, st);
+        output_projection(p, C, R, V, out, st);
+    });
+}
+
+int elattn_gpu_el_attention_decode(elattn_gpu_params_t p, const void* qprime, const void* H,
+                                   const int* n_per_input, int B, int rows, int n, void* ctx,
+                                   elattn_stream_t stream) {
+    return guarded([&] {
+        check_handle(p);
+        ELA_REQUIRE(B >= 1 && rows >= 1, ELATTN_ERR_SHAPE, "el_attention_decode: B, rows must be >= 1");
+        ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "el_attention_decode: empty context");
+        ELA_REQUIRE(qprime && H && ctx, ELATTN_ERR_PARAM, "el_attention_decode: null buffer");
+        decode(p, qprime, H, n_per_input, B, rows, n, ctx, reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
+int elattn_gpu_el_attention_step(elattn_gpu_params_t p, const void* Y, const void* H,
+                                 const int* n_per_input, int B, int x, int n, void* out, void* ws,
+                                 size_t ws_bytes, elattn_stream_t stream) {
+    return guarded([&] {
+        check_handle(p);
+        ELA_REQUIRE(B >= 1 && x >= 1, ELATTN_ERR_SHAPE, "el_attention_step: B and x must be >= 1");
+        ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "el_attention: empty context");
+        ELA_REQUIRE(Y && H && out, ELATTN_ERR_PARAM, "el_attention_step: null buffer");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const int64_t R = int64_t(B) * x;
+        const size_t e = dtype_bytes(p->dtype);
+        const size_t qb = size_t(R) * p->h * p->d_k * e, qpb = size_t(R) * p->h * p->d_m * e;
+        Scratch scratch(ws, ws_bytes, step_workspace(p, R), st);
+        void* Q = scratch.take(qb);
+        void* qp = scratch.take(qpb);
+        void* C = scratch.take(qpb);
+        void* V = scratch.take(qb);
+        query_expansion(p, Y, R, Q, qp, st);
+        decode(p, qp, H, n_per_input, B, x * p->h, n, C, st);
+        output_projection(p, C, R, V, out, st);
+    });
+}
+
+}  // extern "C"

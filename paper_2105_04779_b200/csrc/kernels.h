@@ -1,0 +1,49 @@
+// kernels.h — host-side launchers for every device kernel in the library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace elattn_gpu {
+
+// Batched GEMM on CUDA cores (fp32 FFMA), operands of storage type `dtype`:
+//   C[z][m][n] = alpha * sum_k A[z][m][k] * B[z][n][k] + bias[z][n]
+// (B is given K-major, i.e. as [N][K]).  bias may be null; C has the same
+// storage dtype as A/B unless c_f32.
+struct GemmArgs {
+    const void* A;
+    int64_t lda, sAz;
+    const void* B;
+    int64_t ldb, sBz;
+    void* C;
+    int64_t ldc, sCz;
+    const float* bias;
+    int64_t sbz;
+    int M, N, K, Z;
+    float alpha;
+};
+void launch_simt_gemm(int dtype, const GemmArgs& g, cudaStream_t st);
+
+// s[r*h + i] = sum_c Q[r][i*d_k + c] * bk[i*d_k + c]  (key-bias scalars).
+void launch_key_bias_scalars(int dtype, const void* Q, const float* bk, int R, int h, int d_k,
+                             float* s, cudaStream_t st);
+
+// SIMT fused EL decode: ctx[b*rows + r] = softmax(q'_r . H_b^T * scale) . H_b.
+void launch_el_decode_simt(int dtype, const void* qp, const void* H, const int* n_per_input,
+                           int B, int rows_per_input, int n_stride, int d_m, float scale,
+                           void* ctx, cudaStream_t st);
+
+// tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM, bf16 out), same contract as
+// launch_simt_gemm but requires K % 64 == 0, 16-byte aligned rows and
+// N % 16 == 0.  Returns false if the shape is outside its envelope.
+bool tc_gemm_supported(const GemmArgs& g);
+void launch_tc_gemm(const GemmArgs& g, cudaStream_t st);
+
+// tcgen05/TMA fused EL decode for bf16 (cluster of 2 CTAs per input, split d_m).
+bool el_decode_tc_supported(int rows_per_input, int d_m);
+void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B,
+                         int rows_per_input, int n_stride, int d_m, float scale, void* ctx,
+                         cudaStream_t st);
+
+}  // namespace elattn_gpu

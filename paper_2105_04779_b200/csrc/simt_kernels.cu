@@ -1,0 +1,259 @@
+// simt_kernels.cu — the fp32 (FFMA) path of the EL decode step.
+//
+// These kernels are the product for ELATTN_DTYPE_F32 (the reference's f32
+// precision class, gated at 1e-5 relative): single-pass TF32 tensor cores
+// cannot meet that bound, so fp32 runs on CUDA cores.  They also serve bf16
+// shapes outside the tcgen05 kernels' envelope (e.g. the reference tests'
+// d_m = 8..128, d_k = 3).  All accumulation is fp32.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace elattn_gpu {
+
+// --------------------------------------------------------------------------
+// Batched GEMM, C = alpha * A . B^T + bias  (B stored [N][K]).
+// Replaces the reference's matmul triple loop (tensor.hpp:161-178) for the
+// projections Y.Wq, Q_i.Wk_i^T, C_i.Wv_i, V.Wo (attention.hpp:205-206, 286).
+// --------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) simt_gemm_kernel(GemmArgs g) {
+    constexpr int BM = 64, BN = 64, BK = 16;
+    __shared__ float As[BK][BM + 4];
+    __shared__ float Bs[BK][BN + 4];
+    const int z = blockIdx.z;
+    const T* A = static_cast<const T*>(g.A) + z * g.sAz;
+    const T* B = static_cast<const T*>(g.B) + z * g.sBz;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < g.K; k0 += BK) {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const int e = tid + l * 256;  // 0..1023
+            const int r = e / BK, c = e % BK;
+            const int gm = m0 + r, gn = n0 + r, gk = k0 + c;
+            As[c][r] = (gm < g.M && gk < g.K) ? to_f32(A[gm * g.lda + gk]) : 0.f;
+            Bs[c][r] = (gn < g.N && gk < g.K) ? to_f32(B[gn * g.ldb + gk]) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    T* C = static_cast<T*>(g.C) + z * g.sCz;
+    const float* bias = g.bias ? g.bias + z * g.sbz : nullptr;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gm = m0 + ty * 4 + i;
+        if (gm >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gn = n0 + tx * 4 + j;
+            if (gn >= g.N) continue;
+            float v = acc[i][j] * g.alpha;
+            if (bias) v += bias[gn];
+            C[gm * g.ldc + gn] = from_f32<T>(v);
+        }
+    }
+}
+
+void launch_simt_gemm(int dtype, const GemmArgs& g, cudaStream_t st) {
+    dim3 grid(unsigned(ceil_div(g.N, 64)), unsigned(ceil_div(g.M, 64)), unsigned(g.Z));
+    if (dtype == ELATTN_DTYPE_BF16)
+        simt_gemm_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(g);
+    else
+        simt_gemm_kernel<float><<<grid, 256, 0, st>>>(g);
+    ELA_CHECK_LAUNCH();
+}
+
+// --------------------------------------------------------------------------
+// Key-bias scalars s_{r,i} = Q_{r,i} . bk_i (attention.hpp:208-212).
+// --------------------------------------------------------------------------
+template <typename T>
+__global__ void key_bias_kernel(const T* Q, const float* bk, int R, int h, int d_k, float* s) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= R * h) return;
+    const int r = idx / h, i = idx % h;
+    float acc = 0.f;
+    for (int c = 0; c < d_k; ++c) acc = fmaf(to_f32(Q[(int64_t)r * h * d_k + i * d_k + c]), bk[i * d_k + c], acc);
+    s[idx] = acc;
+}
+
+void launch_key_bias_scalars(int dtype, const void* Q, const float* bk, int R, int h, int d_k,
+                             float* s, cudaStream_t st) {
+    const int total = R * h;
+    const int blocks = int(ceil_div(total, 256));
+    if (dtype == ELATTN_DTYPE_BF16)
+        key_bias_kernel<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(Q), bk, R, h, d_k, s);
+    else
+        key_bias_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(Q), bk, R, h, d_k, s);
+    ELA_CHECK_LAUNCH();
+}
+
+// --------------------------------------------------------------------------
+// SIMT fused EL decode (the core of el_attention_folded, attention.hpp:272-280):
+// one CTA owns 16 EL-Q rows of one input and streams H_b in 16-row tiles
+// through shared memory once, using each tile as both key and value:
+//   S = q'.Hᵀ  -> online softmax (exp2, running max / sum) -> O += P.H.
+// No per-head K/V and no beam-expanded H is ever formed.
+// --------------------------------------------------------------------------
+constexpr int kSimtRows = 16;  // query rows per CTA
+constexpr int kSimtTile = 16;  // H rows per tile
+
+template <typename T, int CPT>
+__global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict__ qp,
+                                                             const T* __restrict__ H,
+                                                             const int* __restrict__ n_per_input,
+                                                             int rows_per_input, int n_stride,
+                                                             int d_m, float scale_log2,
+                                                             T* __restrict__ ctx) {
+    extern __shared__ float smem[];
+    const int ldq = d_m, ldh = d_m + 1;  // +1: conflict-free column walks of the H tile
+    float* sq = smem;                                // [16][d_m]
+    float* sh = sq + kSimtRows * ldq;                // [16][d_m + 1]
+    float* sp = sh + kSimtTile * ldh;                // [16][16]
+    float* s_alpha = sp + kSimtRows * kSimtTile;     // [16]
+    float* s_l = s_alpha + kSimtRows;                // [16]
+    const int b = blockIdx.y, r0 = blockIdx.x * kSimtRows, tid = threadIdx.x;
+    const int n = n_per_input ? n_per_input[b] : n_stride;
+    const T* Hb = H + (int64_t)b * n_stride * d_m;
+    const int64_t row_base = (int64_t)b * rows_per_input + r0;
+    const int nrows = min(kSimtRows, rows_per_input - r0);
+
+    if (n < 1 || n > n_stride) {  // ragged length out of contract: loud NaN rows
+        for (int e = tid; e < nrows * d_m; e += 256)
+            ctx[(row_base + e / d_m) * d_m + e % d_m] = from_f32<T>(__int_as_float(0x7fc00000));
+        return;
+    }
+    for (int e = tid; e < kSimtRows * d_m; e += 256) {
+        const int r = e / d_m, c = e % d_m;
+        sq[r * ldq + c] = r < nrows ? to_f32(qp[(row_base + r) * d_m + c]) : 0.f;
+    }
+    float acc[kSimtRows][CPT];
+#pragma unroll
+    for (int r = 0; r < kSimtRows; ++r)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[r][c] = 0.f;
+    // Score-thread mapping: 16 threads per query row, one H row each.
+    const int sr = tid / kSimtTile, st_ = tid % kSimtTile;
+    float m_run = -INFINITY, l_run = 0.f;  // valid in threads with st_ == 0 (replicated)
+
+    for (int t0 = 0; t0 < n; t0 += kSimtTile) {
+        __syncthreads();  // previous tile fully consumed
+        for (int e = tid; e < kSimtTile * d_m; e += 256) {
+            const int r = e / d_m, c = e % d_m;
+            sh[r * ldh + c] = (t0 + r < n) ? to_f32(Hb[(int64_t)(t0 + r) * d_m + c]) : 0.f;
+        }
+        __syncthreads();
+        float s = 0.f;
+        {
+            const float* a = sq + sr * ldq;
+            const float* h = sh + st_ * ldh;
+            for (int k = 0; k < d_m; ++k) s = fmaf(a[k], h[k], s);
+        }
+        s = (t0 + st_ < n) ? s * scale_log2 : -INFINITY;
+        float mx = s;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o, 16));
+        const float m_new = fmaxf(m_run, mx);
+        const float p = exp2f(s - m_new);
+        float sum = p;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o, 16);
+        const float alpha = exp2f(m_run - m_new);  // 0 on the first tile
+        l_run = l_run * alpha + sum;
+        m_run = m_new;
+        sp[sr * kSimtTile + st_] = p;
+        if (st_ == 0) {
+            s_alpha[sr] = alpha;
+            s_l[sr] = l_run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kSimtRows; ++r) {
+            const float a = s_alpha[r];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) acc[r][c] *= a;
+        }
+#pragma unroll 4
+        for (int t = 0; t < kSimtTile; ++t) {
+            float hv[CPT];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const int col = tid + c * 256;
+                hv[c] = col < d_m ? sh[t * ldh + col] : 0.f;
+            }
+#pragma unroll
+            for (int r = 0; r < kSimtRows; ++r) {
+                const float pr = sp[r * kSimtTile + t];
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) acc[r][c] = fmaf(pr, hv[c], acc[r][c]);
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSimtRows; ++r) {
+        if (r >= nrows) break;
+        const float inv = 1.f / s_l[r];
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            const int col = tid + c * 256;
+            if (col < d_m) ctx[(row_base + r) * d_m + col] = from_f32<T>(acc[r][c] * inv);
+        }
+    }
+}
+
+template <typename T, int CPT>
+static void launch_decode_cpt(const void* qp, const void* H, const int* npi, int B, int rows,
+                              int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st) {
+    const size_t smem =
+        sizeof(float) * (size_t(kSimtRows) * d_m + size_t(kSimtTile) * (d_m + 1) +
+                         kSimtRows * kSimtTile + 2 * kSimtRows);
+    auto kern = el_decode_simt_kernel<T, CPT>;
+    ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    dim3 grid(unsigned(ceil_div(rows, kSimtRows)), unsigned(B));
+    kern<<<grid, 256, smem, st>>>(static_cast<const T*>(qp), static_cast<const T*>(H), npi, rows,
+                                  n_stride, d_m, scale_log2, static_cast<T*>(ctx));
+    ELA_CHECK_LAUNCH();
+}
+
+template <typename T>
+static void launch_decode_t(const void* qp, const void* H, const int* npi, int B, int rows,
+                            int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st) {
+    const int cpt = int(ceil_div(d_m, 256));
+    switch (cpt) {
+        case 1: return launch_decode_cpt<T, 1>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
+        case 2: return launch_decode_cpt<T, 2>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
+        case 3: return launch_decode_cpt<T, 3>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
+        case 4: return launch_decode_cpt<T, 4>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
+        case 5: return launch_decode_cpt<T, 5>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
+        case 6: return launch_decode_cpt<T, 6>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
+        default:
+            throw Status{ELATTN_ERR_UNSUPPORTED, "SIMT decode supports d_m <= 1536"};
+    }
+}
+
+void launch_el_decode_simt(int dtype, const void* qp, const void* H, const int* n_per_input,
+                           int B, int rows_per_input, int n_stride, int d_m, float scale,
+                           void* ctx, cudaStream_t st) {
+    const float scale_log2 = scale * 1.4426950408889634f;
+    if (dtype == ELATTN_DTYPE_BF16)
+        launch_decode_t<__nv_bfloat16>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m,
+                                       scale_log2, ctx, st);
+    else
+        launch_decode_t<float>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2,
+                               ctx, st);
+}
+
+}  // namespace elattn_gpu
