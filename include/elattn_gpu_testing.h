@@ -1,0 +1,34 @@
+/*
+ * elattn_gpu_testing.h — test hooks of libelattn_gpu.so (not part of the
+ * reference-facing boundary).  They expose single internal kernels so the
+ * tests can pin them in isolation against a torch fp32 reference.
+ */
+#ifndef ELATTN_GPU_TESTING_H_
+#define ELATTN_GPU_TESTING_H_
+
+#include <stdint.h>
+
+#include "elattn_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* C[z][m][n] = alpha * sum_k A[z][m][k] * B[z][n][k] + bias[z][n]   (bf16 in/out,
+ * fp32 accumulate).  kernel: 0 = SIMT, 1 = tcgen05 (UNSUPPORTED if the shape is
+ * outside its envelope). */
+int elattn_gpu_testing_gemm_bf16(const void* A, int64_t lda, int64_t sAz, const void* B, int64_t ldb,
+                                 int64_t sBz, void* C, int64_t ldc, int64_t sCz, const float* bias,
+                                 int64_t sbz, int M, int N, int K, int Z, float alpha, int kernel,
+                                 elattn_stream_t stream);
+
+/* Stage (2) with an explicit kernel choice: 0 = SIMT, 1 = tcgen05. */
+int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H, const int* n_per_input, int B,
+                                   int rows, int n, int d_m, float scale, void* ctx, int kernel,
+                                   elattn_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -361,3 +361,38 @@ int elattn_gpu_el_attention_step(elattn_gpu_params_t p, const void* Y, const voi
 }
 
 }  // extern "C"
+
+#include "elattn_gpu_testing.h"
+
+extern "C" int elattn_gpu_testing_gemm_bf16(const void* A, int64_t lda, int64_t sAz, const void* B, int64_t ldb,
+                                            int64_t sBz, void* C, int64_t ldc, int64_t sCz, const float* bias,
+                                            int64_t sbz, int M, int N, int K, int Z, float alpha, int kernel,
+                                            elattn_stream_t stream) {
+    return guarded([&] {
+        GemmArgs g{};
+        g.A = A, g.lda = lda, g.sAz = sAz, g.B = B, g.ldb = ldb, g.sBz = sBz, g.C = C, g.ldc = ldc, g.sCz = sCz;
+        g.bias = bias, g.sbz = sbz, g.M = M, g.N = N, g.K = K, g.Z = Z, g.alpha = alpha;
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        if (kernel == 1) {
+            ELA_REQUIRE(tc_gemm_supported(g), ELATTN_ERR_UNSUPPORTED, "shape outside the tcgen05 GEMM envelope");
+            launch_tc_gemm(g, st);
+        } else {
+            launch_simt_gemm(ELATTN_DTYPE_BF16, g, st);
+        }
+    });
+}
+
+extern "C" int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H, const int* n_per_input, int B,
+                                              int rows, int n, int d_m, float scale, void* ctx, int kernel,
+                                              elattn_stream_t stream) {
+    return guarded([&] {
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        if (kernel == 1) {
+            ELA_REQUIRE(el_decode_tc_supported(rows, d_m), ELATTN_ERR_UNSUPPORTED,
+                        "shape outside the tcgen05 decode envelope");
+            launch_el_decode_tc(qprime, H, n_per_input, B, rows, n, d_m, scale, ctx, st);
+        } else {
+            launch_el_decode_simt(ELATTN_DTYPE_BF16, qprime, H, n_per_input, B, rows, n, d_m, scale, ctx, st);
+        }
+    });
+}

@@ -1,0 +1,18 @@
+// tmap.h — host-side TMA tensor-map encoding (cuTensorMapEncodeTiled via the
+// runtime's driver entry point, so the library needs no -lcuda).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace elattn_gpu {
+
+// bf16 tensor map with up to 3 dims (dim 0 innermost, contiguous).
+// dims/box in elements, strides (for dims 1..rank-1) in bytes; SWIZZLE_128B,
+// out-of-bounds elements are filled with zeros.
+CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                           const uint32_t* box, bool swizzle128 = true);
+
+}  // namespace elattn_gpu

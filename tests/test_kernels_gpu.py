@@ -1,0 +1,154 @@
+"""Single-kernel numerics: each sm_100a kernel against a plain torch fp32 reference
+of the same op (the kernels' own contract, independent of the EL bookkeeping)."""
+import ctypes
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _testing_lib():
+    from paper_2105_04779_b200 import capi
+
+    L = capi.lib()
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    L.elattn_gpu_testing_gemm_bf16.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, i64, vp, i64,
+                                               i32, i32, i32, i32, ctypes.c_float, i32, vp]
+    L.elattn_gpu_testing_decode_bf16.argtypes = [vp, vp, vp, i32, i32, i32, i32, ctypes.c_float, vp, i32, vp]
+    return L, capi
+
+
+def gemm_case(kernel, M, N, K, Z, layout, seed=0, with_bias=True, alpha=1.0):
+    """layout: 'plain' (A [Z][M][K], B [Z][N][K]) or 'heads' (A columns of a [M][Z*K]
+    matrix, C rows r*Z+z of a [M*Z][N] matrix — the query-expansion pattern)."""
+    import torch
+
+    L, capi = _testing_lib()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    bf = torch.bfloat16
+    if layout == "plain":
+        A = torch.randn(Z, M, K, generator=g, device="cuda").to(bf)
+        lda, sAz = K, M * K
+        Aview = A.float()
+        Cbuf = torch.zeros(Z, M, N, device="cuda", dtype=bf)
+        ldc, sCz = N, M * N
+    else:
+        Afull = torch.randn(M, Z * K, generator=g, device="cuda").to(bf)
+        A = Afull
+        lda, sAz = Z * K, K
+        Aview = Afull.float().view(M, Z, K).permute(1, 0, 2)
+        Cbuf = torch.zeros(M * Z, N, device="cuda", dtype=bf)
+        ldc, sCz = Z * N, N
+    Bm = torch.randn(Z, N, K, generator=g, device="cuda").to(bf)
+    bias = torch.randn(Z, N, generator=g, device="cuda") if with_bias else None
+    rc = L.elattn_gpu_testing_gemm_bf16(A.data_ptr(), lda, sAz, Bm.data_ptr(), K, N * K, Cbuf.data_ptr(), ldc, sCz,
+                                        bias.data_ptr() if bias is not None else None, N, M, N, K, Z, alpha, kernel,
+                                        torch.cuda.current_stream().cuda_stream)
+    capi.check(rc)
+    torch.cuda.synchronize()
+    want = alpha * torch.einsum("zmk,znk->zmn", Aview, Bm.float())
+    if bias is not None:
+        want = want + bias[:, None, :]
+    got = Cbuf.float().view(M, Z, N).permute(1, 0, 2) if layout == "heads" else Cbuf.float()
+    return got, want
+
+
+@pytest.mark.parametrize("kernel", [1, 0])
+@pytest.mark.parametrize("M,N,K,Z,layout", [
+    (128, 128, 64, 1, "plain"),
+    (256, 1024, 1024, 1, "plain"),      # Q = Y.W_Q (BART)
+    (200, 64, 1024, 3, "plain"),        # M tail, N = d_k
+    (1280, 1024, 64, 16, "heads"),      # q'_{r,i} = Q_{r,i}.W_K,i^T (BART, B=320)
+    (77, 96, 128, 2, "heads"),
+])
+def test_gemm_vs_torch(kernel, M, N, K, Z, layout):
+    got, want = gemm_case(kernel, M, N, K, Z, layout, seed=M + N + K)
+    err = (got - want).abs().max().item() / want.abs().max().item()
+    assert err < 1e-2, err
+
+
+def decode_ref(qp, H, rows, scale, npi=None):
+    """torch fp32: C[b*rows+q] = softmax(q' H_b^T * scale) H_b."""
+    import torch
+
+    B, n, d_m = H.shape
+    q = qp.float().view(B, rows, d_m)
+    Hf = H.float()
+    S = torch.einsum("bqd,bnd->bqn", q, Hf) * scale
+    if npi is not None:
+        mask = torch.arange(n, device=H.device)[None, None, :] >= npi.view(B, 1, 1)
+        S = S.masked_fill(mask, float("-inf"))
+        Hf = Hf.masked_fill((torch.arange(n, device=H.device)[None, :, None] >= npi.view(B, 1, 1)), 0.0)
+    P = torch.softmax(S, dim=-1)
+    return torch.einsum("bqn,bnd->bqd", P, Hf).reshape(B * rows, d_m)
+
+
+@pytest.mark.parametrize("kernel", [1, 0])
+@pytest.mark.parametrize("B,rows,n,d_m", [
+    (1, 64, 32, 512), (2, 64, 1024, 1024), (3, 16, 77, 1024), (2, 48, 300, 256), (5, 64, 129, 768),
+])
+def test_decode_vs_torch(kernel, B, rows, n, d_m):
+    import torch
+
+    L, capi = _testing_lib()
+    g = torch.Generator(device="cuda").manual_seed(B * 1000 + n)
+    qp = (torch.randn(B * rows, d_m, generator=g, device="cuda") * 0.3).to(torch.bfloat16)
+    H = (torch.rand(B, n, d_m, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    ctx = torch.full((B * rows, d_m), float("nan"), device="cuda", dtype=torch.bfloat16)
+    scale = 1.0 / 8.0
+    capi.check(L.elattn_gpu_testing_decode_bf16(qp.data_ptr(), H.data_ptr(), None, B, rows, n, d_m, scale,
+                                                ctx.data_ptr(), kernel, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = decode_ref(qp, H, rows, scale)
+    err = (ctx.float() - want).abs().max().item() / want.abs().max().item()
+    assert torch.isfinite(ctx.float()).all()
+    assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("kernel", [1, 0])
+def test_decode_large_scores_rescale_path(kernel):
+    """Scores whose running max jumps by far more than 2^8 between tiles force the
+    lazy O rescale (FA4-style threshold) — must stay exact."""
+    import torch
+
+    L, capi = _testing_lib()
+    B, rows, n, d_m = 2, 64, 256, 512
+    g = torch.Generator(device="cuda").manual_seed(7)
+    qp = torch.randn(B * rows, d_m, generator=g, device="cuda").to(torch.bfloat16)
+    H = (torch.rand(B, n, d_m, generator=g, device="cuda") * 2 - 1)
+    H[:, 100:] *= 4.0  # later tiles dominate: max grows tile after tile
+    H = H.to(torch.bfloat16)
+    ctx = torch.empty(B * rows, d_m, device="cuda", dtype=torch.bfloat16)
+    scale = 0.5
+    capi.check(L.elattn_gpu_testing_decode_bf16(qp.data_ptr(), H.data_ptr(), None, B, rows, n, d_m, scale,
+                                                ctx.data_ptr(), kernel, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = decode_ref(qp, H, rows, scale)
+    err = (ctx.float() - want).abs().max().item() / want.abs().max().item()
+    assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("kernel", [1, 0])
+def test_decode_ragged_garbage_padding(kernel):
+    import torch
+
+    L, capi = _testing_lib()
+    B, rows, n, d_m = 4, 64, 200, 1024
+    g = torch.Generator(device="cuda").manual_seed(9)
+    qp = (torch.randn(B * rows, d_m, generator=g, device="cuda") * 0.3).to(torch.bfloat16)
+    H = (torch.rand(B, n, d_m, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    npi = torch.tensor([200, 1, 33, 150], dtype=torch.int32, device="cuda")
+    Hg = H.clone()
+    for b in range(B):
+        Hg[b, int(npi[b]):] = float("nan")  # padding is garbage, even NaN
+    ctx = torch.empty(B * rows, d_m, device="cuda", dtype=torch.bfloat16)
+    capi.check(L.elattn_gpu_testing_decode_bf16(qp.data_ptr(), Hg.data_ptr(), npi.data_ptr(), B, rows, n, d_m,
+                                                0.125, ctx.data_ptr(), kernel,
+                                                torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = decode_ref(qp, H, rows, 0.125, npi)
+    assert torch.isfinite(ctx.float()).all()
+    err = (ctx.float() - want).abs().max().item() / want.abs().max().item()
+    assert err < 2e-2, err
