@@ -382,6 +382,11 @@ extern "C" int elattn_gpu_testing_gemm_bf16(const void* A, int64_t lda, int64_t 
     });
 }
 
+extern "C" int elattn_gpu_testing_set_decode_trace(unsigned long long* trace) {
+    g_decode_trace = trace;
+    return ELATTN_OK;
+}
+
 extern "C" int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H, const int* n_per_input, int B,
                                               int rows, int n, int d_m, float scale, void* ctx, int kernel,
                                               elattn_stream_t stream) {

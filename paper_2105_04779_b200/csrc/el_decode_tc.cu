@@ -7,8 +7,8 @@
 //
 // Work split — one thread-block CLUSTER of 2 CTAs per input, split along d_m:
 //   CTA r owns d_m columns [r*d_m/2, (r+1)*d_m/2).  Its EL-Q half q'_r (64 x d_m/2)
-//   stays resident in smem; H_b streams through a TMA ring in tiles of 32 rows x
-//   d_m/2 (SWIZZLE_128B, 128-column "units" of 8 KB).
+//   stays resident in smem; H_b streams through a 128 KB TMA ring in tiles of
+//   32 rows x d_m/2 (SWIZZLE_128B, 128-column "units" of 8 KB).
 //   Per tile j:
 //     S_r   = q'_r . H_tile,r^T         tcgen05.mma M=64 N=32, K = d_m/2   (TMEM)
 //     S     = S_0 + S_1                  partial scores swapped through DSMEM
@@ -21,6 +21,11 @@
 //   by the softmax sums and writes C rows b*rows + q, columns of this CTA's half.
 // Both CTAs see bit-identical S (fp32 add commutes), so their softmax decisions agree.
 //
+// Pipelining: the MMA warp runs S two tiles ahead of O (issue order
+// S0 S1 | O0 S2 | O1 S3 | ...); the softmax warps take tile j+1's scores out of
+// TMEM and post them to the peer (stage A) before finishing tile j (stage B), so
+// the DSMEM round trip overlaps a whole tile of work.
+//
 // Roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (+TMEM owner),
 // warps 2..5 softmax / rescale / epilogue (TMEM lane quadrant = warp % 4).
 #include "common.cuh"
@@ -30,27 +35,33 @@
 
 namespace elattn_gpu {
 
+unsigned long long* g_decode_trace = nullptr;  // testing hook (elattn_gpu_testing_decode_trace)
+
 namespace {
 
-constexpr int kRowsQ = 64;     // EL-Q rows per input (padded)
-constexpr int kNT = 32;        // H rows per tile
-constexpr int kRing = 12;      // 8 KB units in the H ring
+constexpr int kRowsQ = 64;         // EL-Q rows per input (padded)
+constexpr int kNT = 32;            // H rows per tile
+constexpr int kRing = 16;          // 8 KB units in the H ring (128 KB)
 constexpr int kUnitBytes = 8192;   // 32 rows x 128 d_m x bf16
 constexpr int kChunkBytes = 4096;  // 32 rows x 64 d_m
 constexpr int kThreads = 192;
+constexpr int kSBuf = 4;           // S accumulators in TMEM (S runs up to 3 tiles ahead of O)
+constexpr int kSAhead = 3;
+constexpr int kL2Ahead = 6;        // tiles prefetched into L2 ahead of the smem ring
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max grows by > 2^8
 
 template <int UNITS>  // 128-column units per CTA: d_m = 256 * UNITS
 struct DecSmem {
-    static constexpr uint32_t kQBytes = UNITS * 2 * 8192;        // 64 rows x d_m/2
+    static constexpr uint32_t kQBytes = UNITS * 2 * 8192;             // 64 rows x d_m/2
     static constexpr uint32_t kRingOff = kQBytes;
     static constexpr uint32_t kPOff = kRingOff + kRing * kUnitBytes;  // 2 x (64 rows x 128 B)
     static constexpr uint32_t kRecvOff = kPOff + 2 * 8192;            // 2 x (64 x 32 fp32)
     static constexpr uint32_t kAlphaOff = kRecvOff + 2 * 8192;        // 2 x 64 fp32
     static constexpr uint32_t kLOff = kAlphaOff + 2 * 64 * 4;         // 64 fp32
     static constexpr uint32_t kBarOff = kLOff + 64 * 4;
-    static constexpr int kNumBars = 1 + 2 * kRing + 2 * 5 + 2;
+    static constexpr int kNumBars = 1 + 2 * kRing + 2 * kSBuf + 2 * 4 + 2;
     static constexpr uint32_t kTotal = kBarOff + kNumBars * 8 + 16 + 1024;
+    static_assert(kTotal <= 232448, "shared memory budget");
 };
 
 __device__ __forceinline__ uint32_t softmax_bar_or(uint32_t pred) {
@@ -78,12 +89,20 @@ template <int UNITS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     el_decode_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_h,
                         const int* __restrict__ n_per_input, int rows, int n_stride, int d_m, float scale_log2,
-                        __nv_bfloat16* __restrict__ ctx) {
+                        __nv_bfloat16* __restrict__ ctx, unsigned long long* __restrict__ trace) {
     using L = DecSmem<UNITS>;
+    // optional per-tile clock64 trace of the first cluster (testing hook)
+#define ELA_TRACE(ev, j)                                                                          \
+    do {                                                                                          \
+        if (trace != nullptr && blockIdx.x < 2 && (j) < 64)                                       \
+            trace[(blockIdx.x * 16 + (ev)) * 64 + (j)] = clock64();                               \
+    } while (0)
     constexpr int kTmemCols = 512;
-    constexpr uint32_t kTmemS = 256;  // S double buffer at columns 256..319
+    constexpr uint32_t kTmemS = 256;  // S buffers at columns 256..383
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-B alignment for SWIZZLE_128B, by offsetting the __shared__ array itself so
+    // the compiler keeps the shared address space (LDS/STS, not generic LD/ST)
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sq = smem;
     uint8_t* ring = smem + L::kRingOff;
     uint8_t* sP = smem + L::kPOff;
@@ -95,11 +114,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* unit_full = bars + 1;
     uint64_t* unit_empty = unit_full + kRing;
     uint64_t* s_full = unit_empty + kRing;
-    uint64_t* s_empty = s_full + 2;
-    uint64_t* p_full = s_empty + 2;
+    uint64_t* s_empty = s_full + kSBuf;
+    uint64_t* p_full = s_empty + kSBuf;
     uint64_t* p_empty = p_full + 2;
     uint64_t* recv_full = p_empty + 2;
-    uint64_t* o_done = recv_full + 2;
+    uint64_t* recv_free = recv_full + 2;  // arrived by the PEER's softmax warps
+    uint64_t* o_done = recv_free + 2;
     uint64_t* o_full = o_done + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
@@ -120,12 +140,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::mbar_init(&unit_full[s], 1);
                 ptx::mbar_init(&unit_empty[s], 1);
             }
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < kSBuf; ++i) {
                 ptx::mbar_init(&s_full[i], 1);
                 ptx::mbar_init(&s_empty[i], 4);
+            }
+            for (int i = 0; i < 2; ++i) {
                 ptx::mbar_init(&p_full[i], 4);
                 ptx::mbar_init(&p_empty[i], 1);
                 ptx::mbar_init(&recv_full[i], 1);
+                ptx::mbar_init(&recv_free[i], 4);
             }
             ptx::mbar_init(o_done, 1);
             ptx::mbar_init(o_full, 1);
@@ -136,7 +159,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tmem_alloc<kTmemCols>(tmem_slot);
     }
     ptx::tc_fence_before();
-    ptx::cluster_sync();  // peer barriers initialised before any st.async targets them
+    ptx::cluster_sync();  // peer barriers initialised before any st.async / remote arrive targets them
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -146,10 +169,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_arrive_expect_tx(q_full, L::kQBytes);
             for (int c = 0; c < 2 * UNITS; ++c)
                 ptx::tma_load_2d(sq + c * 8192, &tm_q, q_full, dm_off + 64 * c, b * rows, ptx::kEvictNormal);
+            // warm L2 with the first tiles; later tiles are prefetched kL2Ahead ahead
+            for (int j = 0; j < kL2Ahead && j < T; ++j)
+                for (int c = 0; c < 2 * UNITS; ++c) ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, j * kNT, b);
             for (int j = 0; j < T; ++j) {
+                if (j + kL2Ahead < T)
+                    for (int c = 0; c < 2 * UNITS; ++c)
+                        ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + kL2Ahead) * kNT, b);
                 for (int u = 0; u < UNITS; ++u) {
                     const int g = j * UNITS + u, s = g % kRing;
+                    if (u == 0) ELA_TRACE(0, j);
                     ptx::mbar_wait(&unit_empty[s], ((g / kRing) & 1) ^ 1);
+                    if (u == 0) ELA_TRACE(1, j);
                     uint8_t* dst = ring + s * kUnitBytes;
                     ptx::mbar_arrive_expect_tx(&unit_full[s], kUnitBytes);
                     const int col = dm_off + 128 * u;
@@ -163,12 +194,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ================= MMA issuer =================
         if (ptx::elect_one() && T > 0) {
-            constexpr uint32_t idS = ptx::idesc_bf16(64, kNT, 0, 0);    // S = q' . H^T
-            constexpr uint32_t idO = ptx::idesc_bf16(128, 64, 1, 0);    // O^T += H^T . P^T (A MN-major)
+            constexpr uint32_t idS = ptx::idesc_bf16(64, kNT, 0, 0);  // S = q' . H^T
+            constexpr uint32_t idO = ptx::idesc_bf16(128, 64, 1, 0);  // O^T += H^T . P^T (A MN-major)
             const uint32_t q_base = ptx::smem_u32(sq), ring_base = ptx::smem_u32(ring), p_base = ptx::smem_u32(sP);
+            auto issue_S = [&](int j) {
+                const int sb = j & (kSBuf - 1);
+                ELA_TRACE(2, j);
+                ptx::mbar_wait(&s_empty[sb], ((j / kSBuf) & 1) ^ 1);
+                ELA_TRACE(3, j);
+                ptx::tc_fence_after();
+#pragma unroll
+                for (int u = 0; u < UNITS; ++u) {
+                    const int g = j * UNITS + u, s = g % kRing;
+                    ptx::mbar_wait(&unit_full[s], (g / kRing) & 1);
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const int h = kk >> 2, k16 = kk & 3;
+                        const uint64_t a = ptx::sdesc_sw128(q_base + (2 * u + h) * 8192 + 32 * k16, 0, 1024);
+                        const uint64_t bd =
+                            ptx::sdesc_sw128(ring_base + s * kUnitBytes + h * kChunkBytes + 32 * k16, 0, 1024);
+                        ptx::mma_bf16(tmem + kTmemS + sb * kNT, a, bd, idS, (u | kk) != 0 ? 1u : 0u);  // sb: S buffer
+                    }
+                }
+                ptx::mma_commit(&s_full[sb]);
+                ELA_TRACE(4, j);
+            };
             auto issue_O = [&](int t) {
                 const int pb = t & 1;
+                ELA_TRACE(5, t);
                 ptx::mbar_wait(&p_full[pb], (t >> 1) & 1);
+                ELA_TRACE(6, t);
                 ptx::tc_fence_after();
 #pragma unroll
                 for (int m = 0; m < UNITS; ++m) {
@@ -185,132 +241,163 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::mma_commit(o_done);
             };
             ptx::mbar_wait(q_full, 0);
-            for (int j = 0; j < T; ++j) {
-                const int sb = j & 1;
-                ptx::mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
-                ptx::tc_fence_after();
-#pragma unroll
-                for (int u = 0; u < UNITS; ++u) {
-                    const int g = j * UNITS + u, s = g % kRing;
-                    ptx::mbar_wait(&unit_full[s], (g / kRing) & 1);
-                    ptx::tc_fence_after();
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const int h = kk >> 2, k16 = kk & 3;
-                        const uint64_t a = ptx::sdesc_sw128(q_base + (2 * u + h) * 8192 + 32 * k16, 0, 1024);
-                        const uint64_t bd =
-                            ptx::sdesc_sw128(ring_base + s * kUnitBytes + h * kChunkBytes + 32 * k16, 0, 1024);
-                        ptx::mma_bf16(tmem + kTmemS + sb * kNT, a, bd, idS, (u | kk) != 0 ? 1u : 0u);
-                    }
-                }
-                ptx::mma_commit(&s_full[sb]);
-                if (j >= 1) issue_O(j - 1);
+            for (int j = 0; j < kSAhead && j < T; ++j) issue_S(j);
+            for (int k = 0; k < T; ++k) {
+                issue_O(k);
+                if (k + kSAhead < T) issue_S(k + kSAhead);
             }
-            issue_O(T - 1);
             ptx::mma_commit(o_full);
         }
         __syncwarp();
     } else {
         // ================= softmax / rescale / epilogue (warps 2..5) =================
-        const uint32_t qd = warp & 3;          // TMEM lane quadrant of this warp
-        const int q = int(qd) * 16 + int(lane);  // query row owned (lanes 0..15, M=64 layout)
-        const bool owner = lane < 16;
+        // Score fragments are read with tcgen05.ld.16x256b so all 32 lanes work on
+        // the M=64 tile: thread t owns query rows ra = 16*qd + t/4 and rb = ra + 8,
+        // columns 8k + 2(t%4) + {0,1}; row reductions run over the 4-thread quad.
+        const uint32_t qd = warp & 3;  // TMEM lane quadrant of this warp
+        const int ra = int(qd) * 16 + int(lane >> 2), rb = ra + 8;
+        const int cpair = 2 * int(lane & 3);
         const uint32_t t_lane = tmem + ((qd * 32) << 16);
         const uint32_t recv_base = ptx::smem_u32(recv);
-        float m_used = -INFINITY, l_sum = 0.f;
+        const uint32_t peer_recv_full0 = ptx::mapa(ptx::smem_u32(&recv_full[0]), peer);
+        const uint32_t peer_recv_free0 = ptx::mapa(ptx::smem_u32(&recv_free[0]), peer);
+        const uint32_t peer_recv0 = ptx::mapa(recv_base, peer);
+        // recv slot of (buffer, quadrant, k, lane): float4-interleaved, conflict-free
+        auto recv_off = [&](int sb, int k) { return uint32_t((((sb * 4 + int(qd)) * 4 + k) * 32 + int(lane)) * 16); };
+        float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
         const bool zero_tail = (n_per_input != nullptr) && (T * kNT > n_b);
-        for (int j = 0; j < T; ++j) {
+
+        // Stage A(j): scores of tile j out of TMEM, partial posted to the peer.
+        auto stage_A = [&](int j, uint32_t (&sr)[16]) {
             const int sb = j & 1;
             const uint32_t par = (j >> 1) & 1;
+            const int sbuf = j & (kSBuf - 1);
             if (warp == 2 && lane == 0) ptx::mbar_arrive_expect_tx(&recv_full[sb], kRowsQ * kNT * 4);
-            ptx::mbar_wait(&s_full[sb], par);
+            if (warp == 2 && lane == 0) ELA_TRACE(7, j);
+            ptx::mbar_wait(&s_full[sbuf], (j / kSBuf) & 1);
+            if (warp == 2 && lane == 0) ELA_TRACE(8, j);
             ptx::tc_fence_after();
-            uint32_t sr[32];
-            {
-                uint32_t lo[16], hi[16];
-                ptx::tmem_ld16(t_lane + kTmemS + sb * kNT, lo);
-                ptx::tmem_ld16(t_lane + kTmemS + sb * kNT + 16, hi);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int i = 0; i < 16; ++i) sr[i] = lo[i], sr[16 + i] = hi[i];
-            }
+            ptx::tmem_ld_16x256b_x4(t_lane + kTmemS + sbuf * kNT, sr);
+            ptx::tmem_ld_wait();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
-            // swap partial scores with the peer CTA
-            if (owner) {
-                const uint32_t dst = ptx::mapa(recv_base + uint32_t((sb * kRowsQ + q) * kNT * 4), peer);
-                const uint32_t rbar = ptx::mapa(ptx::smem_u32(&recv_full[sb]), peer);
+            if (lane == 0) ptx::mbar_arrive(&s_empty[sbuf]);
+            // the peer must have consumed its recv[sb] of tile j-2
+            ptx::mbar_wait(&recv_free[sb], par ^ 1);
+            if (warp == 2 && lane == 0) ELA_TRACE(9, j);
+            const uint32_t rbar = peer_recv_full0 + sb * 8;
 #pragma unroll
-                for (int i = 0; i < kNT; i += 4)
-                    ptx::st_async_v4(dst + i * 4, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]),
-                                     __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]), rbar);
-            }
+            for (int k = 0; k < 4; ++k)
+                ptx::st_async_v4(peer_recv0 + recv_off(sb, k), __uint_as_float(sr[4 * k]),
+                                 __uint_as_float(sr[4 * k + 1]), __uint_as_float(sr[4 * k + 2]),
+                                 __uint_as_float(sr[4 * k + 3]), rbar);
+        };
+
+        uint32_t s_cur[16], s_next[16];
+        if (T > 0) stage_A(0, s_cur);
+        for (int j = 0; j < T; ++j) {
+            if (j + 1 < T) stage_A(j + 1, s_next);
+            // ---- stage B(j)
+            const int sb = j & 1;
+            const uint32_t par = (j >> 1) & 1;
+            if (warp == 2 && lane == 0) ELA_TRACE(10, j);
             ptx::mbar_wait(&recv_full[sb], par);
-            uint32_t need = 0;
-            uint32_t pk[16];
-            if (owner) {
-                const float4* pr = reinterpret_cast<const float4*>(recv + (sb * kRowsQ + q) * kNT);
-                const int nvalid = min(kNT, n_b - j * kNT);
-                float s[kNT];
+            if (warp == 2 && lane == 0) ELA_TRACE(11, j);
+            const int nvalid = min(kNT, n_b - j * kNT);
+            float s[16];
 #pragma unroll
-                for (int i = 0; i < kNT / 4; ++i) {
-                    const float4 v = pr[i];
-                    s[4 * i + 0] = (__uint_as_float(sr[4 * i + 0]) + v.x) * scale_log2;
-                    s[4 * i + 1] = (__uint_as_float(sr[4 * i + 1]) + v.y) * scale_log2;
-                    s[4 * i + 2] = (__uint_as_float(sr[4 * i + 2]) + v.z) * scale_log2;
-                    s[4 * i + 3] = (__uint_as_float(sr[4 * i + 3]) + v.w) * scale_log2;
-                }
-                float mt = -INFINITY;
-#pragma unroll
-                for (int i = 0; i < kNT; ++i) {
-                    if (i >= nvalid) s[i] = -INFINITY;
-                    mt = fmaxf(mt, s[i]);
-                }
-                float alpha = 1.f;
-                if (mt > m_used + kRescaleThreshold) {
-                    need = 1;
-                    alpha = exp2f(m_used - mt);  // 0 on the first tile
-                    l_sum *= alpha;
-                    m_used = mt;
-                }
-                s_alpha[sb * 64 + q] = alpha;
-                float acc = 0.f;
-#pragma unroll
-                for (int i = 0; i < kNT; i += 2) {
-                    const float p0 = exp2f(s[i] - m_used), p1 = exp2f(s[i + 1] - m_used);
-                    acc += p0 + p1;
-                    pk[i / 2] = pack_bf16x2(p0, p1);
-                }
-                l_sum += acc;
+            for (int k = 0; k < 4; ++k) {
+                const float4 v = ptx::lds_f4(recv_base + recv_off(sb, k));
+                s[4 * k + 0] = (__uint_as_float(s_cur[4 * k + 0]) + v.x) * scale_log2;
+                s[4 * k + 1] = (__uint_as_float(s_cur[4 * k + 1]) + v.y) * scale_log2;
+                s[4 * k + 2] = (__uint_as_float(s_cur[4 * k + 2]) + v.z) * scale_log2;
+                s[4 * k + 3] = (__uint_as_float(s_cur[4 * k + 3]) + v.w) * scale_log2;
             }
-            // P[sb] is free once O(j-2) has consumed it
-            ptx::mbar_wait(&p_empty[sb], par ^ 1);
-            if (owner) {
-                uint8_t* prow = sP + sb * 8192 + q * 128;
+            if (nvalid < kNT) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    *reinterpret_cast<uint4*>(prow + ((c ^ (q & 7)) << 4)) =
-                        make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (8 * k + cpair + (i & 1) >= nvalid) s[4 * k + i] = -INFINITY;
+            }
+            float xa = fmaxf(fmaxf(s[0], s[1]), fmaxf(s[4], s[5]));
+            float xb = fmaxf(fmaxf(s[2], s[3]), fmaxf(s[6], s[7]));
+            xa = fmaxf(xa, fmaxf(fmaxf(s[8], s[9]), fmaxf(s[12], s[13])));
+            xb = fmaxf(xb, fmaxf(fmaxf(s[10], s[11]), fmaxf(s[14], s[15])));
+            xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 1));
+            xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 1));
+            xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
+            xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 2));
+            // every value read from recv[sb] has reached a register (the shuffles above
+            // consumed them), so the peer may refill the buffer
+            if (lane == 0) ptx::mbar_arrive_remote(peer_recv_free0 + sb * 8);
+            uint32_t need = 0;
+            float alpha_a = 1.f, alpha_b = 1.f;
+            if (xa > m_a + kRescaleThreshold) {  // identical decision in all 4 quad threads
+                need = 1;
+                alpha_a = ptx::ex2(m_a - xa);  // 0 on the first tile
+                l_a *= alpha_a;
+                m_a = xa;
+            }
+            if (xb > m_b + kRescaleThreshold) {
+                need = 1;
+                alpha_b = ptx::ex2(m_b - xb);
+                l_b *= alpha_b;
+                m_b = xb;
+            }
+            if ((lane & 3) == 0) {
+                s_alpha[sb * 64 + ra] = alpha_a;
+                s_alpha[sb * 64 + rb] = alpha_b;
+            }
+            uint32_t pa[4], pb[4];
+            float sa = 0.f, sbs = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float p0 = ptx::ex2(s[4 * k] - m_a), p1 = ptx::ex2(s[4 * k + 1] - m_a);
+                const float p2 = ptx::ex2(s[4 * k + 2] - m_b), p3 = ptx::ex2(s[4 * k + 3] - m_b);
+                sa += p0 + p1;
+                sbs += p2 + p3;
+                pa[k] = pack_bf16x2(p0, p1);
+                pb[k] = pack_bf16x2(p2, p3);
+            }
+            sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+            sbs += __shfl_xor_sync(0xffffffffu, sbs, 1);
+            sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+            sbs += __shfl_xor_sync(0xffffffffu, sbs, 2);
+            l_a += sa;
+            l_b += sbs;
+            // P[sb] is free once O(j-2) has consumed it
+            if (warp == 2 && lane == 0) ELA_TRACE(12, j);
+            ptx::mbar_wait(&p_empty[sb], par ^ 1);
+            if (warp == 2 && lane == 0) ELA_TRACE(13, j);
+            {
+                uint8_t* P = sP + sb * 8192;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    *reinterpret_cast<uint32_t*>(P + ra * 128 + ((k ^ (ra & 7)) << 4) + 2 * cpair) = pa[k];
+                    *reinterpret_cast<uint32_t*>(P + rb * 128 + ((k ^ (rb & 7)) << 4) + 2 * cpair) = pb[k];
+                }
             }
             if (zero_tail && j == T - 1) {
                 // rows n_b.. of the last tile are in-bounds padding of H_b: zero them
                 // before they meet P = 0 in the MMA (0 * NaN would poison O).
                 const int r0 = n_b - j * kNT;
                 const int tid = int(threadIdx.x) - 64;
-                for (int idx = tid; idx < UNITS * 2 * (kNT - r0) * 8; idx += 128) {
-                    const int per_chunk = (kNT - r0) * 8;
+                const int per_chunk = (kNT - r0) * 8;
+                for (int idx = tid; idx < UNITS * 2 * per_chunk; idx += 128) {
                     const int ch = idx / per_chunk, rem = idx % per_chunk;
                     const int r = r0 + rem / 8, c16 = rem % 8;
-                    const int s = (j * UNITS + ch / 2) % kRing;
-                    *reinterpret_cast<uint4*>(ring + s * kUnitBytes + (ch & 1) * kChunkBytes + r * 128 + c16 * 16) =
+                    const int sl = (j * UNITS + ch / 2) % kRing;
+                    *reinterpret_cast<uint4*>(ring + sl * kUnitBytes + (ch & 1) * kChunkBytes + r * 128 + c16 * 16) =
                         make_uint4(0, 0, 0, 0);
                 }
             }
             const uint32_t any = softmax_bar_or(need);
+            // consume o_done phases in order (one per tile) so the parity wait is exact;
+            // O(j-1) was issued a full stage ago, so this rarely blocks
+            if (j > 0) ptx::mbar_wait(o_done, (j - 1) & 1);
             if (any && j > 0) {
-                // lazy rescale of the running O^T columns: wait for O(j-1), then O *= alpha
-                ptx::mbar_wait(o_done, (j - 1) & 1);
+                // lazy rescale of the running O^T columns (O(j-1) complete): O *= alpha
                 ptx::tc_fence_after();
 #pragma unroll 1
                 for (int m = 0; m < UNITS; ++m) {
@@ -331,17 +418,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
+            if (warp == 2 && lane == 0) ELA_TRACE(14, j);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) s_cur[i] = s_next[i];
         }
-        // ---- epilogue: C[b*rows + q][dm_off + d] = O^T[d][q] / l_q
-        if (owner) s_l[q] = l_sum;
-        softmax_bar_sync();
+
+        // ---- epilogue: C[b*rows + q][dm_off + d] = O^T[d][q] / l_q, staged through
+        // smem (two 16 KB [64 q][128 d] bf16 buffers in the drained ring) so the
+        // global stores are coalesced 16-byte vectors.
+        if ((lane & 3) == 0) {
+            s_l[ra] = 1.f / l_a;
+            s_l[rb] = 1.f / l_b;
+        }
         if (T > 0) {
             ptx::mbar_wait(o_full, 0);
             ptx::tc_fence_after();
         }
+        softmax_bar_sync();
         const int d_local = int(qd) * 32 + int(lane);
+        const int tid = int(threadIdx.x) - 64;
         for (int m = 0; m < UNITS; ++m) {
-            const int d = dm_off + m * 128 + d_local;
+            __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(ring + (m & 1) * 16384);
 #pragma unroll
             for (int c0 = 0; c0 < 64; c0 += 16) {
                 uint32_t r[16];
@@ -352,11 +449,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int qq = c0 + i;
-                    if (qq < rows) {
-                        const float v = T > 0 ? __uint_as_float(r[i]) / s_l[qq] : __int_as_float(0x7fc00000);
-                        ctx[(int64_t(b) * rows + qq) * d_m + d] = __float2bfloat16_rn(v);
-                    }
+                    const float v = T > 0 ? __uint_as_float(r[i]) * s_l[qq] : __int_as_float(0x7fc00000);
+                    stage[qq * 128 + d_local] = __float2bfloat16_rn(v);
                 }
+            }
+            softmax_bar_sync();
+            // 64 rows x 256 B = 1024 16-byte vectors, 8 per thread
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                const int idx = tid + v * 128;
+                const int qq = idx >> 4, c16 = idx & 15;
+                if (qq < rows)
+                    *reinterpret_cast<uint4*>(ctx + (int64_t(b) * rows + qq) * d_m + dm_off + m * 128 + c16 * 8) =
+                        *reinterpret_cast<const uint4*>(stage + qq * 128 + c16 * 8);
             }
         }
     }
@@ -386,7 +491,7 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     constexpr uint32_t smem = DecSmem<UNITS>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<dim3(2 * B), kThreads, smem, st>>>(tq, th, npi, rows, n_stride, d_m, scale_log2,
-                                               static_cast<__nv_bfloat16*>(ctx));
+                                               static_cast<__nv_bfloat16*>(ctx), g_decode_trace);
     ELA_CHECK_LAUNCH();
 }
 
@@ -400,8 +505,9 @@ void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, 
                          int n_stride, int d_m, float scale, void* ctx, cudaStream_t st) {
     ELA_REQUIRE(el_decode_tc_supported(rows_per_input, d_m), ELATTN_ERR_UNSUPPORTED,
                 "tcgen05 decode: rows <= 64 and d_m in {256, 512, 768, 1024}");
-    ELA_REQUIRE((reinterpret_cast<uintptr_t>(qp) & 15) == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0,
-                ELATTN_ERR_PARAM, "tcgen05 decode: q' and H must be 16-byte aligned");
+    ELA_REQUIRE((reinterpret_cast<uintptr_t>(qp) & 15) == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(ctx) & 15) == 0,
+                ELATTN_ERR_PARAM, "tcgen05 decode: q', H and C must be 16-byte aligned");
     const float scale_log2 = scale * 1.4426950408889634f;
     switch (d_m / 256) {
         case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st);
