@@ -27,7 +27,7 @@ int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H, const int*
                                    int rows, int n, int d_m, float scale, void* ctx, int kernel,
                                    elattn_stream_t stream);
 
-/* Device buffer (>= 2*16*64 u64) that receives clock64 stamps from the first
+/* Device buffer (>= 2*24*64 u64) that receives clock64 stamps from the first
  * cluster of every following tcgen05 decode launch; NULL disables tracing. */
 int elattn_gpu_testing_set_decode_trace(unsigned long long* trace);
 

@@ -21,17 +21,21 @@
 //   by the softmax sums and writes C rows b*rows + q, columns of this CTA's half.
 // Both CTAs see bit-identical S (fp32 add commutes), so their softmax decisions agree.
 //
-// Pipelining: the MMA warp runs S two tiles ahead of O (issue order
-// S0 S1 | O0 S2 | O1 S3 | ...); the softmax warps take tile j+1's scores out of
-// TMEM and post them to the peer (stage A) before finishing tile j (stage B), so
-// the DSMEM round trip overlaps a whole tile of work.
+// Pipelining: the MMA warp runs S three tiles ahead of O (issue order
+// S0 S1 S2 | O0 S3 | O1 S4 | ...).  Four "exchange" warps take each S tile out of
+// TMEM and post it to the peer as soon as it is computed, so the DSMEM transfer
+// overlaps whole tiles of softmax work and the softmax warps never fence behind
+// their own in-flight remote stores.
 //
-// Roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (+TMEM owner),
-// warps 2..5 softmax / rescale / epilogue (TMEM lane quadrant = warp % 4).
+// Roles (384 threads): warp 0 TMA producer, warps 1 and 11 S-MMA issuers (even /
+// odd tiles; warp 1 owns TMEM), warps 2..5 softmax / rescale / epilogue, warps 6..9
+// score exchange (TMEM lane quadrant = warp % 4 for both groups), warp 10 O-MMA issuer.
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx_sm100.cuh"
 #include "tmap.h"
+
+#include <cstdlib>
 
 namespace elattn_gpu {
 
@@ -41,27 +45,45 @@ namespace {
 
 constexpr int kRowsQ = 64;         // EL-Q rows per input (padded)
 constexpr int kNT = 32;            // H rows per tile
-constexpr int kRing = 16;          // 8 KB units in the H ring (128 KB)
 constexpr int kUnitBytes = 8192;   // 32 rows x 128 d_m x bf16
 constexpr int kChunkBytes = 4096;  // 32 rows x 64 d_m
-constexpr int kThreads = 192;
+constexpr int kThreads = 384;
 constexpr int kSBuf = 4;           // S accumulators in TMEM (S runs up to 3 tiles ahead of O)
-constexpr int kSAhead = 3;
-constexpr int kL2Ahead = 6;        // tiles prefetched into L2 ahead of the smem ring
+// Tuning knobs (runtime so they can be swept; defaults chosen by tools/sweep_decode.py):
+//   s_ahead  — how many tiles S may run ahead of O (<= kSBuf);
+//   l2_ahead — how many tiles ahead of the smem ring H is prefetched into L2 (0 = off).
+struct DecodeTuning {
+    int s_ahead = 4;
+    int l2_ahead = 0;
+};
+DecodeTuning g_tuning;
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max grows by > 2^8
 
-template <int UNITS>  // 128-column units per CTA: d_m = 256 * UNITS
-struct DecSmem {
-    static constexpr uint32_t kQBytes = UNITS * 2 * 8192;             // 64 rows x d_m/2
+// TMEM columns (512): O^T [0, 64*UNITS) | S buffers [64*UNITS, +128) | q' units held in
+// TMEM as the M=64 A operand [.., 512).  q' units that do not fit stay in smem.
+template <int UNITS>
+struct DecLayout {
+    static constexpr int kTmemO = 0;
+    static constexpr int kTmemS = 64 * UNITS;
+    static constexpr int kTmemQ = kTmemS + 32 * kSBuf;
+    static constexpr int kQTmemUnits = (512 - kTmemQ) / 64 < UNITS ? (512 - kTmemQ) / 64 : UNITS;
+    static constexpr int kQSmemUnits = UNITS - kQTmemUnits;
+    // shared memory
+    static constexpr uint32_t kQBytes = kQSmemUnits * 2 * 8192;  // 64 rows x 128 d_m per unit
+    static constexpr uint32_t kFixed = kQBytes + 2 * 8192 /*P*/ + 2 * 8192 /*recv*/ + 2 * 64 * 4 + 64 * 4 + 1024;
+    static constexpr int kRingMax = 24;
+    static constexpr int kRingFit = int((232448u - kFixed - 512u) / 8192u);
+    static constexpr int kRing = kRingFit < kRingMax ? kRingFit : kRingMax;  // 8 KB units in the H ring
     static constexpr uint32_t kRingOff = kQBytes;
     static constexpr uint32_t kPOff = kRingOff + kRing * kUnitBytes;  // 2 x (64 rows x 128 B)
     static constexpr uint32_t kRecvOff = kPOff + 2 * 8192;            // 2 x (64 x 32 fp32)
     static constexpr uint32_t kAlphaOff = kRecvOff + 2 * 8192;        // 2 x 64 fp32
     static constexpr uint32_t kLOff = kAlphaOff + 2 * 64 * 4;         // 64 fp32
     static constexpr uint32_t kBarOff = kLOff + 64 * 4;
-    static constexpr int kNumBars = 1 + 2 * kRing + 2 * kSBuf + 2 * 4 + 2;
+    static constexpr int kNumBars = 2 + 2 * kRing + 2 * kSBuf + 2 * 4 + 2;
     static constexpr uint32_t kTotal = kBarOff + kNumBars * 8 + 16 + 1024;
     static_assert(kTotal <= 232448, "shared memory budget");
+    static_assert(kQTmemUnits >= 1, "at least one q' unit in TMEM");
 };
 
 __device__ __forceinline__ uint32_t softmax_bar_or(uint32_t pred) {
@@ -80,6 +102,12 @@ __device__ __forceinline__ uint32_t softmax_bar_or(uint32_t pred) {
 }
 __device__ __forceinline__ void softmax_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+// byte offset of (buffer, quadrant, k, lane) in the partial-score exchange buffer:
+// float4-interleaved so both the remote writes and the local reads are conflict-free
+__device__ __forceinline__ uint32_t recv_slot(int sb, uint32_t qd, int k, uint32_t lane) {
+    return uint32_t((((sb * 4 + int(qd)) * 4 + k) * 32 + int(lane)) * 16);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&v);
@@ -88,17 +116,20 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 template <int UNITS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     el_decode_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_h,
+                        const __nv_bfloat16* __restrict__ qp_rows, int total_rows,
                         const int* __restrict__ n_per_input, int rows, int n_stride, int d_m, float scale_log2,
-                        __nv_bfloat16* __restrict__ ctx, unsigned long long* __restrict__ trace) {
-    using L = DecSmem<UNITS>;
+                        __nv_bfloat16* __restrict__ ctx, unsigned long long* __restrict__ trace,
+                        DecodeTuning tune) {
+    using L = DecLayout<UNITS>;
+    constexpr int kRing = L::kRing;
     // optional per-tile clock64 trace of the first cluster (testing hook)
 #define ELA_TRACE(ev, j)                                                                          \
     do {                                                                                          \
         if (trace != nullptr && blockIdx.x < 2 && (j) < 64)                                       \
-            trace[(blockIdx.x * 16 + (ev)) * 64 + (j)] = clock64();                               \
+            trace[(blockIdx.x * 24 + (ev)) * 64 + (j)] = clock64();                               \
     } while (0)
     constexpr int kTmemCols = 512;
-    constexpr uint32_t kTmemS = 256;  // S buffers at columns 256..383
+    constexpr uint32_t kTmemS = L::kTmemS;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B, by offsetting the __shared__ array itself so
     // the compiler keeps the shared address space (LDS/STS, not generic LD/ST)
@@ -111,7 +142,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float* s_l = reinterpret_cast<float*>(smem + L::kLOff);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
     uint64_t* q_full = bars;
-    uint64_t* unit_full = bars + 1;
+    uint64_t* q_tmem_full = bars + 1;  // q' units written into TMEM by the softmax warps
+    uint64_t* unit_full = bars + 2;
     uint64_t* unit_empty = unit_full + kRing;
     uint64_t* s_full = unit_empty + kRing;
     uint64_t* s_empty = s_full + kSBuf;
@@ -130,19 +162,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int n_b = n_per_input ? n_per_input[b] : n_stride;
     const bool valid = n_b >= 1 && n_b <= n_stride;
     const int T = valid ? (n_b + kNT - 1) / kNT : 0;
+    // q' rows of this input that exist in memory (the 64-row box pads with the next
+    // input's rows, or zeros past the end, exactly like the TMA path)
+    const int rows_valid_for_tmem = min(kRowsQ, total_rows - b * rows);
 
     if (warp == 0) {
         if (ptx::elect_one()) {
             ptx::prefetch_tmap(&tm_q);
             ptx::prefetch_tmap(&tm_h);
             ptx::mbar_init(q_full, 1);
+            ptx::mbar_init(q_tmem_full, 4);
             for (int s = 0; s < kRing; ++s) {
                 ptx::mbar_init(&unit_full[s], 1);
                 ptx::mbar_init(&unit_empty[s], 1);
             }
             for (int i = 0; i < kSBuf; ++i) {
                 ptx::mbar_init(&s_full[i], 1);
-                ptx::mbar_init(&s_empty[i], 4);
+                ptx::mbar_init(&s_empty[i], 5);  // 4 exchange warps + the O issuer
             }
             for (int i = 0; i < 2; ++i) {
                 ptx::mbar_init(&p_full[i], 4);
@@ -153,6 +189,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_init(o_done, 1);
             ptx::mbar_init(o_full, 1);
             ptx::fence_mbar_init();
+            // expected bytes of the peer's partial scores for tiles 0 and 1; later
+            // tiles are posted by the softmax warps once the previous phase is consumed
+            ptx::mbar_arrive_expect_tx(&recv_full[0], kRowsQ * kNT * 4);
+            ptx::mbar_arrive_expect_tx(&recv_full[1], kRowsQ * kNT * 4);
         }
         __syncwarp();
     } else if (warp == 1) {
@@ -166,16 +206,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ================= TMA producer =================
         if (ptx::elect_one() && T > 0) {
-            ptx::mbar_arrive_expect_tx(q_full, L::kQBytes);
-            for (int c = 0; c < 2 * UNITS; ++c)
-                ptx::tma_load_2d(sq + c * 8192, &tm_q, q_full, dm_off + 64 * c, b * rows, ptx::kEvictNormal);
-            // warm L2 with the first tiles; later tiles are prefetched kL2Ahead ahead
-            for (int j = 0; j < kL2Ahead && j < T; ++j)
+            if (L::kQSmemUnits > 0) {
+                ptx::mbar_arrive_expect_tx(q_full, L::kQBytes);
+                for (int c = 0; c < 2 * L::kQSmemUnits; ++c)
+                    ptx::tma_load_2d(sq + c * 8192, &tm_q, q_full, dm_off + 128 * L::kQTmemUnits + 64 * c, b * rows,
+                                     ptx::kEvictNormal);
+            }
+            // optionally warm L2 with the first tiles; later tiles are prefetched l2_ahead ahead
+            for (int j = 0; j < tune.l2_ahead && j < T; ++j)
                 for (int c = 0; c < 2 * UNITS; ++c) ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, j * kNT, b);
             for (int j = 0; j < T; ++j) {
-                if (j + kL2Ahead < T)
+                if (tune.l2_ahead > 0 && j + tune.l2_ahead < T)
                     for (int c = 0; c < 2 * UNITS; ++c)
-                        ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + kL2Ahead) * kNT, b);
+                        ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, b);
                 for (int u = 0; u < UNITS; ++u) {
                     const int g = j * UNITS + u, s = g % kRing;
                     if (u == 0) ELA_TRACE(0, j);
@@ -191,64 +234,128 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp == 1) {
-        // ================= MMA issuer =================
-        if (ptx::elect_one() && T > 0) {
+    } else if (warp == 1 || warp == 11) {
+        // ================= S issuers (warp 1: even tiles, warp 11: odd tiles) =================
+        // One thread can issue only ~1 tcgen05.mma per 56 cycles (measured by
+        // tools/probes/mma_rate_probe.cu), and an S tile is 32 small MMAs, so two warps
+        // issue alternate tiles.  The whole warp runs the loop (slot/phase arithmetic
+        // stays warp-uniform, on the uniform datapath next to UTCHMMA); lane 0 issues.
+        if (T > 0) {
             constexpr uint32_t idS = ptx::idesc_bf16(64, kNT, 0, 0);  // S = q' . H^T
-            constexpr uint32_t idO = ptx::idesc_bf16(128, 64, 1, 0);  // O^T += H^T . P^T (A MN-major)
-            const uint32_t q_base = ptx::smem_u32(sq), ring_base = ptx::smem_u32(ring), p_base = ptx::smem_u32(sP);
-            auto issue_S = [&](int j) {
+            const uint64_t dRing = ptx::sdesc_sw128(ptx::smem_u32(ring), 0, 1024);
+            const uint64_t dQ = ptx::sdesc_sw128(ptx::smem_u32(sq), 0, 1024);
+            if (L::kQSmemUnits > 0) ptx::mbar_wait(q_full, 0);
+            ptx::mbar_wait(q_tmem_full, 0);
+            for (int j = (warp == 1 ? 0 : 1); j < T; j += 2) {
                 const int sb = j & (kSBuf - 1);
-                ELA_TRACE(2, j);
+                const uint32_t d = tmem + kTmemS + sb * kNT;
+                if (lane == 0) ELA_TRACE(2, j);
+                // buffer j%4 is free once the exchange warps and (relayed by the O issuer)
+                // the softmax have consumed S(j-4)
                 ptx::mbar_wait(&s_empty[sb], ((j / kSBuf) & 1) ^ 1);
-                ELA_TRACE(3, j);
-                ptx::tc_fence_after();
+                if (tune.s_ahead < kSBuf && j >= tune.s_ahead) {
+                    const int jj = j - tune.s_ahead;  // bound the lookahead: O(j - s_ahead) issued
+                    ptx::mbar_wait(&s_empty[jj & (kSBuf - 1)], (jj / kSBuf) & 1);
+                }
 #pragma unroll
                 for (int u = 0; u < UNITS; ++u) {
-                    const int g = j * UNITS + u, s = g % kRing;
-                    ptx::mbar_wait(&unit_full[s], (g / kRing) & 1);
+                    const int g = j * UNITS + u, slot = g % kRing;
+                    if (lane == 0 && u == 0) ELA_TRACE(16, j);
+                    ptx::mbar_wait(&unit_full[slot], (g / kRing) & 1);
+                    if (lane == 0 && u == 0) ELA_TRACE(17, j);
+                    if (lane == 0 && u == UNITS - 1) ELA_TRACE(18, j);
                     ptx::tc_fence_after();
+                    const uint64_t dB = dRing + uint64_t((slot * kUnitBytes) >> 4);
+                    if (lane == 0) {
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const int h = kk >> 2, k16 = kk & 3;
-                        const uint64_t a = ptx::sdesc_sw128(q_base + (2 * u + h) * 8192 + 32 * k16, 0, 1024);
-                        const uint64_t bd =
-                            ptx::sdesc_sw128(ring_base + s * kUnitBytes + h * kChunkBytes + 32 * k16, 0, 1024);
-                        ptx::mma_bf16(tmem + kTmemS + sb * kNT, a, bd, idS, (u | kk) != 0 ? 1u : 0u);  // sb: S buffer
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const int h = kk >> 2, k16 = kk & 3;
+                            const uint64_t bd = dB + uint64_t((h * kChunkBytes + 32 * k16) >> 4);
+                            const uint32_t acc = (u | kk) != 0 ? 1u : 0u;
+                            if (u < L::kQTmemUnits) {  // A (q') from TMEM: no smem operand traffic
+                                ptx::mma_bf16_tmem_a(d, tmem + L::kTmemQ + u * 64 + kk * 8, bd, idS, acc);
+                            } else {
+                                const uint64_t a =
+                                    dQ + uint64_t(((2 * (u - L::kQTmemUnits) + h) * 8192 + 32 * k16) >> 4);
+                                ptx::mma_bf16(d, a, bd, idS, acc);
+                            }
+                        }
                     }
+                    __syncwarp();
                 }
-                ptx::mma_commit(&s_full[sb]);
-                ELA_TRACE(4, j);
-            };
-            auto issue_O = [&](int t) {
-                const int pb = t & 1;
-                ELA_TRACE(5, t);
-                ptx::mbar_wait(&p_full[pb], (t >> 1) & 1);
-                ELA_TRACE(6, t);
-                ptx::tc_fence_after();
-#pragma unroll
-                for (int m = 0; m < UNITS; ++m) {
-                    const int s = (t * UNITS + m) % kRing;
-#pragma unroll
-                    for (int kk = 0; kk < kNT / 16; ++kk) {
-                        const uint64_t a = ptx::sdesc_sw128(ring_base + s * kUnitBytes + kk * 2048, kChunkBytes, 1024);
-                        const uint64_t bd = ptx::sdesc_sw128(p_base + pb * 8192 + 32 * kk, 0, 1024);
-                        ptx::mma_bf16(tmem + m * 64, a, bd, idO, (t > 0 || kk > 0) ? 1u : 0u);
-                    }
-                    ptx::mma_commit(&unit_empty[s]);
+                if (lane == 0) {
+                    ELA_TRACE(19, j);
+                    ptx::mma_commit(&s_full[sb]);
+                    ELA_TRACE(3, j);
                 }
-                ptx::mma_commit(&p_empty[pb]);
-                ptx::mma_commit(o_done);
-            };
-            ptx::mbar_wait(q_full, 0);
-            for (int j = 0; j < kSAhead && j < T; ++j) issue_S(j);
-            for (int k = 0; k < T; ++k) {
-                issue_O(k);
-                if (k + kSAhead < T) issue_S(k + kSAhead);
+                __syncwarp();
             }
-            ptx::mma_commit(o_full);
         }
-        __syncwarp();
+    } else if (warp == 10) {
+        // ================= O issuer =================
+        // A second issuer warp, so O(k) (the softmax critical path) never queues behind
+        // S(k+3) waiting for TMA data.  Whole warp loops, lane 0 issues and commits.
+        if (T > 0) {
+            constexpr uint32_t idO = ptx::idesc_bf16(128, 64, 1, 0);  // O^T += H^T . P^T (A MN-major)
+            const uint64_t dRingMN = ptx::sdesc_sw128(ptx::smem_u32(ring), kChunkBytes, 1024);
+            const uint64_t dP = ptx::sdesc_sw128(ptx::smem_u32(sP), 0, 1024);
+            for (int t = 0; t < T; ++t) {
+                const int pb = t & 1;
+                if (lane == 0) ELA_TRACE(4, t);
+                ptx::mbar_wait(&p_full[pb], (t >> 1) & 1);
+                if (lane == 0) ELA_TRACE(5, t);
+                ptx::tc_fence_after();
+                if (lane == 0) {
+#pragma unroll
+                    for (int m = 0; m < UNITS; ++m) {
+                        const int slot = (t * UNITS + m) % kRing;
+#pragma unroll
+                        for (int kk = 0; kk < kNT / 16; ++kk) {
+                            const uint64_t a = dRingMN + uint64_t((slot * kUnitBytes + kk * 2048) >> 4);
+                            const uint64_t bd = dP + uint64_t((pb * 8192 + 32 * kk) >> 4);
+                            ptx::mma_bf16(tmem + m * 64, a, bd, idO, (t > 0 || kk > 0) ? 1u : 0u);
+                        }
+                        ptx::mma_commit(&unit_empty[slot]);
+                    }
+                    ptx::mma_commit(&p_empty[pb]);
+                    ptx::mma_commit(o_done);
+                    // P(t) observed => the softmax has consumed S(t): release its buffer
+                    ptx::mbar_arrive(&s_empty[t & (kSBuf - 1)]);
+                }
+                __syncwarp();
+            }
+            if (lane == 0) ptx::mma_commit(o_full);
+            __syncwarp();
+        }
+    } else if (warp >= 6 && warp <= 9) {
+        // ================= score exchange (warps 6..9) =================
+        const uint32_t qd = warp & 3;
+        const uint32_t t_lane = tmem + ((qd * 32) << 16);
+        const uint32_t peer_recv_full0 = ptx::mapa(ptx::smem_u32(&recv_full[0]), peer);
+        const uint32_t peer_recv0 = ptx::mapa(ptx::smem_u32(recv), peer);
+        for (int j = 0; j < T; ++j) {
+            const int sb = j & 1, sbuf = j & (kSBuf - 1);
+            if (warp == 6 && lane == 0) ELA_TRACE(6, j);
+            ptx::mbar_wait(&s_full[sbuf], (j / kSBuf) & 1);
+            if (warp == 6 && lane == 0) ELA_TRACE(7, j);
+            ptx::tc_fence_after();
+            uint32_t sr[16];
+            ptx::tmem_ld_16x256b_x4(t_lane + kTmemS + sbuf * kNT, sr);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&s_empty[sbuf]);
+            // the peer must have consumed its recv[sb] of tile j-2
+            ptx::mbar_wait(&recv_free[sb], ((j >> 1) & 1) ^ 1);
+            if (warp == 6 && lane == 0) ELA_TRACE(8, j);
+            const uint32_t rbar = peer_recv_full0 + sb * 8;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                ptx::st_async_v4(peer_recv0 + recv_slot(sb, qd, k, lane), __uint_as_float(sr[4 * k]),
+                                 __uint_as_float(sr[4 * k + 1]), __uint_as_float(sr[4 * k + 2]),
+                                 __uint_as_float(sr[4 * k + 3]), rbar);
+            if (warp == 6 && lane == 0) ELA_TRACE(9, j);
+        }
     } else {
         // ================= softmax / rescale / epilogue (warps 2..5) =================
         // Score fragments are read with tcgen05.ld.16x256b so all 32 lanes work on
@@ -259,66 +366,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int cpair = 2 * int(lane & 3);
         const uint32_t t_lane = tmem + ((qd * 32) << 16);
         const uint32_t recv_base = ptx::smem_u32(recv);
-        const uint32_t peer_recv_full0 = ptx::mapa(ptx::smem_u32(&recv_full[0]), peer);
         const uint32_t peer_recv_free0 = ptx::mapa(ptx::smem_u32(&recv_free[0]), peer);
-        const uint32_t peer_recv0 = ptx::mapa(recv_base, peer);
-        // recv slot of (buffer, quadrant, k, lane): float4-interleaved, conflict-free
-        auto recv_off = [&](int sb, int k) { return uint32_t((((sb * 4 + int(qd)) * 4 + k) * 32 + int(lane)) * 16); };
-        float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+        const float neg_inf = -INFINITY;
+        float m_a = neg_inf, m_b = neg_inf, l_a = 0.f, l_b = 0.f;  // running max (raw score units), sums
         const bool zero_tail = (n_per_input != nullptr) && (T * kNT > n_b);
-
-        // Stage A(j): scores of tile j out of TMEM, partial posted to the peer.
-        auto stage_A = [&](int j, uint32_t (&sr)[16]) {
-            const int sb = j & 1;
-            const uint32_t par = (j >> 1) & 1;
-            const int sbuf = j & (kSBuf - 1);
-            if (warp == 2 && lane == 0) ptx::mbar_arrive_expect_tx(&recv_full[sb], kRowsQ * kNT * 4);
-            if (warp == 2 && lane == 0) ELA_TRACE(7, j);
-            ptx::mbar_wait(&s_full[sbuf], (j / kSBuf) & 1);
-            if (warp == 2 && lane == 0) ELA_TRACE(8, j);
-            ptx::tc_fence_after();
-            ptx::tmem_ld_16x256b_x4(t_lane + kTmemS + sbuf * kNT, sr);
-            ptx::tmem_ld_wait();
+        if (T > 0) {
+            // q' units [0, kQTmemUnits) of this CTA's d_m half -> TMEM, M=64 A layout:
+            // row 16*qd + t (t < 16) in lane 32*qd + t, bf16 pairs packed per column.
+            const uint4* qrow = reinterpret_cast<const uint4*>(
+                qp_rows + (int64_t(b) * rows + int(qd) * 16 + int(lane)) * d_m + dm_off);
+            const bool row_ok = lane < 16 && int(qd) * 16 + int(lane) < rows_valid_for_tmem;
+            for (int c0 = 0; c0 < L::kQTmemUnits * 64; c0 += 16) {  // 16 columns = 32 bf16 per store
+                uint32_t v[16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint4 x = row_ok ? __ldg(qrow + c0 / 4 + i) : make_uint4(0, 0, 0, 0);
+                    v[4 * i] = x.x, v[4 * i + 1] = x.y, v[4 * i + 2] = x.z, v[4 * i + 3] = x.w;
+                }
+                ptx::tmem_st16(t_lane + L::kTmemQ + c0, v);
+            }
+            ptx::tmem_st_wait();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&s_empty[sbuf]);
-            // the peer must have consumed its recv[sb] of tile j-2
-            ptx::mbar_wait(&recv_free[sb], par ^ 1);
-            if (warp == 2 && lane == 0) ELA_TRACE(9, j);
-            const uint32_t rbar = peer_recv_full0 + sb * 8;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                ptx::st_async_v4(peer_recv0 + recv_off(sb, k), __uint_as_float(sr[4 * k]),
-                                 __uint_as_float(sr[4 * k + 1]), __uint_as_float(sr[4 * k + 2]),
-                                 __uint_as_float(sr[4 * k + 3]), rbar);
-        };
-
-        uint32_t s_cur[16], s_next[16];
-        if (T > 0) stage_A(0, s_cur);
+            if (lane == 0) ptx::mbar_arrive(q_tmem_full);
+        }
         for (int j = 0; j < T; ++j) {
-            if (j + 1 < T) stage_A(j + 1, s_next);
-            // ---- stage B(j)
-            const int sb = j & 1;
+            const int sb = j & 1, sbuf = j & (kSBuf - 1);
             const uint32_t par = (j >> 1) & 1;
             if (warp == 2 && lane == 0) ELA_TRACE(10, j);
+            ptx::mbar_wait(&s_full[sbuf], (j / kSBuf) & 1);
+            ptx::tc_fence_after();
+            uint32_t sr[16];
+            ptx::tmem_ld_16x256b_x4(t_lane + kTmemS + sbuf * kNT, sr);
             ptx::mbar_wait(&recv_full[sb], par);
-            if (warp == 2 && lane == 0) ELA_TRACE(11, j);
+            if (warp == 2 && lane == 0) {
+                ELA_TRACE(11, j);
+                // this phase is consumed: arm the same buffer for tile j+2
+                if (j + 2 < T) ptx::mbar_arrive_expect_tx(&recv_full[sb], kRowsQ * kNT * 4);
+            }
+            ptx::tmem_ld_wait();
             const int nvalid = min(kNT, n_b - j * kNT);
-            float s[16];
+            float s[16];  // raw scores S_0 + S_1 (scale folded into the exponent below)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const float4 v = ptx::lds_f4(recv_base + recv_off(sb, k));
-                s[4 * k + 0] = (__uint_as_float(s_cur[4 * k + 0]) + v.x) * scale_log2;
-                s[4 * k + 1] = (__uint_as_float(s_cur[4 * k + 1]) + v.y) * scale_log2;
-                s[4 * k + 2] = (__uint_as_float(s_cur[4 * k + 2]) + v.z) * scale_log2;
-                s[4 * k + 3] = (__uint_as_float(s_cur[4 * k + 3]) + v.w) * scale_log2;
+                const float4 v = ptx::lds_f4(recv_base + recv_slot(sb, qd, k, lane));
+                s[4 * k + 0] = __uint_as_float(sr[4 * k + 0]) + v.x;
+                s[4 * k + 1] = __uint_as_float(sr[4 * k + 1]) + v.y;
+                s[4 * k + 2] = __uint_as_float(sr[4 * k + 2]) + v.z;
+                s[4 * k + 3] = __uint_as_float(sr[4 * k + 3]) + v.w;
             }
             if (nvalid < kNT) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
-                        if (8 * k + cpair + (i & 1) >= nvalid) s[4 * k + i] = -INFINITY;
+                        if (8 * k + cpair + (i & 1) >= nvalid) s[4 * k + i] = neg_inf;
             }
             float xa = fmaxf(fmaxf(s[0], s[1]), fmaxf(s[4], s[5]));
             float xb = fmaxf(fmaxf(s[2], s[3]), fmaxf(s[6], s[7]));
@@ -333,15 +435,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (lane == 0) ptx::mbar_arrive_remote(peer_recv_free0 + sb * 8);
             uint32_t need = 0;
             float alpha_a = 1.f, alpha_b = 1.f;
-            if (xa > m_a + kRescaleThreshold) {  // identical decision in all 4 quad threads
+            // lazy rescale: the reference max only moves when the tile max exceeds it
+            // by more than 2^8 in probability (identical decision in all 4 quad threads
+            // and in both CTAs of the cluster)
+            if ((xa - m_a) * scale_log2 > kRescaleThreshold) {
                 need = 1;
-                alpha_a = ptx::ex2(m_a - xa);  // 0 on the first tile
+                alpha_a = ptx::ex2((m_a - xa) * scale_log2);  // 0 on the first tile
                 l_a *= alpha_a;
                 m_a = xa;
             }
-            if (xb > m_b + kRescaleThreshold) {
+            if ((xb - m_b) * scale_log2 > kRescaleThreshold) {
                 need = 1;
-                alpha_b = ptx::ex2(m_b - xb);
+                alpha_b = ptx::ex2((m_b - xb) * scale_log2);
                 l_b *= alpha_b;
                 m_b = xb;
             }
@@ -349,12 +454,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 s_alpha[sb * 64 + ra] = alpha_a;
                 s_alpha[sb * 64 + rb] = alpha_b;
             }
+            const float ma_s = m_a * scale_log2, mb_s = m_b * scale_log2;
             uint32_t pa[4], pb[4];
             float sa = 0.f, sbs = 0.f;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const float p0 = ptx::ex2(s[4 * k] - m_a), p1 = ptx::ex2(s[4 * k + 1] - m_a);
-                const float p2 = ptx::ex2(s[4 * k + 2] - m_b), p3 = ptx::ex2(s[4 * k + 3] - m_b);
+                const float p0 = ptx::ex2(fmaf(s[4 * k], scale_log2, -ma_s));
+                const float p1 = ptx::ex2(fmaf(s[4 * k + 1], scale_log2, -ma_s));
+                const float p2 = ptx::ex2(fmaf(s[4 * k + 2], scale_log2, -mb_s));
+                const float p3 = ptx::ex2(fmaf(s[4 * k + 3], scale_log2, -mb_s));
                 sa += p0 + p1;
                 sbs += p2 + p3;
                 pa[k] = pack_bf16x2(p0, p1);
@@ -366,10 +474,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             sbs += __shfl_xor_sync(0xffffffffu, sbs, 2);
             l_a += sa;
             l_b += sbs;
-            // P[sb] is free once O(j-2) has consumed it
             if (warp == 2 && lane == 0) ELA_TRACE(12, j);
+            // P[sb] is free once O(j-2) has consumed it
             ptx::mbar_wait(&p_empty[sb], par ^ 1);
-            if (warp == 2 && lane == 0) ELA_TRACE(13, j);
             {
                 uint8_t* P = sP + sb * 8192;
 #pragma unroll
@@ -418,14 +525,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
-            if (warp == 2 && lane == 0) ELA_TRACE(14, j);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) s_cur[i] = s_next[i];
+            if (warp == 2 && lane == 0) ELA_TRACE(13, j);
         }
 
-        // ---- epilogue: C[b*rows + q][dm_off + d] = O^T[d][q] / l_q, staged through
-        // smem (two 16 KB [64 q][128 d] bf16 buffers in the drained ring) so the
-        // global stores are coalesced 16-byte vectors.
+        // ---- epilogue: C[b*rows + q][dm_off + d] = O^T[d][q] / l_q.
+        // O^T comes out of TMEM with tcgen05.ld.16x256b (thread t: lanes d = t/4, t/4+8,
+        // columns q = 2(t%4)+{0,1} per 8-column group), i.e. already in the 8x8 bf16
+        // fragment layout of stmatrix; stmatrix.trans writes the transpose into a
+        // [64 q][128 d] smem stage (row pitch 272 B: conflict-free), which is then stored
+        // to global memory as coalesced 16-byte vectors.
+        if (warp == 2 && lane == 0) ELA_TRACE(14, 0);
         if ((lane & 3) == 0) {
             s_l[ra] = 1.f / l_a;
             s_l[rb] = 1.f / l_b;
@@ -435,23 +544,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
         }
         softmax_bar_sync();
-        const int d_local = int(qd) * 32 + int(lane);
+        constexpr int kPitch = 272;  // bytes per staged q row (256 + 16)
         const int tid = int(threadIdx.x) - 64;
+        float inv_l[16];  // 1/l for this thread's columns q = 8k + 2(t%4) + {0,1}
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float2 v = *reinterpret_cast<const float2*>(s_l + 8 * k + cpair);
+            inv_l[2 * k] = v.x, inv_l[2 * k + 1] = v.y;
+        }
+        const uint32_t stmatrix_row = uint32_t((lane & 7) * kPitch + (int(qd) * 32 + int(lane >> 3) * 8) * 2);
         for (int m = 0; m < UNITS; ++m) {
-            __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(ring + (m & 1) * 16384);
+            uint8_t* stage = ring + (m & 1) * (64 * kPitch);
+            const uint32_t stage_base = ptx::smem_u32(stage) + stmatrix_row;
+            uint32_t lo[32], hi[32];  // lanes d 0..15 and 16..31 of this warp's quadrant
+            if (T > 0) {
+                ptx::tmem_ld_16x256b_x8(t_lane + m * 64, lo);
+                ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16) + m * 64, hi);
+                ptx::tmem_ld_wait();
+            }
 #pragma unroll
-            for (int c0 = 0; c0 < 64; c0 += 16) {
-                uint32_t r[16];
-                if (T > 0) {
-                    ptx::tmem_ld16(t_lane + m * 64 + c0, r);
-                    ptx::tmem_ld_wait();
-                }
+            for (int k = 0; k < 8; ++k) {  // query columns 8k..8k+7
+                uint32_t f[4];
+                const uint32_t* src[2] = {lo, hi};
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int qq = c0 + i;
-                    const float v = T > 0 ? __uint_as_float(r[i]) * s_l[qq] : __int_as_float(0x7fc00000);
-                    stage[qq * 128 + d_local] = __float2bfloat16_rn(v);
-                }
+                for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        const uint32_t* r = src[h2] + 4 * k + 2 * half;
+                        const float v0 = T > 0 ? __uint_as_float(r[0]) * inv_l[2 * k] : __int_as_float(0x7fc00000);
+                        const float v1 = T > 0 ? __uint_as_float(r[1]) * inv_l[2 * k + 1] : __int_as_float(0x7fc00000);
+                        f[2 * h2 + half] = pack_bf16x2(v0, v1);
+                    }
+                // matrices j = 0..3 cover d = 8j..8j+7 of the quadrant; transposed rows are q = 8k + i
+                ptx::stmatrix_x4_trans(stage_base + uint32_t(8 * k * kPitch), f[0], f[1], f[2], f[3]);
             }
             softmax_bar_sync();
             // 64 rows x 256 B = 1024 16-byte vectors, 8 per thread
@@ -461,9 +586,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int qq = idx >> 4, c16 = idx & 15;
                 if (qq < rows)
                     *reinterpret_cast<uint4*>(ctx + (int64_t(b) * rows + qq) * d_m + dm_off + m * 128 + c16 * 8) =
-                        *reinterpret_cast<const uint4*>(stage + qq * 128 + c16 * 8);
+                        *reinterpret_cast<const uint4*>(stage + qq * kPitch + c16 * 16);
             }
         }
+        if (warp == 2 && lane == 0) ELA_TRACE(15, 0);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -488,10 +614,11 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const uint32_t hbox[3] = {64, kNT, 1};
     CUtensorMap th = make_tmap_bf16(H, 3, hdims, hstr, hbox);
     auto kern = el_decode_tc_kernel<UNITS>;
-    constexpr uint32_t smem = DecSmem<UNITS>::kTotal;
+    constexpr uint32_t smem = DecLayout<UNITS>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<dim3(2 * B), kThreads, smem, st>>>(tq, th, npi, rows, n_stride, d_m, scale_log2,
-                                               static_cast<__nv_bfloat16*>(ctx), g_decode_trace);
+    kern<<<dim3(2 * B), kThreads, smem, st>>>(tq, th, static_cast<const __nv_bfloat16*>(qp), B * rows, npi, rows,
+                                               n_stride, d_m, scale_log2,
+                                               static_cast<__nv_bfloat16*>(ctx), g_decode_trace, g_tuning);
     ELA_CHECK_LAUNCH();
 }
 
@@ -509,6 +636,12 @@ void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, 
                     (reinterpret_cast<uintptr_t>(ctx) & 15) == 0,
                 ELATTN_ERR_PARAM, "tcgen05 decode: q', H and C must be 16-byte aligned");
     const float scale_log2 = scale * 1.4426950408889634f;
+    static const bool env_read = [] {
+        if (const char* e = getenv("ELATTN_DECODE_S_AHEAD")) g_tuning.s_ahead = atoi(e);
+        if (const char* e = getenv("ELATTN_DECODE_L2_AHEAD")) g_tuning.l2_ahead = atoi(e);
+        return true;
+    }();
+    (void)env_read;
     switch (d_m / 256) {
         case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st);
         case 2: return launch_units<2>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st);

@@ -41,7 +41,7 @@ bool tc_gemm_supported(const GemmArgs& g);
 void launch_tc_gemm(const GemmArgs& g, cudaStream_t st);
 
 // Testing hook: when non-null, the tcgen05 decode writes clock64 stamps of its
-// first cluster: trace[(cta*16 + event)*64 + tile].
+// first cluster: trace[(cta*24 + event)*64 + tile].
 extern unsigned long long* g_decode_trace;
 
 // tcgen05/TMA fused EL decode for bf16 (cluster of 2 CTAs per input, split d_m).

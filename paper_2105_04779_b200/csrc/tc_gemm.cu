@@ -118,12 +118,14 @@ __global__ void __launch_bounds__(128, 1)
         __syncwarp();
     }
 
-    // ---- epilogue: thread = output row, 16 columns per tcgen05.ld
+    // ---- epilogue: TMEM -> registers (thread = row) -> alpha/bias -> bf16 -> smem
+    // staging tile (the drained A/B stages) -> coalesced 16-byte global stores.
     ptx::mbar_wait(accum_full, 0);
     ptx::tc_fence_after();
-    const int row = m0 + int(warp) * 32 + int(lane);
+    constexpr int kPitch = BN * 2 + 16;  // bytes per staged row (+16: spread banks)
+    static_assert(kBM * kPitch <= kStages * S::kStageBytes, "staging tile fits in the pipeline buffers");
+    const int r_local = int(warp) * 32 + int(lane);
     const uint32_t t_row = tmem + ((warp * 32) << 16);
-    __nv_bfloat16* Crow = p.C + z * p.sCz + int64_t(row) * p.ldc;
     const float* bias = p.bias ? p.bias + z * p.sbz : nullptr;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -131,20 +133,35 @@ __global__ void __launch_bounds__(128, 1)
         ptx::tmem_ld16(t_row + c0, r);
         ptx::tmem_ld_wait();
         const int n = n0 + c0;
-        if (row < p.M && n < p.N) {
-            alignas(16) __nv_bfloat16 o[16];
+        uint32_t packed[8];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                float v = __uint_as_float(r[j]) * p.alpha;
-                if (bias && n + j < p.N) v += bias[n + j];
-                o[j] = __float2bfloat16_rn(v);
+        for (int j = 0; j < 16; j += 2) {
+            float v0 = __uint_as_float(r[j]) * p.alpha, v1 = __uint_as_float(r[j + 1]) * p.alpha;
+            if (bias) {
+                v0 += (n + j < p.N) ? bias[n + j] : 0.f;
+                v1 += (n + j + 1 < p.N) ? bias[n + j + 1] : 0.f;
             }
-            if (n + 16 <= p.N) {
-                *reinterpret_cast<uint4*>(Crow + n) = *reinterpret_cast<const uint4*>(o);
-                *reinterpret_cast<uint4*>(Crow + n + 8) = *reinterpret_cast<const uint4*>(o + 8);
-            } else {
-                for (int j = 0; j < 16 && n + j < p.N; ++j) Crow[n + j] = o[j];
-            }
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
+            packed[j / 2] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        uint8_t* dst = smem + r_local * kPitch + c0 * 2;
+        *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        *reinterpret_cast<uint4*>(dst + 16) = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+    }
+    __syncthreads();
+    constexpr int kVecPerRow = BN / 8;  // 16-byte vectors per output row
+    const bool full_n = (n0 + BN <= p.N) && (p.N % 8 == 0);
+#pragma unroll 4
+    for (int idx = int(threadIdx.x); idx < kBM * kVecPerRow; idx += 128) {
+        const int rr = idx / kVecPerRow, cv = idx % kVecPerRow;
+        const int row = m0 + rr, n = n0 + cv * 8;
+        if (row >= p.M) continue;
+        __nv_bfloat16* Crow = p.C + z * p.sCz + int64_t(row) * p.ldc;
+        const uint8_t* src = smem + rr * kPitch + cv * 16;
+        if (full_n || n + 8 <= p.N) {
+            *reinterpret_cast<uint4*>(Crow + n) = *reinterpret_cast<const uint4*>(src);
+        } else {
+            for (int j = 0; j < 8 && n + j < p.N; ++j) Crow[n + j] = reinterpret_cast<const __nv_bfloat16*>(src)[j];
         }
     }
     ptx::tc_fence_before();
