@@ -5,31 +5,36 @@
 // i.e. the core of el_attention_folded (attention.hpp:272-280), reading H_b from
 // HBM exactly once and using every staged tile as BOTH key and value.
 //
-// Work split — one thread-block CLUSTER of 2 CTAs per input, split along d_m:
+// Work split — thread-block CLUSTERS of 2 CTAs, split along d_m; persistent:
+//   cluster c processes inputs c, c + #clusters, ... as one continuous pipeline (a
+//   cluster-global tile counter drives every ring / buffer phase across inputs, so
+//   the next input's q' and H tiles stream in while the previous input drains).
 //   CTA r owns d_m columns [r*d_m/2, (r+1)*d_m/2).  Its EL-Q half q'_r (64 x d_m/2)
-//   stays resident in smem; H_b streams through a 128 KB TMA ring in tiles of
-//   32 rows x d_m/2 (SWIZZLE_128B, 128-column "units" of 8 KB).
-//   Per tile j:
+//   is held half in TMEM (as the A operand of the score MMA) and half in smem; H_b
+//   streams through a TMA ring in tiles of 32 rows x d_m/2 (SWIZZLE_128B, 128-column
+//   "units" of 8 KB).  Per tile:
 //     S_r   = q'_r . H_tile,r^T         tcgen05.mma M=64 N=32, K = d_m/2   (TMEM)
 //     S     = S_0 + S_1                  partial scores swapped through DSMEM
 //                                        (st.async + mbarrier complete_tx)
-//     P     = exp2(S*scale*log2e - m)    online softmax, one query row per thread,
-//                                        lazy rescale (FA4-style threshold 2^8)
+//     P     = exp2(S*scale*log2e - m)    online softmax, lazy rescale (FA4-style,
+//                                        threshold 2^8)
 //     O_r^T += H_tile,r^T . P^T          tcgen05.mma M=128 (d_m) N=64 (queries),
 //                                        A = the SAME smem tile read MN-major
 //   O_r (d_m/2 x 64 fp32) lives in TMEM for the whole input; the epilogue divides
 //   by the softmax sums and writes C rows b*rows + q, columns of this CTA's half.
 // Both CTAs see bit-identical S (fp32 add commutes), so their softmax decisions agree.
 //
-// Pipelining: the MMA warp runs S three tiles ahead of O (issue order
-// S0 S1 S2 | O0 S3 | O1 S4 | ...).  Four "exchange" warps take each S tile out of
-// TMEM and post it to the peer as soon as it is computed, so the DSMEM transfer
-// overlaps whole tiles of softmax work and the softmax warps never fence behind
-// their own in-flight remote stores.
+// One thread can issue only ~1 tcgen05.mma per 56 cycles (tools/probes/
+// mma_rate_probe.cu) and a score tile is 32 small MMAs, so three warps issue MMAs:
+// S for even tiles, S for odd tiles, and O.  S runs up to 4 tiles ahead of O.
 //
-// Roles (384 threads): warp 0 TMA producer, warps 1 and 11 S-MMA issuers (even /
-// odd tiles; warp 1 owns TMEM), warps 2..5 softmax / rescale / epilogue, warps 6..9
-// score exchange (TMEM lane quadrant = warp % 4 for both groups), warp 10 O-MMA issuer.
+// Roles (384 threads, 12 warps):
+//   warp 0      TMA producer (q' smem half, H ring)
+//   warp 1      S issuer, even tiles (+ TMEM allocation owner)
+//   warps 2..5  softmax / rescale / epilogue (TMEM lane quadrant = warp % 4)
+//   warps 6..9  score exchange with the peer CTA, q' -> TMEM fill
+//   warp 10     O issuer
+//   warp 11     S issuer, odd tiles
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx_sm100.cuh"
@@ -39,7 +44,7 @@
 
 namespace elattn_gpu {
 
-unsigned long long* g_decode_trace = nullptr;  // testing hook (elattn_gpu_testing_decode_trace)
+unsigned long long* g_decode_trace = nullptr;  // testing hook (elattn_gpu_testing_set_decode_trace)
 
 namespace {
 
@@ -48,8 +53,12 @@ constexpr int kNT = 32;            // H rows per tile
 constexpr int kUnitBytes = 8192;   // 32 rows x 128 d_m x bf16
 constexpr int kChunkBytes = 4096;  // 32 rows x 64 d_m
 constexpr int kThreads = 384;
-constexpr int kSBuf = 4;           // S accumulators in TMEM (S runs up to 3 tiles ahead of O)
-// Tuning knobs (runtime so they can be swept; defaults chosen by tools/sweep_decode.py):
+constexpr int kSBuf = 4;  // S accumulators in TMEM
+constexpr int kEpiPitch = 80;                  // per-warp epilogue stage: 8 q-rows x (32 d + pad)
+constexpr int kEpiWarpBytes = 8 * kEpiPitch;   // 640 B per softmax warp
+constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max grows by > 2^8
+
+// Tuning knobs (runtime so they can be swept):
 //   s_ahead  — how many tiles S may run ahead of O (<= kSBuf);
 //   l2_ahead — how many tiles ahead of the smem ring H is prefetched into L2 (0 = off).
 struct DecodeTuning {
@@ -57,7 +66,6 @@ struct DecodeTuning {
     int l2_ahead = 0;
 };
 DecodeTuning g_tuning;
-constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max grows by > 2^8
 
 // TMEM columns (512): O^T [0, 64*UNITS) | S buffers [64*UNITS, +128) | q' units held in
 // TMEM as the M=64 A operand [.., 512).  q' units that do not fit stay in smem.
@@ -70,7 +78,8 @@ struct DecLayout {
     static constexpr int kQSmemUnits = UNITS - kQTmemUnits;
     // shared memory
     static constexpr uint32_t kQBytes = kQSmemUnits * 2 * 8192;  // 64 rows x 128 d_m per unit
-    static constexpr uint32_t kFixed = kQBytes + 2 * 8192 /*P*/ + 2 * 8192 /*recv*/ + 2 * 64 * 4 + 64 * 4 + 1024;
+    static constexpr uint32_t kFixed =
+        kQBytes + 2 * 8192 /*P*/ + 2 * 8192 /*recv*/ + 2 * 64 * 4 + 64 * 4 + 4 * kEpiWarpBytes + 1024;
     static constexpr int kRingMax = 24;
     static constexpr int kRingFit = int((232448u - kFixed - 512u) / 8192u);
     static constexpr int kRing = kRingFit < kRingMax ? kRingFit : kRingMax;  // 8 KB units in the H ring
@@ -79,8 +88,9 @@ struct DecLayout {
     static constexpr uint32_t kRecvOff = kPOff + 2 * 8192;            // 2 x (64 x 32 fp32)
     static constexpr uint32_t kAlphaOff = kRecvOff + 2 * 8192;        // 2 x 64 fp32
     static constexpr uint32_t kLOff = kAlphaOff + 2 * 64 * 4;         // 64 fp32
-    static constexpr uint32_t kBarOff = kLOff + 64 * 4;
-    static constexpr int kNumBars = 2 + 2 * kRing + 2 * kSBuf + 2 * 4 + 2;
+    static constexpr uint32_t kEpiOff = kLOff + 64 * 4;               // 4 x 640 B
+    static constexpr uint32_t kBarOff = kEpiOff + 4 * kEpiWarpBytes;
+    static constexpr int kNumBars = 2 * kRing + 24;
     static constexpr uint32_t kTotal = kBarOff + kNumBars * 8 + 16 + 1024;
     static_assert(kTotal <= 232448, "shared memory budget");
     static_assert(kQTmemUnits >= 1, "at least one q' unit in TMEM");
@@ -113,20 +123,24 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ int tiles_of(const int* npi, int b, int n_stride) {
+    const int n_b = npi ? npi[b] : n_stride;
+    return (n_b >= 1 && n_b <= n_stride) ? (n_b + kNT - 1) / kNT : 0;
+}
+
 template <int UNITS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     el_decode_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_h,
-                        const __nv_bfloat16* __restrict__ qp_rows, int total_rows,
-                        const int* __restrict__ n_per_input, int rows, int n_stride, int d_m, float scale_log2,
-                        __nv_bfloat16* __restrict__ ctx, unsigned long long* __restrict__ trace,
-                        DecodeTuning tune) {
+                        const __nv_bfloat16* __restrict__ qp_rows, const int* __restrict__ n_per_input, int B,
+                        int rows, int n_stride, int d_m, float scale_log2, __nv_bfloat16* __restrict__ ctx,
+                        unsigned long long* __restrict__ trace, DecodeTuning tune) {
     using L = DecLayout<UNITS>;
     constexpr int kRing = L::kRing;
-    // optional per-tile clock64 trace of the first cluster (testing hook)
-#define ELA_TRACE(ev, j)                                                                          \
+    // optional per-tile clock64 trace of the first cluster (testing hook); G = cluster tile index
+#define ELA_TRACE(ev, G)                                                                          \
     do {                                                                                          \
-        if (trace != nullptr && blockIdx.x < 2 && (j) < 64)                                       \
-            trace[(blockIdx.x * 24 + (ev)) * 64 + (j)] = clock64();                               \
+        if (trace != nullptr && blockIdx.x < 2 && (G) < 64)                                       \
+            trace[(blockIdx.x * 24 + (ev)) * 64 + (G)] = clock64();                               \
     } while (0)
     constexpr int kTmemCols = 512;
     constexpr uint32_t kTmemS = L::kTmemS;
@@ -140,45 +154,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float* recv = reinterpret_cast<float*>(smem + L::kRecvOff);
     float* s_alpha = reinterpret_cast<float*>(smem + L::kAlphaOff);
     float* s_l = reinterpret_cast<float*>(smem + L::kLOff);
+    uint8_t* epi_stage = smem + L::kEpiOff;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-    uint64_t* q_full = bars;
-    uint64_t* q_tmem_full = bars + 1;  // q' units written into TMEM by the softmax warps
-    uint64_t* unit_full = bars + 2;
+    uint64_t* q_full = bars;            // q' smem half landed (per input)
+    uint64_t* q_empty = bars + 1;       // both S issuers finished reading q' (per input)
+    uint64_t* q_tmem_full = bars + 2;   // q' TMEM half written by the exchange warps (per input)
+    uint64_t* o_full = bars + 3;        // last O MMA of an input complete
+    uint64_t* o_free = bars + 4;        // epilogue has read O out of TMEM
+    uint64_t* o_done = bars + 5;        // per tile: O MMAs complete
+    uint64_t* s_full = bars + 6;        // [4]
+    uint64_t* s_empty = s_full + kSBuf;  // [4]
+    uint64_t* p_full = s_empty + kSBuf;  // [2]
+    uint64_t* p_empty = p_full + 2;      // [2]
+    uint64_t* recv_full = p_empty + 2;   // [2]
+    uint64_t* recv_free = recv_full + 2;  // [2] arrived by the PEER's softmax warps
+    uint64_t* unit_full = recv_free + 2;  // [kRing]
     uint64_t* unit_empty = unit_full + kRing;
-    uint64_t* s_full = unit_empty + kRing;
-    uint64_t* s_empty = s_full + kSBuf;
-    uint64_t* p_full = s_empty + kSBuf;
-    uint64_t* p_empty = p_full + 2;
-    uint64_t* recv_full = p_empty + 2;
-    uint64_t* recv_free = recv_full + 2;  // arrived by the PEER's softmax warps
-    uint64_t* o_done = recv_free + 2;
-    uint64_t* o_full = o_done + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(unit_empty + kRing);
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
     const uint32_t rank = ptx::cluster_ctarank(), peer = rank ^ 1u;
-    const int b = blockIdx.x >> 1;
+    const int cl = int(blockIdx.x >> 1), ncl = int(gridDim.x >> 1);
     const int dm_half = d_m / 2, dm_off = int(rank) * dm_half;
-    const int n_b = n_per_input ? n_per_input[b] : n_stride;
-    const bool valid = n_b >= 1 && n_b <= n_stride;
-    const int T = valid ? (n_b + kNT - 1) / kNT : 0;
-    // q' rows of this input that exist in memory (the 64-row box pads with the next
-    // input's rows, or zeros past the end, exactly like the TMA path)
-    const int rows_valid_for_tmem = min(kRowsQ, total_rows - b * rows);
+    const int total_rows = B * rows;
 
     if (warp == 0) {
         if (ptx::elect_one()) {
             ptx::prefetch_tmap(&tm_q);
             ptx::prefetch_tmap(&tm_h);
             ptx::mbar_init(q_full, 1);
+            ptx::mbar_init(q_empty, 2);
             ptx::mbar_init(q_tmem_full, 4);
-            for (int s = 0; s < kRing; ++s) {
-                ptx::mbar_init(&unit_full[s], 1);
-                ptx::mbar_init(&unit_empty[s], 1);
-            }
+            ptx::mbar_init(o_full, 1);
+            ptx::mbar_init(o_free, 4);
+            ptx::mbar_init(o_done, 1);
             for (int i = 0; i < kSBuf; ++i) {
                 ptx::mbar_init(&s_full[i], 1);
-                ptx::mbar_init(&s_empty[i], 5);  // 4 exchange warps + the O issuer
+                ptx::mbar_init(&s_empty[i], 5);  // 4 exchange warps + the O issuer (softmax relay)
             }
             for (int i = 0; i < 2; ++i) {
                 ptx::mbar_init(&p_full[i], 4);
@@ -186,8 +198,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::mbar_init(&recv_full[i], 1);
                 ptx::mbar_init(&recv_free[i], 4);
             }
-            ptx::mbar_init(o_done, 1);
-            ptx::mbar_init(o_full, 1);
+            for (int s = 0; s < kRing; ++s) {
+                ptx::mbar_init(&unit_full[s], 1);
+                ptx::mbar_init(&unit_empty[s], 1);
+            }
             ptx::fence_mbar_init();
             // expected bytes of the peer's partial scores for tiles 0 and 1; later
             // tiles are posted by the softmax warps once the previous phase is consumed
@@ -205,65 +219,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ================= TMA producer =================
-        if (ptx::elect_one() && T > 0) {
-            if (L::kQSmemUnits > 0) {
-                ptx::mbar_arrive_expect_tx(q_full, L::kQBytes);
-                for (int c = 0; c < 2 * L::kQSmemUnits; ++c)
-                    ptx::tma_load_2d(sq + c * 8192, &tm_q, q_full, dm_off + 128 * L::kQTmemUnits + 64 * c, b * rows,
-                                     ptx::kEvictNormal);
-            }
-            // optionally warm L2 with the first tiles; later tiles are prefetched l2_ahead ahead
-            for (int j = 0; j < tune.l2_ahead && j < T; ++j)
-                for (int c = 0; c < 2 * UNITS; ++c) ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, j * kNT, b);
-            for (int j = 0; j < T; ++j) {
-                if (tune.l2_ahead > 0 && j + tune.l2_ahead < T)
-                    for (int c = 0; c < 2 * UNITS; ++c)
-                        ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, b);
-                for (int u = 0; u < UNITS; ++u) {
-                    const int g = j * UNITS + u, s = g % kRing;
-                    if (u == 0) ELA_TRACE(0, j);
-                    ptx::mbar_wait(&unit_empty[s], ((g / kRing) & 1) ^ 1);
-                    if (u == 0) ELA_TRACE(1, j);
-                    uint8_t* dst = ring + s * kUnitBytes;
-                    ptx::mbar_arrive_expect_tx(&unit_full[s], kUnitBytes);
-                    const int col = dm_off + 128 * u;
-                    ptx::tma_load_3d(dst, &tm_h, &unit_full[s], col, j * kNT, b, ptx::kEvictFirst);
-                    ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, b,
-                                     ptx::kEvictFirst);
+        if (ptx::elect_one()) {
+            int G = 0, li = 0;
+            for (int b = cl; b < B; b += ncl) {
+                const int T = tiles_of(n_per_input, b, n_stride);
+                if (T == 0) continue;
+                for (int j = 0; j < T; ++j) {
+                    const int Gt = G + j;
+                    if (tune.l2_ahead > 0 && j + tune.l2_ahead < T)
+                        for (int c = 0; c < 2 * UNITS; ++c)
+                            ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, b);
+                    for (int u = 0; u < UNITS; ++u) {
+                        const int g = Gt * UNITS + u, s = g % kRing;
+                        if (u == 0) ELA_TRACE(0, Gt);
+                        ptx::mbar_wait(&unit_empty[s], ((g / kRing) & 1) ^ 1);
+                        if (u == 0) ELA_TRACE(1, Gt);
+                        uint8_t* dst = ring + s * kUnitBytes;
+                        ptx::mbar_arrive_expect_tx(&unit_full[s], kUnitBytes);
+                        const int col = dm_off + 128 * u;
+                        ptx::tma_load_3d(dst, &tm_h, &unit_full[s], col, j * kNT, b, ptx::kEvictFirst);
+                        ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, b,
+                                         ptx::kEvictFirst);
+                    }
+                    if (j == 0 && L::kQSmemUnits > 0) {
+                        // this input's smem half of q', once the previous input's S no longer reads it
+                        if (li > 0) ptx::mbar_wait(q_empty, (li - 1) & 1);
+                        ptx::mbar_arrive_expect_tx(q_full, L::kQBytes);
+                        for (int c = 0; c < 2 * L::kQSmemUnits; ++c)
+                            ptx::tma_load_2d(sq + c * 8192, &tm_q, q_full, dm_off + 128 * L::kQTmemUnits + 64 * c,
+                                             b * rows, ptx::kEvictNormal);
+                    }
                 }
+                G += T;
+                ++li;
             }
         }
         __syncwarp();
     } else if (warp == 1 || warp == 11) {
         // ================= S issuers (warp 1: even tiles, warp 11: odd tiles) =================
-        // One thread can issue only ~1 tcgen05.mma per 56 cycles (measured by
-        // tools/probes/mma_rate_probe.cu), and an S tile is 32 small MMAs, so two warps
-        // issue alternate tiles.  The whole warp runs the loop (slot/phase arithmetic
-        // stays warp-uniform, on the uniform datapath next to UTCHMMA); lane 0 issues.
-        if (T > 0) {
-            constexpr uint32_t idS = ptx::idesc_bf16(64, kNT, 0, 0);  // S = q' . H^T
-            const uint64_t dRing = ptx::sdesc_sw128(ptx::smem_u32(ring), 0, 1024);
-            const uint64_t dQ = ptx::sdesc_sw128(ptx::smem_u32(sq), 0, 1024);
-            if (L::kQSmemUnits > 0) ptx::mbar_wait(q_full, 0);
-            ptx::mbar_wait(q_tmem_full, 0);
-            for (int j = (warp == 1 ? 0 : 1); j < T; j += 2) {
-                const int sb = j & (kSBuf - 1);
+        // The whole warp runs the loop (slot/phase arithmetic stays warp-uniform, on the
+        // uniform datapath next to UTCHMMA); lane 0 issues and commits.
+        constexpr uint32_t idS = ptx::idesc_bf16(64, kNT, 0, 0);  // S = q' . H^T
+        const uint64_t dRing = ptx::sdesc_sw128(ptx::smem_u32(ring), 0, 1024);
+        const uint64_t dQ = ptx::sdesc_sw128(ptx::smem_u32(sq), 0, 1024);
+        const int parity_mine = warp == 1 ? 0 : 1;
+        int G = 0, li = 0;
+        for (int b = cl; b < B; b += ncl) {
+            const int T = tiles_of(n_per_input, b, n_stride);
+            if (T == 0) continue;
+            if (L::kQSmemUnits > 0) ptx::mbar_wait(q_full, li & 1);
+            ptx::mbar_wait(q_tmem_full, li & 1);
+            for (int Gt = G + ((G & 1) != parity_mine ? 1 : 0); Gt < G + T; Gt += 2) {
+                const int sb = Gt & (kSBuf - 1);
                 const uint32_t d = tmem + kTmemS + sb * kNT;
-                if (lane == 0) ELA_TRACE(2, j);
-                // buffer j%4 is free once the exchange warps and (relayed by the O issuer)
-                // the softmax have consumed S(j-4)
-                ptx::mbar_wait(&s_empty[sb], ((j / kSBuf) & 1) ^ 1);
-                if (tune.s_ahead < kSBuf && j >= tune.s_ahead) {
-                    const int jj = j - tune.s_ahead;  // bound the lookahead: O(j - s_ahead) issued
+                if (lane == 0) ELA_TRACE(2, Gt);
+                // buffer Gt%4 is free once the exchange warps and (relayed by the O
+                // issuer) the softmax have consumed S(Gt-4)
+                ptx::mbar_wait(&s_empty[sb], ((Gt / kSBuf) & 1) ^ 1);
+                if (tune.s_ahead < kSBuf && Gt >= tune.s_ahead) {
+                    const int jj = Gt - tune.s_ahead;  // bound the lookahead: O(Gt - s_ahead) issued
                     ptx::mbar_wait(&s_empty[jj & (kSBuf - 1)], (jj / kSBuf) & 1);
                 }
 #pragma unroll
                 for (int u = 0; u < UNITS; ++u) {
-                    const int g = j * UNITS + u, slot = g % kRing;
-                    if (lane == 0 && u == 0) ELA_TRACE(16, j);
+                    const int g = Gt * UNITS + u, slot = g % kRing;
                     ptx::mbar_wait(&unit_full[slot], (g / kRing) & 1);
-                    if (lane == 0 && u == 0) ELA_TRACE(17, j);
-                    if (lane == 0 && u == UNITS - 1) ELA_TRACE(18, j);
                     ptx::tc_fence_after();
                     const uint64_t dB = dRing + uint64_t((slot * kUnitBytes) >> 4);
                     if (lane == 0) {
@@ -284,77 +304,117 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     __syncwarp();
                 }
                 if (lane == 0) {
-                    ELA_TRACE(19, j);
                     ptx::mma_commit(&s_full[sb]);
-                    ELA_TRACE(3, j);
+                    ELA_TRACE(3, Gt);
                 }
                 __syncwarp();
             }
+            // this issuer is done reading the input's q' (smem + TMEM) once its MMAs drain
+            if (lane == 0) ptx::mma_commit(q_empty);
+            __syncwarp();
+            G += T;
+            ++li;
         }
     } else if (warp == 10) {
         // ================= O issuer =================
-        // A second issuer warp, so O(k) (the softmax critical path) never queues behind
-        // S(k+3) waiting for TMA data.  Whole warp loops, lane 0 issues and commits.
-        if (T > 0) {
-            constexpr uint32_t idO = ptx::idesc_bf16(128, 64, 1, 0);  // O^T += H^T . P^T (A MN-major)
-            const uint64_t dRingMN = ptx::sdesc_sw128(ptx::smem_u32(ring), kChunkBytes, 1024);
-            const uint64_t dP = ptx::sdesc_sw128(ptx::smem_u32(sP), 0, 1024);
-            for (int t = 0; t < T; ++t) {
-                const int pb = t & 1;
-                if (lane == 0) ELA_TRACE(4, t);
-                ptx::mbar_wait(&p_full[pb], (t >> 1) & 1);
-                if (lane == 0) ELA_TRACE(5, t);
+        constexpr uint32_t idO = ptx::idesc_bf16(128, 64, 1, 0);  // O^T += H^T . P^T (A MN-major)
+        const uint64_t dRingMN = ptx::sdesc_sw128(ptx::smem_u32(ring), kChunkBytes, 1024);
+        const uint64_t dP = ptx::sdesc_sw128(ptx::smem_u32(sP), 0, 1024);
+        int G = 0, li = 0;
+        for (int b = cl; b < B; b += ncl) {
+            const int T = tiles_of(n_per_input, b, n_stride);
+            if (T == 0) continue;
+            for (int j = 0; j < T; ++j) {
+                const int Gt = G + j, pb = Gt & 1;
+                if (lane == 0) ELA_TRACE(4, Gt);
+                ptx::mbar_wait(&p_full[pb], (Gt >> 1) & 1);
+                // the first O of an input overwrites the accumulator: the previous
+                // input's epilogue must have read it out
+                if (j == 0 && li > 0) ptx::mbar_wait(o_free, (li - 1) & 1);
+                if (lane == 0) ELA_TRACE(5, Gt);
                 ptx::tc_fence_after();
                 if (lane == 0) {
 #pragma unroll
                     for (int m = 0; m < UNITS; ++m) {
-                        const int slot = (t * UNITS + m) % kRing;
+                        const int slot = (Gt * UNITS + m) % kRing;
 #pragma unroll
                         for (int kk = 0; kk < kNT / 16; ++kk) {
                             const uint64_t a = dRingMN + uint64_t((slot * kUnitBytes + kk * 2048) >> 4);
                             const uint64_t bd = dP + uint64_t((pb * 8192 + 32 * kk) >> 4);
-                            ptx::mma_bf16(tmem + m * 64, a, bd, idO, (t > 0 || kk > 0) ? 1u : 0u);
+                            ptx::mma_bf16(tmem + m * 64, a, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
                         }
                         ptx::mma_commit(&unit_empty[slot]);
                     }
                     ptx::mma_commit(&p_empty[pb]);
                     ptx::mma_commit(o_done);
-                    // P(t) observed => the softmax has consumed S(t): release its buffer
-                    ptx::mbar_arrive(&s_empty[t & (kSBuf - 1)]);
+                    // P(Gt) observed => the softmax has consumed S(Gt): release its buffer
+                    ptx::mbar_arrive(&s_empty[Gt & (kSBuf - 1)]);
                 }
                 __syncwarp();
             }
             if (lane == 0) ptx::mma_commit(o_full);
             __syncwarp();
+            G += T;
+            ++li;
         }
-    } else if (warp >= 6 && warp <= 9) {
-        // ================= score exchange (warps 6..9) =================
+    } else if (warp >= 6) {
+        // ================= score exchange + q' TMEM fill (warps 6..9) =================
         const uint32_t qd = warp & 3;
         const uint32_t t_lane = tmem + ((qd * 32) << 16);
         const uint32_t peer_recv_full0 = ptx::mapa(ptx::smem_u32(&recv_full[0]), peer);
         const uint32_t peer_recv0 = ptx::mapa(ptx::smem_u32(recv), peer);
-        for (int j = 0; j < T; ++j) {
-            const int sb = j & 1, sbuf = j & (kSBuf - 1);
-            if (warp == 6 && lane == 0) ELA_TRACE(6, j);
-            ptx::mbar_wait(&s_full[sbuf], (j / kSBuf) & 1);
-            if (warp == 6 && lane == 0) ELA_TRACE(7, j);
-            ptx::tc_fence_after();
-            uint32_t sr[16];
-            ptx::tmem_ld_16x256b_x4(t_lane + kTmemS + sbuf * kNT, sr);
-            ptx::tmem_ld_wait();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&s_empty[sbuf]);
-            // the peer must have consumed its recv[sb] of tile j-2
-            ptx::mbar_wait(&recv_free[sb], ((j >> 1) & 1) ^ 1);
-            if (warp == 6 && lane == 0) ELA_TRACE(8, j);
-            const uint32_t rbar = peer_recv_full0 + sb * 8;
+        int G = 0, li = 0;
+        for (int b = cl; b < B; b += ncl) {
+            const int T = tiles_of(n_per_input, b, n_stride);
+            if (T == 0) continue;
+            {
+                // q' units [0, kQTmemUnits) of this CTA's d_m half -> TMEM, M=64 A layout:
+                // row 16*qd + t (t < 16) in lane 32*qd + t, bf16 pairs packed per column.
+                // Rows past this input's `rows` come from the next input (or zeros past
+                // the end), matching the 64-row TMA box of the smem half.
+                if (li > 0) ptx::mbar_wait(q_empty, (li - 1) & 1);  // previous input's S done
+                const int q = int(qd) * 16 + int(lane);
+                const bool row_ok = lane < 16 && b * rows + q < total_rows;
+                const uint4* qrow = reinterpret_cast<const uint4*>(qp_rows + (int64_t(b) * rows + q) * d_m + dm_off);
+                for (int c0 = 0; c0 < L::kQTmemUnits * 64; c0 += 16) {  // 16 columns = 32 bf16 per store
+                    uint32_t v[16];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                ptx::st_async_v4(peer_recv0 + recv_slot(sb, qd, k, lane), __uint_as_float(sr[4 * k]),
-                                 __uint_as_float(sr[4 * k + 1]), __uint_as_float(sr[4 * k + 2]),
-                                 __uint_as_float(sr[4 * k + 3]), rbar);
-            if (warp == 6 && lane == 0) ELA_TRACE(9, j);
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 x = row_ok ? __ldg(qrow + c0 / 4 + i) : make_uint4(0, 0, 0, 0);
+                        v[4 * i] = x.x, v[4 * i + 1] = x.y, v[4 * i + 2] = x.z, v[4 * i + 3] = x.w;
+                    }
+                    ptx::tmem_st16(t_lane + L::kTmemQ + c0, v);
+                }
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(q_tmem_full);
+            }
+            for (int j = 0; j < T; ++j) {
+                const int Gt = G + j, sb = Gt & 1, sbuf = Gt & (kSBuf - 1);
+                if (warp == 6 && lane == 0) ELA_TRACE(6, Gt);
+                ptx::mbar_wait(&s_full[sbuf], (Gt / kSBuf) & 1);
+                if (warp == 6 && lane == 0) ELA_TRACE(7, Gt);
+                ptx::tc_fence_after();
+                uint32_t sr[16];
+                ptx::tmem_ld_16x256b_x4(t_lane + kTmemS + sbuf * kNT, sr);
+                ptx::tmem_ld_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&s_empty[sbuf]);
+                // the peer must have consumed its recv[sb] of tile Gt-2
+                ptx::mbar_wait(&recv_free[sb], ((Gt >> 1) & 1) ^ 1);
+                if (warp == 6 && lane == 0) ELA_TRACE(8, Gt);
+                const uint32_t rbar = peer_recv_full0 + sb * 8;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    ptx::st_async_v4(peer_recv0 + recv_slot(sb, qd, k, lane), __uint_as_float(sr[4 * k]),
+                                     __uint_as_float(sr[4 * k + 1]), __uint_as_float(sr[4 * k + 2]),
+                                     __uint_as_float(sr[4 * k + 3]), rbar);
+                if (warp == 6 && lane == 0) ELA_TRACE(9, Gt);
+            }
+            G += T;
+            ++li;
         }
     } else {
         // ================= softmax / rescale / epilogue (warps 2..5) =================
@@ -368,228 +428,223 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t recv_base = ptx::smem_u32(recv);
         const uint32_t peer_recv_free0 = ptx::mapa(ptx::smem_u32(&recv_free[0]), peer);
         const float neg_inf = -INFINITY;
-        float m_a = neg_inf, m_b = neg_inf, l_a = 0.f, l_b = 0.f;  // running max (raw score units), sums
-        const bool zero_tail = (n_per_input != nullptr) && (T * kNT > n_b);
-        if (T > 0) {
-            // q' units [0, kQTmemUnits) of this CTA's d_m half -> TMEM, M=64 A layout:
-            // row 16*qd + t (t < 16) in lane 32*qd + t, bf16 pairs packed per column.
-            const uint4* qrow = reinterpret_cast<const uint4*>(
-                qp_rows + (int64_t(b) * rows + int(qd) * 16 + int(lane)) * d_m + dm_off);
-            const bool row_ok = lane < 16 && int(qd) * 16 + int(lane) < rows_valid_for_tmem;
-            for (int c0 = 0; c0 < L::kQTmemUnits * 64; c0 += 16) {  // 16 columns = 32 bf16 per store
-                uint32_t v[16];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint4 x = row_ok ? __ldg(qrow + c0 / 4 + i) : make_uint4(0, 0, 0, 0);
-                    v[4 * i] = x.x, v[4 * i + 1] = x.y, v[4 * i + 2] = x.z, v[4 * i + 3] = x.w;
+        // total tiles of this cluster (to stop arming recv_full past the end)
+        int G_total = 0;
+        for (int b = cl; b < B; b += ncl) G_total += tiles_of(n_per_input, b, n_stride);
+        uint8_t* my_stage = epi_stage + (warp - 2) * kEpiWarpBytes;
+        const uint32_t stm_addr =
+            ptx::smem_u32(my_stage) + uint32_t((lane & 7) * kEpiPitch + (lane >> 3) * 16);  // stmatrix rows
+        int G = 0, li = 0;
+        for (int b = cl; b < B; b += ncl) {
+            const int T = tiles_of(n_per_input, b, n_stride);
+            if (T == 0) continue;
+            const int n_b = n_per_input ? n_per_input[b] : n_stride;
+            const bool zero_tail = (n_per_input != nullptr) && (T * kNT > n_b);
+            float m_a = neg_inf, m_b = neg_inf, l_a = 0.f, l_b = 0.f;  // running max (raw units), sums
+            for (int j = 0; j < T; ++j) {
+                const int Gt = G + j, sb = Gt & 1, sbuf = Gt & (kSBuf - 1);
+                const uint32_t par = (Gt >> 1) & 1;
+                if (warp == 2 && lane == 0) ELA_TRACE(10, Gt);
+                ptx::mbar_wait(&s_full[sbuf], (Gt / kSBuf) & 1);
+                ptx::tc_fence_after();
+                uint32_t sr[16];
+                ptx::tmem_ld_16x256b_x4(t_lane + kTmemS + sbuf * kNT, sr);
+                ptx::mbar_wait(&recv_full[sb], par);
+                if (warp == 2 && lane == 0) {
+                    ELA_TRACE(11, Gt);
+                    // this phase is consumed: arm the same buffer for tile Gt+2
+                    if (Gt + 2 < G_total) ptx::mbar_arrive_expect_tx(&recv_full[sb], kRowsQ * kNT * 4);
                 }
-                ptx::tmem_st16(t_lane + L::kTmemQ + c0, v);
-            }
-            ptx::tmem_st_wait();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(q_tmem_full);
-        }
-        for (int j = 0; j < T; ++j) {
-            const int sb = j & 1, sbuf = j & (kSBuf - 1);
-            const uint32_t par = (j >> 1) & 1;
-            if (warp == 2 && lane == 0) ELA_TRACE(10, j);
-            ptx::mbar_wait(&s_full[sbuf], (j / kSBuf) & 1);
-            ptx::tc_fence_after();
-            uint32_t sr[16];
-            ptx::tmem_ld_16x256b_x4(t_lane + kTmemS + sbuf * kNT, sr);
-            ptx::mbar_wait(&recv_full[sb], par);
-            if (warp == 2 && lane == 0) {
-                ELA_TRACE(11, j);
-                // this phase is consumed: arm the same buffer for tile j+2
-                if (j + 2 < T) ptx::mbar_arrive_expect_tx(&recv_full[sb], kRowsQ * kNT * 4);
-            }
-            ptx::tmem_ld_wait();
-            const int nvalid = min(kNT, n_b - j * kNT);
-            float s[16];  // raw scores S_0 + S_1 (scale folded into the exponent below)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float4 v = ptx::lds_f4(recv_base + recv_slot(sb, qd, k, lane));
-                s[4 * k + 0] = __uint_as_float(sr[4 * k + 0]) + v.x;
-                s[4 * k + 1] = __uint_as_float(sr[4 * k + 1]) + v.y;
-                s[4 * k + 2] = __uint_as_float(sr[4 * k + 2]) + v.z;
-                s[4 * k + 3] = __uint_as_float(sr[4 * k + 3]) + v.w;
-            }
-            if (nvalid < kNT) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (8 * k + cpair + (i & 1) >= nvalid) s[4 * k + i] = neg_inf;
-            }
-            float xa = fmaxf(fmaxf(s[0], s[1]), fmaxf(s[4], s[5]));
-            float xb = fmaxf(fmaxf(s[2], s[3]), fmaxf(s[6], s[7]));
-            xa = fmaxf(xa, fmaxf(fmaxf(s[8], s[9]), fmaxf(s[12], s[13])));
-            xb = fmaxf(xb, fmaxf(fmaxf(s[10], s[11]), fmaxf(s[14], s[15])));
-            xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 1));
-            xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 1));
-            xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
-            xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 2));
-            // every value read from recv[sb] has reached a register (the shuffles above
-            // consumed them), so the peer may refill the buffer
-            if (lane == 0) ptx::mbar_arrive_remote(peer_recv_free0 + sb * 8);
-            uint32_t need = 0;
-            float alpha_a = 1.f, alpha_b = 1.f;
-            // lazy rescale: the reference max only moves when the tile max exceeds it
-            // by more than 2^8 in probability (identical decision in all 4 quad threads
-            // and in both CTAs of the cluster)
-            if ((xa - m_a) * scale_log2 > kRescaleThreshold) {
-                need = 1;
-                alpha_a = ptx::ex2((m_a - xa) * scale_log2);  // 0 on the first tile
-                l_a *= alpha_a;
-                m_a = xa;
-            }
-            if ((xb - m_b) * scale_log2 > kRescaleThreshold) {
-                need = 1;
-                alpha_b = ptx::ex2((m_b - xb) * scale_log2);
-                l_b *= alpha_b;
-                m_b = xb;
-            }
-            if ((lane & 3) == 0) {
-                s_alpha[sb * 64 + ra] = alpha_a;
-                s_alpha[sb * 64 + rb] = alpha_b;
-            }
-            const float ma_s = m_a * scale_log2, mb_s = m_b * scale_log2;
-            uint32_t pa[4], pb[4];
-            float sa = 0.f, sbs = 0.f;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float p0 = ptx::ex2(fmaf(s[4 * k], scale_log2, -ma_s));
-                const float p1 = ptx::ex2(fmaf(s[4 * k + 1], scale_log2, -ma_s));
-                const float p2 = ptx::ex2(fmaf(s[4 * k + 2], scale_log2, -mb_s));
-                const float p3 = ptx::ex2(fmaf(s[4 * k + 3], scale_log2, -mb_s));
-                sa += p0 + p1;
-                sbs += p2 + p3;
-                pa[k] = pack_bf16x2(p0, p1);
-                pb[k] = pack_bf16x2(p2, p3);
-            }
-            sa += __shfl_xor_sync(0xffffffffu, sa, 1);
-            sbs += __shfl_xor_sync(0xffffffffu, sbs, 1);
-            sa += __shfl_xor_sync(0xffffffffu, sa, 2);
-            sbs += __shfl_xor_sync(0xffffffffu, sbs, 2);
-            l_a += sa;
-            l_b += sbs;
-            if (warp == 2 && lane == 0) ELA_TRACE(12, j);
-            // P[sb] is free once O(j-2) has consumed it
-            ptx::mbar_wait(&p_empty[sb], par ^ 1);
-            {
-                uint8_t* P = sP + sb * 8192;
+                ptx::tmem_ld_wait();
+                const int nvalid = min(kNT, n_b - j * kNT);
+                float s[16];  // raw scores S_0 + S_1 (scale folded into the exponent below)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    *reinterpret_cast<uint32_t*>(P + ra * 128 + ((k ^ (ra & 7)) << 4) + 2 * cpair) = pa[k];
-                    *reinterpret_cast<uint32_t*>(P + rb * 128 + ((k ^ (rb & 7)) << 4) + 2 * cpair) = pb[k];
+                    const float4 v = ptx::lds_f4(recv_base + recv_slot(sb, qd, k, lane));
+                    s[4 * k + 0] = __uint_as_float(sr[4 * k + 0]) + v.x;
+                    s[4 * k + 1] = __uint_as_float(sr[4 * k + 1]) + v.y;
+                    s[4 * k + 2] = __uint_as_float(sr[4 * k + 2]) + v.z;
+                    s[4 * k + 3] = __uint_as_float(sr[4 * k + 3]) + v.w;
                 }
-            }
-            if (zero_tail && j == T - 1) {
-                // rows n_b.. of the last tile are in-bounds padding of H_b: zero them
-                // before they meet P = 0 in the MMA (0 * NaN would poison O).
-                const int r0 = n_b - j * kNT;
-                const int tid = int(threadIdx.x) - 64;
-                const int per_chunk = (kNT - r0) * 8;
-                for (int idx = tid; idx < UNITS * 2 * per_chunk; idx += 128) {
-                    const int ch = idx / per_chunk, rem = idx % per_chunk;
-                    const int r = r0 + rem / 8, c16 = rem % 8;
-                    const int sl = (j * UNITS + ch / 2) % kRing;
-                    *reinterpret_cast<uint4*>(ring + sl * kUnitBytes + (ch & 1) * kChunkBytes + r * 128 + c16 * 16) =
-                        make_uint4(0, 0, 0, 0);
+                if (nvalid < kNT) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            if (8 * k + cpair + (i & 1) >= nvalid) s[4 * k + i] = neg_inf;
                 }
-            }
-            const uint32_t any = softmax_bar_or(need);
-            // consume o_done phases in order (one per tile) so the parity wait is exact;
-            // O(j-1) was issued a full stage ago, so this rarely blocks
-            if (j > 0) ptx::mbar_wait(o_done, (j - 1) & 1);
-            if (any && j > 0) {
-                // lazy rescale of the running O^T columns (O(j-1) complete): O *= alpha
-                ptx::tc_fence_after();
-#pragma unroll 1
-                for (int m = 0; m < UNITS; ++m) {
+                float xa = fmaxf(fmaxf(s[0], s[1]), fmaxf(s[4], s[5]));
+                float xb = fmaxf(fmaxf(s[2], s[3]), fmaxf(s[6], s[7]));
+                xa = fmaxf(xa, fmaxf(fmaxf(s[8], s[9]), fmaxf(s[12], s[13])));
+                xb = fmaxf(xb, fmaxf(fmaxf(s[10], s[11]), fmaxf(s[14], s[15])));
+                xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 1));
+                xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 1));
+                xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
+                xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 2));
+                // every value read from recv[sb] has reached a register (the shuffles above
+                // consumed them), so the peer may refill the buffer
+                if (lane == 0) ptx::mbar_arrive_remote(peer_recv_free0 + sb * 8);
+                uint32_t need = 0;
+                float alpha_a = 1.f, alpha_b = 1.f;
+                // lazy rescale: the reference max only moves when the tile max exceeds it
+                // by more than 2^8 in probability (identical decision in all 4 quad threads
+                // and in both CTAs of the cluster)
+                if ((xa - m_a) * scale_log2 > kRescaleThreshold) {
+                    need = 1;
+                    alpha_a = ptx::ex2((m_a - xa) * scale_log2);  // 0 on the first tile
+                    l_a *= alpha_a;
+                    m_a = xa;
+                }
+                if ((xb - m_b) * scale_log2 > kRescaleThreshold) {
+                    need = 1;
+                    alpha_b = ptx::ex2((m_b - xb) * scale_log2);
+                    l_b *= alpha_b;
+                    m_b = xb;
+                }
+                if ((lane & 3) == 0) {
+                    s_alpha[sb * 64 + ra] = alpha_a;
+                    s_alpha[sb * 64 + rb] = alpha_b;
+                }
+                const float ma_s = m_a * scale_log2, mb_s = m_b * scale_log2;
+                uint32_t pa[4], pb[4];
+                float sa = 0.f, sbs = 0.f;
 #pragma unroll
-                    for (int c0 = 0; c0 < 64; c0 += 16) {
-                        uint32_t r[16];
-                        ptx::tmem_ld16(t_lane + m * 64 + c0, r);
-                        ptx::tmem_ld_wait();
+                for (int k = 0; k < 4; ++k) {
+                    const float p0 = ptx::ex2(fmaf(s[4 * k], scale_log2, -ma_s));
+                    const float p1 = ptx::ex2(fmaf(s[4 * k + 1], scale_log2, -ma_s));
+                    const float p2 = ptx::ex2(fmaf(s[4 * k + 2], scale_log2, -mb_s));
+                    const float p3 = ptx::ex2(fmaf(s[4 * k + 3], scale_log2, -mb_s));
+                    sa += p0 + p1;
+                    sbs += p2 + p3;
+                    pa[k] = pack_bf16x2(p0, p1);
+                    pb[k] = pack_bf16x2(p2, p3);
+                }
+                sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+                sbs += __shfl_xor_sync(0xffffffffu, sbs, 1);
+                sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+                sbs += __shfl_xor_sync(0xffffffffu, sbs, 2);
+                l_a += sa;
+                l_b += sbs;
+                if (warp == 2 && lane == 0) ELA_TRACE(12, Gt);
+                // P[sb] is free once O(Gt-2) has consumed it
+                ptx::mbar_wait(&p_empty[sb], par ^ 1);
+                {
+                    uint8_t* P = sP + sb * 8192;
 #pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            r[i] = __float_as_uint(__uint_as_float(r[i]) * s_alpha[sb * 64 + c0 + i]);
-                        ptx::tmem_st16(t_lane + m * 64 + c0, r);
+                    for (int k = 0; k < 4; ++k) {
+                        *reinterpret_cast<uint32_t*>(P + ra * 128 + ((k ^ (ra & 7)) << 4) + 2 * cpair) = pa[k];
+                        *reinterpret_cast<uint32_t*>(P + rb * 128 + ((k ^ (rb & 7)) << 4) + 2 * cpair) = pb[k];
                     }
                 }
-                ptx::tmem_st_wait();
-            }
-            ptx::fence_proxy_async_smem();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
-            if (warp == 2 && lane == 0) ELA_TRACE(13, j);
-        }
-
-        // ---- epilogue: C[b*rows + q][dm_off + d] = O^T[d][q] / l_q.
-        // O^T comes out of TMEM with tcgen05.ld.16x256b (thread t: lanes d = t/4, t/4+8,
-        // columns q = 2(t%4)+{0,1} per 8-column group), i.e. already in the 8x8 bf16
-        // fragment layout of stmatrix; stmatrix.trans writes the transpose into a
-        // [64 q][128 d] smem stage (row pitch 272 B: conflict-free), which is then stored
-        // to global memory as coalesced 16-byte vectors.
-        if (warp == 2 && lane == 0) ELA_TRACE(14, 0);
-        if ((lane & 3) == 0) {
-            s_l[ra] = 1.f / l_a;
-            s_l[rb] = 1.f / l_b;
-        }
-        if (T > 0) {
-            ptx::mbar_wait(o_full, 0);
-            ptx::tc_fence_after();
-        }
-        softmax_bar_sync();
-        constexpr int kPitch = 272;  // bytes per staged q row (256 + 16)
-        const int tid = int(threadIdx.x) - 64;
-        float inv_l[16];  // 1/l for this thread's columns q = 8k + 2(t%4) + {0,1}
+                if (zero_tail && j == T - 1) {
+                    // rows n_b.. of the last tile are in-bounds padding of H_b: zero them
+                    // before they meet P = 0 in the MMA (0 * NaN would poison O).
+                    const int r0 = n_b - j * kNT;
+                    const int tid = int(threadIdx.x) - 64;
+                    const int per_chunk = (kNT - r0) * 8;
+                    for (int idx = tid; idx < UNITS * 2 * per_chunk; idx += 128) {
+                        const int ch = idx / per_chunk, rem = idx % per_chunk;
+                        const int r = r0 + rem / 8, c16 = rem % 8;
+                        const int sl = (Gt * UNITS + ch / 2) % kRing;
+                        *reinterpret_cast<uint4*>(ring + sl * kUnitBytes + (ch & 1) * kChunkBytes + r * 128 +
+                                                  c16 * 16) = make_uint4(0, 0, 0, 0);
+                    }
+                }
+                const uint32_t any = softmax_bar_or(need);
+                // consume o_done phases in order (one per tile) so the parity wait is exact;
+                // O(Gt-1) was issued a full stage ago, so this rarely blocks
+                if (Gt > 0) ptx::mbar_wait(o_done, (Gt - 1) & 1);
+                if (any && j > 0) {
+                    // lazy rescale of the running O^T columns (O(Gt-1) complete): O *= alpha
+                    ptx::tc_fence_after();
+#pragma unroll 1
+                    for (int m = 0; m < UNITS; ++m) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float2 v = *reinterpret_cast<const float2*>(s_l + 8 * k + cpair);
-            inv_l[2 * k] = v.x, inv_l[2 * k + 1] = v.y;
-        }
-        const uint32_t stmatrix_row = uint32_t((lane & 7) * kPitch + (int(qd) * 32 + int(lane >> 3) * 8) * 2);
-        for (int m = 0; m < UNITS; ++m) {
-            uint8_t* stage = ring + (m & 1) * (64 * kPitch);
-            const uint32_t stage_base = ptx::smem_u32(stage) + stmatrix_row;
-            uint32_t lo[32], hi[32];  // lanes d 0..15 and 16..31 of this warp's quadrant
-            if (T > 0) {
+                        for (int c0 = 0; c0 < 64; c0 += 16) {
+                            uint32_t r[16];
+                            ptx::tmem_ld16(t_lane + m * 64 + c0, r);
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                r[i] = __float_as_uint(__uint_as_float(r[i]) * s_alpha[sb * 64 + c0 + i]);
+                            ptx::tmem_st16(t_lane + m * 64 + c0, r);
+                        }
+                    }
+                    ptx::tmem_st_wait();
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
+                if (warp == 2 && lane == 0) ELA_TRACE(13, Gt);
+            }
+
+            // ---- epilogue: C[b*rows + q][dm_off + d] = O^T[d][q] / l_q.
+            // O^T comes out of TMEM with tcgen05.ld.16x256b (thread t: lanes d = t/4,
+            // t/4+8, columns q = 2(t%4)+{0,1} per 8-column group), i.e. already in the
+            // 8x8 bf16 fragment layout of stmatrix; stmatrix.trans turns each 8(q) x 32(d)
+            // slab into rows of a tiny per-warp stage, re-read as one 16-byte vector per
+            // lane and stored.  No CTA-wide barrier: the next input streams meanwhile.
+            if (warp == 2 && lane == 0) ELA_TRACE(14, li);
+            if ((lane & 3) == 0) {
+                s_l[ra] = 1.f / l_a;
+                s_l[rb] = 1.f / l_b;
+            }
+            softmax_bar_sync();
+            float inv_l[16];  // 1/l for this thread's columns q = 8k + 2(t%4) + {0,1}
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float2 v = *reinterpret_cast<const float2*>(s_l + 8 * k + cpair);
+                inv_l[2 * k] = v.x, inv_l[2 * k + 1] = v.y;
+            }
+            ptx::mbar_wait(o_full, li & 1);
+            ptx::tc_fence_after();
+            for (int m = 0; m < UNITS; ++m) {
+                uint32_t lo[32], hi[32];  // lanes d 0..15 and 16..31 of this warp's quadrant
                 ptx::tmem_ld_16x256b_x8(t_lane + m * 64, lo);
                 ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16) + m * 64, hi);
                 ptx::tmem_ld_wait();
+                if (m == UNITS - 1) {  // O read out: the next input may overwrite it
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(o_free);
+                }
+                const int d_base = dm_off + m * 128 + int(qd) * 32;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {  // query columns 8k..8k+7
+                    uint32_t f[4];
+                    const uint32_t* src[2] = {lo, hi};
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            const uint32_t* r = src[h2] + 4 * k + 2 * half;
+                            f[2 * h2 + half] = pack_bf16x2(__uint_as_float(r[0]) * inv_l[2 * k],
+                                                           __uint_as_float(r[1]) * inv_l[2 * k + 1]);
+                        }
+                    // matrices j = 0..3 cover d = 8j..8j+7; transposed rows are q = 8k + i
+                    ptx::stmatrix_x4_trans(stm_addr, f[0], f[1], f[2], f[3]);
+                    __syncwarp();
+                    const int qq = 8 * k + int(lane >> 2);
+                    const uint4 v = *reinterpret_cast<const uint4*>(my_stage + (lane >> 2) * kEpiPitch +
+                                                                    (lane & 3) * 16);
+                    if (qq < rows)
+                        *reinterpret_cast<uint4*>(ctx + (int64_t(b) * rows + qq) * d_m + d_base + (lane & 3) * 8) = v;
+                    __syncwarp();
+                }
             }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {  // query columns 8k..8k+7
-                uint32_t f[4];
-                const uint32_t* src[2] = {lo, hi};
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        const uint32_t* r = src[h2] + 4 * k + 2 * half;
-                        const float v0 = T > 0 ? __uint_as_float(r[0]) * inv_l[2 * k] : __int_as_float(0x7fc00000);
-                        const float v1 = T > 0 ? __uint_as_float(r[1]) * inv_l[2 * k + 1] : __int_as_float(0x7fc00000);
-                        f[2 * h2 + half] = pack_bf16x2(v0, v1);
-                    }
-                // matrices j = 0..3 cover d = 8j..8j+7 of the quadrant; transposed rows are q = 8k + i
-                ptx::stmatrix_x4_trans(stage_base + uint32_t(8 * k * kPitch), f[0], f[1], f[2], f[3]);
-            }
-            softmax_bar_sync();
-            // 64 rows x 256 B = 1024 16-byte vectors, 8 per thread
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-                const int idx = tid + v * 128;
-                const int qq = idx >> 4, c16 = idx & 15;
-                if (qq < rows)
-                    *reinterpret_cast<uint4*>(ctx + (int64_t(b) * rows + qq) * d_m + dm_off + m * 128 + c16 * 8) =
-                        *reinterpret_cast<const uint4*>(stage + qq * kPitch + c16 * 16);
-            }
+            if (warp == 2 && lane == 0) ELA_TRACE(15, li);
+            G += T;
+            ++li;
         }
-        if (warp == 2 && lane == 0) ELA_TRACE(15, 0);
+        // inputs whose context length is out of contract: loud NaN rows
+        for (int b = cl; b < B; b += ncl) {
+            if (tiles_of(n_per_input, b, n_stride) != 0) continue;
+            const int tid = int(threadIdx.x) - 64;
+            for (int e = tid; e < rows * dm_half; e += 128)
+                ctx[(int64_t(b) * rows + e / dm_half) * d_m + dm_off + e % dm_half] =
+                    __float2bfloat16_rn(__int_as_float(0x7fc00000));
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -598,6 +653,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<kTmemCols>(tmem);
     }
+#undef ELA_TRACE
+}
+
+int num_sms_decode() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
 }
 
 template <int UNITS>
@@ -616,9 +681,11 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     auto kern = el_decode_tc_kernel<UNITS>;
     constexpr uint32_t smem = DecLayout<UNITS>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<dim3(2 * B), kThreads, smem, st>>>(tq, th, static_cast<const __nv_bfloat16*>(qp), B * rows, npi, rows,
-                                               n_stride, d_m, scale_log2,
-                                               static_cast<__nv_bfloat16*>(ctx), g_decode_trace, g_tuning);
+    // persistent: one cluster per pair of SMs (or per input when there are fewer)
+    const int clusters = B < num_sms_decode() / 2 ? B : num_sms_decode() / 2;
+    kern<<<dim3(2 * clusters), kThreads, smem, st>>>(tq, th, static_cast<const __nv_bfloat16*>(qp), npi, B, rows,
+                                                     n_stride, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx),
+                                                     g_decode_trace, g_tuning);
     ELA_CHECK_LAUNCH();
 }
 

@@ -1,14 +1,19 @@
-// tc_gemm.cu — tcgen05 GEMM for the projection stages of the bf16 path.
+// tc_gemm.cu — persistent tcgen05 GEMM for the projection stages of the bf16 path.
 //
 //   C[z][m][n] = alpha * sum_k A[z][m][k] * B[z][n][k] + bias[z][n]     (bf16 in/out)
 //
 // Replaces the reference's CPU matmuls of query expansion (attention.hpp:205-206:
 // q.Wq_i + bq_i, Q_i.Wk_i^T) and of the output projection (:286, :221-231:
-// ctx.Wv_i + bv_i, then .Wo + bo).  One 128 x BN output tile per CTA:
-// a TMA producer (warp 0) streams 128x64 / BNx64 bf16 K-slices (SWIZZLE_128B)
-// through a 4-stage mbarrier ring, a single thread (warp 1) issues
-// tcgen05.mma (M=128, N=BN, K=16) into a TMEM fp32 accumulator, and all four
-// warps run the epilogue (tcgen05.ld -> alpha/bias -> bf16 -> st.global).
+// ctx.Wv_i + bv_i, then .Wo + bo).
+//
+// Persistent, warp-specialised: one CTA per SM walks 128 x BN output tiles
+// (n fastest, so consecutive tiles reuse the A block from L2).
+//   warp 0      TMA producer: 128x64 / BNx64 bf16 K-slices (SWIZZLE_128B) through a
+//               4-stage mbarrier ring;
+//   warp 1      MMA issuer (tcgen05.mma M=128 N=BN K=16, fp32 accumulator in TMEM,
+//               double-buffered so the epilogue of tile t overlaps the MMAs of t+1);
+//   warps 2..5  epilogue: tcgen05.ld -> alpha/bias -> bf16 -> padded smem stage ->
+//               coalesced 16-byte global stores.
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx_sm100.cuh"
@@ -18,19 +23,24 @@ namespace elattn_gpu {
 
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kStages = 4;
+constexpr int kBM = 128, kBK = 64;
+constexpr int kThreads = 192;
 
 template <int BN>
 struct GemmSmem {
+    static constexpr int kStages = BN >= 128 ? 5 : 7;  // deepest ring that fits next to the stage
     static constexpr uint32_t kABytes = kBM * kBK * 2;
     static constexpr uint32_t kBBytes = BN * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    static constexpr uint32_t kBarOff = kStages * kStageBytes;
+    static constexpr int kPitch = BN * 2 + 16;  // staged output row (bytes), +16 spreads banks
+    static constexpr uint32_t kStageOff = kStages * kStageBytes;
+    static constexpr uint32_t kBarOff = kStageOff + kBM * kPitch;
     static constexpr uint32_t kTotal = kBarOff + 256 + 1024;  // + barriers + alignment slack
 };
 
 struct GemmParams {
-    int M, N, K;
+    int M, N, K, Z;
+    int tiles_m, tiles_n;
     float alpha;
     const float* bias;
     int64_t sbz;
@@ -39,23 +49,40 @@ struct GemmParams {
     int a_zm, b_zm;  // 1: tensor map coordinate order is (k, z, m) instead of (k, m, z)
 };
 
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
 template <int BN>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
     using S = GemmSmem<BN>;
+    constexpr int kStages = S::kStages;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B, by offsetting the __shared__ array itself so
     // the compiler keeps the shared address space (LDS/STS, not generic LD/ST)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* stage = smem + S::kStageOff;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOff);
     uint64_t* empty = full + kStages;
-    uint64_t* accum_full = empty + kStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
-    constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+    uint64_t* acc_full = empty + kStages;  // [2] MMA -> epilogue
+    uint64_t* acc_empty = acc_full + 2;    // [2] epilogue -> MMA
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-    const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN, z = blockIdx.z;
     const int num_k = p.K / kBK;
+    const int num_tiles = p.Z * p.tiles_m * p.tiles_n;
+    auto tile_coords = [&](int t, int& z, int& m0, int& n0) {
+        const int per_z = p.tiles_m * p.tiles_n;
+        z = t / per_z;
+        const int r = t % per_z;
+        m0 = (r / p.tiles_n) * kBM;
+        n0 = (r % p.tiles_n) * BN;
+    };
 
     if (warp == 0) {
         if (ptx::elect_one()) {
@@ -65,7 +92,10 @@ __global__ void __launch_bounds__(128, 1)
                 ptx::mbar_init(&full[s], 1);
                 ptx::mbar_init(&empty[s], 1);
             }
-            ptx::mbar_init(accum_full, 1);
+            for (int i = 0; i < 2; ++i) {
+                ptx::mbar_init(&acc_full[i], 1);
+                ptx::mbar_init(&acc_empty[i], 4);
+            }
             ptx::fence_mbar_init();
         }
         __syncwarp();
@@ -78,95 +108,126 @@ __global__ void __launch_bounds__(128, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (ptx::elect_one()) {  // ---- TMA producer
-            for (int kb = 0; kb < num_k; ++kb) {
-                const int s = kb % kStages;
-                const uint32_t ph = (kb / kStages) & 1;
-                ptx::mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* a = smem + s * S::kStageBytes;
-                uint8_t* b = a + S::kABytes;
-                ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
-                if (p.a_zm)
-                    ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, z, m0, ptx::kEvictNormal);
-                else
-                    ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, m0, z, ptx::kEvictNormal);
-                if (p.b_zm)
-                    ptx::tma_load_3d(b, &tmB, &full[s], kb * kBK, z, n0, ptx::kEvictLast);
-                else
-                    ptx::tma_load_3d(b, &tmB, &full[s], kb * kBK, n0, z, ptx::kEvictLast);
+        // ---- TMA producer
+        if (ptx::elect_one()) {
+            int it = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                int z, m0, n0;
+                tile_coords(t, z, m0, n0);
+                for (int kb = 0; kb < num_k; ++kb, ++it) {
+                    const int s = it % kStages;
+                    ptx::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+                    uint8_t* a = smem + s * S::kStageBytes;
+                    uint8_t* b = a + S::kABytes;
+                    ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
+                    if (p.a_zm)
+                        ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, z, m0, ptx::kEvictNormal);
+                    else
+                        ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, m0, z, ptx::kEvictNormal);
+                    if (p.b_zm)
+                        ptx::tma_load_3d(b, &tmB, &full[s], kb * kBK, z, n0, ptx::kEvictLast);
+                    else
+                        ptx::tma_load_3d(b, &tmB, &full[s], kb * kBK, n0, z, ptx::kEvictLast);
+                }
             }
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (ptx::elect_one()) {  // ---- MMA issuer
-            constexpr uint32_t idesc = ptx::idesc_bf16(kBM, BN, 0, 0);
-            for (int kb = 0; kb < num_k; ++kb) {
-                const int s = kb % kStages;
-                const uint32_t ph = (kb / kStages) & 1;
-                ptx::mbar_wait(&full[s], ph);
+        // ---- MMA issuer (whole warp loops; lane 0 issues and commits)
+        constexpr uint32_t idesc = ptx::idesc_bf16(kBM, BN, 0, 0);
+        const uint64_t d0 = ptx::sdesc_sw128(ptx::smem_u32(smem), 0, 1024);
+        int it = 0, local = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+            const int ab = local & 1;
+            ptx::mbar_wait(&acc_empty[ab], ((local >> 1) & 1) ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem + ab * BN;
+            for (int kb = 0; kb < num_k; ++kb, ++it) {
+                const int s = it % kStages;
+                ptx::mbar_wait(&full[s], (it / kStages) & 1);
                 ptx::tc_fence_after();
-                const uint32_t a = ptx::smem_u32(smem + s * S::kStageBytes);
-                const uint32_t b = a + S::kABytes;
+                if (lane == 0) {
+                    const uint64_t a = d0 + uint64_t((s * S::kStageBytes) >> 4);
+                    const uint64_t b = a + uint64_t(S::kABytes >> 4);
 #pragma unroll
-                for (int k = 0; k < kBK / 16; ++k)
-                    ptx::mma_bf16(tmem, ptx::sdesc_sw128(a + 32 * k, 0, 1024), ptx::sdesc_sw128(b + 32 * k, 0, 1024),
-                                  idesc, (kb | k) != 0);
-                ptx::mma_commit(&empty[s]);
+                    for (int k = 0; k < kBK / 16; ++k)
+                        ptx::mma_bf16(d, a + uint64_t(2 * k), b + uint64_t(2 * k), idesc, (kb | k) != 0);
+                    ptx::mma_commit(&empty[s]);
+                }
+                __syncwarp();
             }
-            ptx::mma_commit(accum_full);
+            if (lane == 0) ptx::mma_commit(&acc_full[ab]);
+            __syncwarp();
         }
-        __syncwarp();
-    }
-
-    // ---- epilogue: TMEM -> registers (thread = row) -> alpha/bias -> bf16 -> smem
-    // staging tile (the drained A/B stages) -> coalesced 16-byte global stores.
-    ptx::mbar_wait(accum_full, 0);
-    ptx::tc_fence_after();
-    constexpr int kPitch = BN * 2 + 16;  // bytes per staged row (+16: spread banks)
-    static_assert(kBM * kPitch <= kStages * S::kStageBytes, "staging tile fits in the pipeline buffers");
-    const int r_local = int(warp) * 32 + int(lane);
-    const uint32_t t_row = tmem + ((warp * 32) << 16);
-    const float* bias = p.bias ? p.bias + z * p.sbz : nullptr;
+    } else {
+        // ---- epilogue warps 2..5: TMEM lane quadrant = warp % 4 -> output rows
+        const uint32_t qd = warp & 3;
+        const int r_local = int(qd) * 32 + int(lane);
+        const int tid = int(threadIdx.x) - 64;
+        int local = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+            int z, m0, n0;
+            tile_coords(t, z, m0, n0);
+            const int ab = local & 1;
+            ptx::mbar_wait(&acc_full[ab], (local >> 1) & 1);
+            ptx::tc_fence_after();
+            const uint32_t t_row = tmem + ((qd * 32) << 16) + ab * BN;
+            const float* bias = p.bias ? p.bias + z * p.sbz : nullptr;
+            epi_bar_sync();  // the stage is free (previous tile's global stores done)
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
-        ptx::tmem_ld16(t_row + c0, r);
-        ptx::tmem_ld_wait();
-        const int n = n0 + c0;
-        uint32_t packed[8];
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r[32];
+                ptx::tmem_ld16(t_row + c0, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+                ptx::tmem_ld16(t_row + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+                ptx::tmem_ld_wait();
+                if (c0 + 32 >= BN) {
+                    // accumulator fully read: let the MMA warp reuse it
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
+                }
+                const int n = n0 + c0;
+                uint32_t packed[16];
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-            float v0 = __uint_as_float(r[j]) * p.alpha, v1 = __uint_as_float(r[j + 1]) * p.alpha;
-            if (bias) {
-                v0 += (n + j < p.N) ? bias[n + j] : 0.f;
-                v1 += (n + j + 1 < p.N) ? bias[n + j + 1] : 0.f;
+                for (int j = 0; j < 32; j += 2) {
+                    float v0 = __uint_as_float(r[j]) * p.alpha, v1 = __uint_as_float(r[j + 1]) * p.alpha;
+                    if (bias) {
+                        v0 += (n + j < p.N) ? bias[n + j] : 0.f;
+                        v1 += (n + j + 1 < p.N) ? bias[n + j + 1] : 0.f;
+                    }
+                    packed[j / 2] = pack2(v0, v1);
+                }
+                uint8_t* dst = stage + r_local * S::kPitch + c0 * 2;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    *reinterpret_cast<uint4*>(dst + 16 * q) =
+                        make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
             }
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
-            packed[j / 2] = *reinterpret_cast<uint32_t*>(&h2);
-        }
-        uint8_t* dst = smem + r_local * kPitch + c0 * 2;
-        *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        *reinterpret_cast<uint4*>(dst + 16) = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-    }
-    __syncthreads();
-    constexpr int kVecPerRow = BN / 8;  // 16-byte vectors per output row
-    const bool full_n = (n0 + BN <= p.N) && (p.N % 8 == 0);
+            epi_bar_sync();
+            constexpr int kVecPerRow = BN / 8;  // 16-byte vectors per output row
+            const bool full_n = (n0 + BN <= p.N);
 #pragma unroll 4
-    for (int idx = int(threadIdx.x); idx < kBM * kVecPerRow; idx += 128) {
-        const int rr = idx / kVecPerRow, cv = idx % kVecPerRow;
-        const int row = m0 + rr, n = n0 + cv * 8;
-        if (row >= p.M) continue;
-        __nv_bfloat16* Crow = p.C + z * p.sCz + int64_t(row) * p.ldc;
-        const uint8_t* src = smem + rr * kPitch + cv * 16;
-        if (full_n || n + 8 <= p.N) {
-            *reinterpret_cast<uint4*>(Crow + n) = *reinterpret_cast<const uint4*>(src);
-        } else {
-            for (int j = 0; j < 8 && n + j < p.N; ++j) Crow[n + j] = reinterpret_cast<const __nv_bfloat16*>(src)[j];
+            for (int idx = tid; idx < kBM * kVecPerRow; idx += 128) {
+                const int rr = idx / kVecPerRow, cv = idx % kVecPerRow;
+                const int row = m0 + rr, n = n0 + cv * 8;
+                if (row >= p.M) continue;
+                __nv_bfloat16* Crow = p.C + z * p.sCz + int64_t(row) * p.ldc;
+                const uint8_t* src = stage + rr * S::kPitch + cv * 16;
+                if (full_n || n + 8 <= p.N) {
+                    *reinterpret_cast<uint4*>(Crow + n) = *reinterpret_cast<const uint4*>(src);
+                } else {
+                    for (int j = 0; j < 8 && n + j < p.N; ++j)
+                        Crow[n + j] = reinterpret_cast<const __nv_bfloat16*>(src)[j];
+                }
+            }
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<kTmemCols>(tmem);
+    }
 }
 
 // 3-D map over an operand X[z][r][k] (r = M or N rows, k contiguous):
@@ -190,18 +251,30 @@ CUtensorMap operand_map(const void* base, int64_t ld, int64_t sz, int rows, int 
     return make_tmap_bf16(base, 3, dims, strides, box);
 }
 
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
 template <int BN>
 void launch_bn(const GemmArgs& g, cudaStream_t st) {
     GemmParams p{};
-    p.M = g.M, p.N = g.N, p.K = g.K, p.alpha = g.alpha, p.bias = g.bias, p.sbz = g.sbz;
+    p.M = g.M, p.N = g.N, p.K = g.K, p.Z = g.Z, p.alpha = g.alpha, p.bias = g.bias, p.sbz = g.sbz;
     p.C = static_cast<__nv_bfloat16*>(g.C), p.ldc = g.ldc, p.sCz = g.sCz;
+    p.tiles_m = int(ceil_div(g.M, kBM));
+    p.tiles_n = int(ceil_div(g.N, BN));
     CUtensorMap ta = operand_map(g.A, g.lda, g.sAz, g.M, g.K, g.Z, kBM, &p.a_zm);
     CUtensorMap tb = operand_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, BN, &p.b_zm);
     auto kern = tc_gemm_kernel<BN>;
     constexpr uint32_t smem = GemmSmem<BN>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    dim3 grid(unsigned(ceil_div(g.N, BN)), unsigned(ceil_div(g.M, kBM)), unsigned(g.Z));
-    kern<<<grid, 128, smem, st>>>(ta, tb, p);
+    const int tiles = p.Z * p.tiles_m * p.tiles_n;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    kern<<<grid, kThreads, smem, st>>>(ta, tb, p);
     ELA_CHECK_LAUNCH();
 }
 

@@ -1,0 +1,61 @@
+"""CUDA-event timing of the four projection GEMM shapes of one BART layer step."""
+import argparse
+import ctypes
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import torch  # noqa: E402
+
+from paper_2105_04779_b200 import capi  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--B", type=int, default=320)
+ap.add_argument("--reps", type=int, default=20)
+a = ap.parse_args()
+L = capi.lib()
+vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+L.elattn_gpu_testing_gemm_bf16.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, i64, vp, i64,
+                                           i32, i32, i32, i32, ctypes.c_float, i32, vp]
+h, d_m, d_k, x = 16, 1024, 64, 4
+R = a.B * x
+bf = torch.bfloat16
+dev = "cuda"
+Y = torch.randn(R, d_m, device=dev).to(bf)
+Q = torch.randn(R, h * d_k, device=dev).to(bf)
+qp = torch.empty(R * h, d_m, device=dev, dtype=bf)
+ctx = torch.randn(R * h, d_m, device=dev).to(bf)
+V = torch.empty(R, h * d_k, device=dev, dtype=bf)
+out = torch.empty(R, d_m, device=dev, dtype=bf)
+WqT = torch.randn(h * d_k, d_m, device=dev).to(bf)
+Wk = torch.randn(h, d_m, d_k, device=dev).to(bf)
+WvT = torch.randn(h, d_k, d_m, device=dev).to(bf)
+WoT = torch.randn(d_m, h * d_k, device=dev).to(bf)
+bias = torch.randn(max(h * d_k, d_m), device=dev)
+st = torch.cuda.current_stream().cuda_stream
+shapes = {
+    "Q=Y.Wq": (Y, d_m, 0, WqT, d_m, 0, Q, h * d_k, 0, bias, 0, R, h * d_k, d_m, 1),
+    "q'=Q_i.Wk_i^T": (Q, h * d_k, d_k, Wk, d_k, d_m * d_k, qp, h * d_m, d_m, None, 0, R, d_m, d_k, h),
+    "V_i=C_i.Wv_i": (ctx, h * d_m, d_m, WvT, d_m, d_k * d_m, V, h * d_k, d_k, bias, d_k, R, d_k, d_m, h),
+    "out=V.Wo": (V, h * d_k, 0, WoT, h * d_k, 0, out, d_m, 0, bias, 0, R, d_m, h * d_k, 1),
+}
+for name, (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z) in shapes.items():
+    def run():
+        capi.check(L.elattn_gpu_testing_gemm_bf16(A.data_ptr(), lda, sAz, Bm.data_ptr(), ldb, sBz, C.data_ptr(), ldc,
+                                                  sCz, bs.data_ptr() if bs is not None else None, sbz, M, N, K, Z,
+                                                  1.0, 1, st))
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.reps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / a.reps * 1e3
+    byt = (M * K * Z + N * K * Z + M * N * Z) * 2
+    print(json.dumps({"gemm": name, "us": round(us, 2), "GBps": round(byt / us / 1e3, 1),
+                      "TFLOPs": round(2 * M * N * K * Z / us / 1e6, 1)}))
