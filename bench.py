@@ -9,7 +9,7 @@ output projection; layer l+1 consumes layer l's output rows as its queries.
 
 metric: decoder-step attention tokens/s = (B*x) / t_step, summed over ranks.
 Weak scaling: every rank owns B inputs (its own H shard); no collective in the
-timed region; one NCCL all_gather of output checksums afterwards.
+timed region; one NCCL all_gather of the output rows afterwards (sharding.py).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -60,6 +60,18 @@ def layer_bytes_flops(B, x, n, d_m, h, d_k, bpv=2):
     byt = B * n * d_m * bpv + 4 * d_m * h * d_k * bpv + 2 * B * x * d_m * bpv
     flops = B * x * (4 * h * n * d_m + 8 * d_m * h * d_k)
     return byt, flops
+
+
+def traffic_from_profile(B, n, d_m):
+    """dram read+write bytes per decode launch from the committed ncu capture
+    (profiles/decode_traffic.json), when it was taken at this shape."""
+    try:
+        d = json.loads((ROOT / "profiles" / "decode_traffic.json").read_text())
+        if (d["B"], d["n"], d["d_m"]) == (B, n, d_m):
+            return d["traffic_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
 
 
 # ------------------------------------------------------------------ clocks
@@ -320,15 +332,14 @@ def gpu_arm(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * B * x / (float(te.item()) / 1e3)
 
-    # ---- gather outputs (checksums) to rank 0 over NCCL, outside the timed region
+    # ---- gather every rank's output rows over NCCL, outside the timed region
+    # (input sharding: rank r owns inputs [r*B, (r+1)*B) of the global batch)
+    from paper_2105_04779_b200.sharding import gather_outputs, shard_range
+
     out = step(Y0)
-    chk = out.float().sum().reshape(1)
-    if world > 1:
-        allc = [torch.zeros_like(chk) for _ in range(world)]
-        dist.all_gather(allc, chk)
-        finite = all(bool(torch.isfinite(v).all()) for v in allc)
-    else:
-        finite = bool(torch.isfinite(chk).all())
+    assert shard_range(world * B, rank, world) == (rank * B, (rank + 1) * B)
+    full = gather_outputs(out, world * B, x) if world > 1 else out
+    finite = bool(torch.isfinite(full.float()).all())
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -356,7 +367,7 @@ def gpu_arm(args):
                     "note": "through ElAttentionLayer.step (C ABI); Y H2D from pinned host + output D2H "
                             "every step; H (encoder state) resident, as in the reference's DecoderState"},
             "roofline": {"bound": "hbm", "achieved": dec_gbs, "peak": hbm, "unit": "GB/s",
-                         "frac": dec_gbs / hbm, "traffic": None, "peak_source": peak_src,
+                         "frac": dec_gbs / hbm, "traffic": traffic_from_profile(B, n, d_m), "peak_source": peak_src,
                          "kernel": "fused EL decode (stage 2)", "kernel_ms": dec_ms,
                          "algorithmic_bytes_per_launch": dec_bytes,
                          "step_roofline_frac": step_frac,

@@ -36,7 +36,11 @@ def test_library_is_sm100a_native():
     out = subprocess.run(["cuobjdump", "--list-elf", str(capi.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", str(capi.LIB_PATH)], capture_output=True, text=True).stdout
-    assert "HMMA" not in sass and "HGMMA" not in sass  # no legacy / Hopper tensor paths
+    # Blackwell-native evidence: tcgen05.mma (UTCHMMA), TMA (UTMALDG), TMEM ld/st (LDTM/STTM)
+    for op in ("UTCHMMA", "UTMALDG", "LDTM", "STTM"):
+        assert re.search(rf"\b{op}\b", sass), op
+    # and no legacy mma.sync / Hopper wgmma tensor paths
+    assert not re.search(r"(?<!UTC)\bHMMA\b", sass) and "HGMMA" not in sass
 
 
 def test_errors_without_device_are_statuses_not_crashes():
