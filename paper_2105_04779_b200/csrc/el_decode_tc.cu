@@ -54,8 +54,7 @@ constexpr int kUnitBytes = 8192;   // 32 rows x 128 d_m x bf16
 constexpr int kChunkBytes = 4096;  // 32 rows x 64 d_m
 constexpr int kThreads = 384;
 constexpr int kSBuf = 4;  // S accumulators in TMEM
-constexpr int kEpiPitch = 80;                  // per-warp epilogue stage: 8 q-rows x (32 d + pad)
-constexpr int kEpiWarpBytes = 8 * kEpiPitch;   // 640 B per softmax warp
+constexpr int kEpiWarpBytes = 4096;  // per-warp epilogue stage (64 q x 32 d bf16), aliases P
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max grows by > 2^8
 
 // Tuning knobs (runtime so they can be swept):
@@ -79,7 +78,7 @@ struct DecLayout {
     // shared memory
     static constexpr uint32_t kQBytes = kQSmemUnits * 2 * 8192;  // 64 rows x 128 d_m per unit
     static constexpr uint32_t kFixed =
-        kQBytes + 2 * 8192 /*P*/ + 2 * 8192 /*recv*/ + 2 * 64 * 4 + 64 * 4 + 4 * kEpiWarpBytes + 1024;
+        kQBytes + 2 * 8192 /*P*/ + 2 * 8192 /*recv*/ + 2 * 64 * 4 + 64 * 4 + 1024;
     static constexpr int kRingMax = 24;
     static constexpr int kRingFit = int((232448u - kFixed - 512u) / 8192u);
     static constexpr int kRing = kRingFit < kRingMax ? kRingFit : kRingMax;  // 8 KB units in the H ring
@@ -88,12 +87,12 @@ struct DecLayout {
     static constexpr uint32_t kRecvOff = kPOff + 2 * 8192;            // 2 x (64 x 32 fp32)
     static constexpr uint32_t kAlphaOff = kRecvOff + 2 * 8192;        // 2 x 64 fp32
     static constexpr uint32_t kLOff = kAlphaOff + 2 * 64 * 4;         // 64 fp32
-    static constexpr uint32_t kEpiOff = kLOff + 64 * 4;               // 4 x 640 B
-    static constexpr uint32_t kBarOff = kEpiOff + 4 * kEpiWarpBytes;
+    static constexpr uint32_t kBarOff = kLOff + 64 * 4;
     static constexpr int kNumBars = 2 * kRing + 24;
     static constexpr uint32_t kTotal = kBarOff + kNumBars * 8 + 16 + 1024;
     static_assert(kTotal <= 232448, "shared memory budget");
     static_assert(kQTmemUnits >= 1, "at least one q' unit in TMEM");
+    static_assert(4 * kEpiWarpBytes <= 2 * 8192, "epilogue stages alias the two P buffers");
 };
 
 __device__ __forceinline__ uint32_t softmax_bar_or(uint32_t pred) {
@@ -131,6 +130,7 @@ __device__ __forceinline__ int tiles_of(const int* npi, int b, int n_stride) {
 template <int UNITS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     el_decode_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_h,
+                        const __grid_constant__ CUtensorMap tm_c,
                         const __nv_bfloat16* __restrict__ qp_rows, const int* __restrict__ n_per_input, int B,
                         int rows, int n_stride, int d_m, float scale_log2, __nv_bfloat16* __restrict__ ctx,
                         unsigned long long* __restrict__ trace, DecodeTuning tune) {
@@ -154,7 +154,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float* recv = reinterpret_cast<float*>(smem + L::kRecvOff);
     float* s_alpha = reinterpret_cast<float*>(smem + L::kAlphaOff);
     float* s_l = reinterpret_cast<float*>(smem + L::kLOff);
-    uint8_t* epi_stage = smem + L::kEpiOff;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
     uint64_t* q_full = bars;            // q' smem half landed (per input)
     uint64_t* q_empty = bars + 1;       // both S issuers finished reading q' (per input)
@@ -182,6 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (ptx::elect_one()) {
             ptx::prefetch_tmap(&tm_q);
             ptx::prefetch_tmap(&tm_h);
+            ptx::prefetch_tmap(&tm_c);
             ptx::mbar_init(q_full, 1);
             ptx::mbar_init(q_empty, 2);
             ptx::mbar_init(q_tmem_full, 4);
@@ -241,9 +241,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, b,
                                          ptx::kEvictFirst);
                     }
+                    if (j == 0 && b + ncl < B) {
+                        // warm L2 with the NEXT input's q' (this CTA's d_m half) so the
+                        // input transition does not wait on HBM latency
+                        for (int c = 0; c < 2 * UNITS; ++c) ptx::tma_prefetch_2d(&tm_q, dm_off + 64 * c, (b + ncl) * rows);
+                    }
                     if (j == 0 && L::kQSmemUnits > 0) {
                         // this input's smem half of q', once the previous input's S no longer reads it
                         if (li > 0) ptx::mbar_wait(q_empty, (li - 1) & 1);
+                        ELA_TRACE(22, li);
                         ptx::mbar_arrive_expect_tx(q_full, L::kQBytes);
                         for (int c = 0; c < 2 * L::kQSmemUnits; ++c)
                             ptx::tma_load_2d(sq + c * 8192, &tm_q, q_full, dm_off + 128 * L::kQTmemUnits + 64 * c,
@@ -269,6 +275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (T == 0) continue;
             if (L::kQSmemUnits > 0) ptx::mbar_wait(q_full, li & 1);
             ptx::mbar_wait(q_tmem_full, li & 1);
+            if (warp == 1 && lane == 0) ELA_TRACE(16, li);
             for (int Gt = G + ((G & 1) != parity_mine ? 1 : 0); Gt < G + T; Gt += 2) {
                 const int sb = Gt & (kSBuf - 1);
                 const uint32_t d = tmem + kTmemS + sb * kNT;
@@ -331,6 +338,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // the first O of an input overwrites the accumulator: the previous
                 // input's epilogue must have read it out
                 if (j == 0 && li > 0) ptx::mbar_wait(o_free, (li - 1) & 1);
+                if (j == 0 && lane == 0) ELA_TRACE(20, li);
                 if (lane == 0) ELA_TRACE(5, Gt);
                 ptx::tc_fence_after();
                 if (lane == 0) {
@@ -363,32 +371,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t t_lane = tmem + ((qd * 32) << 16);
         const uint32_t peer_recv_full0 = ptx::mapa(ptx::smem_u32(&recv_full[0]), peer);
         const uint32_t peer_recv0 = ptx::mapa(ptx::smem_u32(recv), peer);
+        // q' units [0, kQTmemUnits) of this CTA's d_m half -> TMEM, M=64 A layout (row
+        // 16*qd + r in lane 32*qd + r, bf16 pairs packed per column), written with
+        // tcgen05.st.16x256b so all 32 lanes carry data: thread t holds rows 16qd + t/4
+        // and +8, columns 8k + 2(t%4) + {0,1}.  The NEXT input's q' is loaded into
+        // registers right after this input's fill, so at the input transition the fill is
+        // only the TMEM store.  Rows past an input's `rows` come from the next input (or
+        // zeros past the end), matching the 64-row TMA box of the smem half.
+        constexpr int kQW = 32 * L::kQTmemUnits;
+        uint32_t qv[kQW];
+        int qv_b = -1;
+        auto q_load = [&](int bb) {
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int q = int(qd) * 16 + int(lane >> 2) + 8 * half;
+                const bool ok = int64_t(bb) * rows + q < int64_t(total_rows);
+                const uint2* src =
+                    reinterpret_cast<const uint2*>(qp_rows + (int64_t(bb) * rows + q) * d_m + dm_off) + (lane & 3);
+#pragma unroll
+                for (int u = 0; u < L::kQTmemUnits; ++u)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint2 v = ok ? __ldg(src + 32 * u + 4 * k) : make_uint2(0, 0);
+                        qv[32 * u + 4 * k + 2 * half] = v.x;
+                        qv[32 * u + 4 * k + 2 * half + 1] = v.y;
+                    }
+            }
+            qv_b = bb;
+        };
         int G = 0, li = 0;
         for (int b = cl; b < B; b += ncl) {
             const int T = tiles_of(n_per_input, b, n_stride);
             if (T == 0) continue;
             {
-                // q' units [0, kQTmemUnits) of this CTA's d_m half -> TMEM, M=64 A layout:
-                // row 16*qd + t (t < 16) in lane 32*qd + t, bf16 pairs packed per column.
-                // Rows past this input's `rows` come from the next input (or zeros past
-                // the end), matching the 64-row TMA box of the smem half.
+                if (qv_b != b) q_load(b);
                 if (li > 0) ptx::mbar_wait(q_empty, (li - 1) & 1);  // previous input's S done
-                const int q = int(qd) * 16 + int(lane);
-                const bool row_ok = lane < 16 && b * rows + q < total_rows;
-                const uint4* qrow = reinterpret_cast<const uint4*>(qp_rows + (int64_t(b) * rows + q) * d_m + dm_off);
-                for (int c0 = 0; c0 < L::kQTmemUnits * 64; c0 += 16) {  // 16 columns = 32 bf16 per store
-                    uint32_t v[16];
+                if (warp == 6 && lane == 0) ELA_TRACE(17, li);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint4 x = row_ok ? __ldg(qrow + c0 / 4 + i) : make_uint4(0, 0, 0, 0);
-                        v[4 * i] = x.x, v[4 * i + 1] = x.y, v[4 * i + 2] = x.z, v[4 * i + 3] = x.w;
-                    }
-                    ptx::tmem_st16(t_lane + L::kTmemQ + c0, v);
-                }
+                for (int u = 0; u < L::kQTmemUnits; ++u)
+                    ptx::tmem_st_16x256b_x8(t_lane + L::kTmemQ + 64 * u, &qv[32 * u]);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(q_tmem_full);
+                if (warp == 6 && lane == 0) ELA_TRACE(18, li);
+                if (b + ncl < B) q_load(b + ncl);  // in flight while this input streams
             }
             for (int j = 0; j < T; ++j) {
                 const int Gt = G + j, sb = Gt & 1, sbuf = Gt & (kSBuf - 1);
@@ -431,9 +458,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // total tiles of this cluster (to stop arming recv_full past the end)
         int G_total = 0;
         for (int b = cl; b < B; b += ncl) G_total += tiles_of(n_per_input, b, n_stride);
-        uint8_t* my_stage = epi_stage + (warp - 2) * kEpiWarpBytes;
-        const uint32_t stm_addr =
-            ptx::smem_u32(my_stage) + uint32_t((lane & 7) * kEpiPitch + (lane >> 3) * 16);  // stmatrix rows
         int G = 0, li = 0;
         for (int b = cl; b < B; b += ncl) {
             const int T = tiles_of(n_per_input, b, n_stride);
@@ -582,9 +606,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // ---- epilogue: C[b*rows + q][dm_off + d] = O^T[d][q] / l_q.
             // O^T comes out of TMEM with tcgen05.ld.16x256b (thread t: lanes d = t/4,
             // t/4+8, columns q = 2(t%4)+{0,1} per 8-column group), i.e. already in the
-            // 8x8 bf16 fragment layout of stmatrix; stmatrix.trans turns each 8(q) x 32(d)
-            // slab into rows of a tiny per-warp stage, re-read as one 16-byte vector per
-            // lane and stored.  No CTA-wide barrier: the next input streams meanwhile.
+            // 8x8 bf16 fragment layout of stmatrix; stmatrix.trans turns each warp's
+            // 32(d) x 64(q) slab into a [q][32 d] SWIZZLE_64B tile (4 KB, aliasing the P
+            // buffers, which are free once O is complete), stored by one TMA store per
+            // warp and unit.  No CTA-wide barrier per unit; the next input streams meanwhile.
             if (warp == 2 && lane == 0) ELA_TRACE(14, li);
             if ((lane & 3) == 0) {
                 s_l[ra] = 1.f / l_a;
@@ -597,19 +622,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const float2 v = *reinterpret_cast<const float2*>(s_l + 8 * k + cpair);
                 inv_l[2 * k] = v.x, inv_l[2 * k + 1] = v.y;
             }
-            ptx::mbar_wait(o_full, li & 1);
+            ptx::mbar_wait(o_full, li & 1);  // all O MMAs done: P buffers are free as stages
             ptx::tc_fence_after();
+            if (warp == 2 && lane == 0) ELA_TRACE(19, li);
+            uint8_t* my_stage = sP + (warp - 2) * kEpiWarpBytes;
+            // stmatrix row address of lane l: matrix j = l/8 (d 8j..8j+7), row i = l%8 (q = 8k+i);
+            // SWIZZLE_64B: 16-byte chunk j of 64-byte row q sits at chunk j ^ ((q >> 1) & 3)
+            const uint32_t stm_i = lane & 7, stm_j = lane >> 3;
+            const uint32_t stm_base = ptx::smem_u32(my_stage) + stm_i * 64;
             for (int m = 0; m < UNITS; ++m) {
                 uint32_t lo[32], hi[32];  // lanes d 0..15 and 16..31 of this warp's quadrant
                 ptx::tmem_ld_16x256b_x8(t_lane + m * 64, lo);
                 ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16) + m * 64, hi);
                 ptx::tmem_ld_wait();
+                if (m == 0 && warp == 2 && lane == 0) ELA_TRACE(21, li);
                 if (m == UNITS - 1) {  // O read out: the next input may overwrite it
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(o_free);
                 }
-                const int d_base = dm_off + m * 128 + int(qd) * 32;
+                if (m > 0) {  // the previous unit's TMA store must have read the stage
+                    if (lane == 0) ptx::bulk_wait_group_read<0>();
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {  // query columns 8k..8k+7
                     uint32_t f[4];
@@ -622,17 +657,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             f[2 * h2 + half] = pack_bf16x2(__uint_as_float(r[0]) * inv_l[2 * k],
                                                            __uint_as_float(r[1]) * inv_l[2 * k + 1]);
                         }
-                    // matrices j = 0..3 cover d = 8j..8j+7; transposed rows are q = 8k + i
-                    ptx::stmatrix_x4_trans(stm_addr, f[0], f[1], f[2], f[3]);
-                    __syncwarp();
-                    const int qq = 8 * k + int(lane >> 2);
-                    const uint4 v = *reinterpret_cast<const uint4*>(my_stage + (lane >> 2) * kEpiPitch +
-                                                                    (lane & 3) * 16);
-                    if (qq < rows)
-                        *reinterpret_cast<uint4*>(ctx + (int64_t(b) * rows + qq) * d_m + d_base + (lane & 3) * 8) = v;
-                    __syncwarp();
+                    const uint32_t q = 8u * k + stm_i;
+                    ptx::stmatrix_x4_trans(stm_base + k * 512 + ((stm_j ^ ((q >> 1) & 3u)) << 4), f[0], f[1], f[2],
+                                           f[3]);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tm_c, my_stage, dm_off + m * 128 + int(qd) * 32, b * rows);
+                    ptx::bulk_commit_group();
                 }
             }
+            if (warp == 2 && lane == 0) ELA_TRACE(23, li);
+            // stages alias P: every warp's last store must have read its stage before
+            // any warp writes P of the next input
+            if (lane == 0) ptx::bulk_wait_group_read<0>();
+            softmax_bar_sync();
             if (warp == 2 && lane == 0) ELA_TRACE(15, li);
             G += T;
             ++li;
@@ -678,12 +718,17 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const uint64_t hstr[2] = {uint64_t(d_m) * 2, uint64_t(n_stride) * d_m * 2};
     const uint32_t hbox[3] = {64, kNT, 1};
     CUtensorMap th = make_tmap_bf16(H, 3, hdims, hstr, hbox);
+    // C viewed as [B*rows][d_m]; box = one input's rows x 32 columns (one softmax warp's
+    // d slab of a unit), SWIZZLE_64B to match the stmatrix stage layout
+    const uint64_t cdims[2] = {uint64_t(d_m), uint64_t(B) * rows};
+    const uint32_t cbox[2] = {32, uint32_t(rows)};
+    CUtensorMap tc = make_tmap_bf16(ctx, 2, cdims, qstr, cbox, 64);
     auto kern = el_decode_tc_kernel<UNITS>;
     constexpr uint32_t smem = DecLayout<UNITS>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // persistent: one cluster per pair of SMs (or per input when there are fewer)
     const int clusters = B < num_sms_decode() / 2 ? B : num_sms_decode() / 2;
-    kern<<<dim3(2 * clusters), kThreads, smem, st>>>(tq, th, static_cast<const __nv_bfloat16*>(qp), npi, B, rows,
+    kern<<<dim3(2 * clusters), kThreads, smem, st>>>(tq, th, tc, static_cast<const __nv_bfloat16*>(qp), npi, B, rows,
                                                      n_stride, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx),
                                                      g_decode_trace, g_tuning);
     ELA_CHECK_LAUNCH();

@@ -26,7 +26,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }  // namespace
 
 CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                           const uint32_t* box, bool swizzle128) {
+                           const uint32_t* box, int swizzle_bytes) {
     CUtensorMap m;
     cuuint32_t elem_strides[3] = {1, 1, 1};
     cuuint64_t gdims[3], gstrides[2];
@@ -38,7 +38,9 @@ CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims, con
     for (int i = 0; i + 1 < rank; ++i) gstrides[i] = strides_bytes[i];
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, cuuint32_t(rank), const_cast<void*>(base),
                              gdims, gstrides, boxd, elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                             swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                             : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                             : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     ELA_REQUIRE(r == CUDA_SUCCESS, ELATTN_ERR_UNSUPPORTED,
                 "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");

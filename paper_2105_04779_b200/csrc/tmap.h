@@ -10,9 +10,10 @@
 namespace elattn_gpu {
 
 // bf16 tensor map with up to 3 dims (dim 0 innermost, contiguous).
-// dims/box in elements, strides (for dims 1..rank-1) in bytes; SWIZZLE_128B,
-// out-of-bounds elements are filled with zeros.
+// dims/box in elements, strides (for dims 1..rank-1) in bytes; swizzle_bytes in
+// {0, 32, 64, 128} (default SWIZZLE_128B); out-of-bounds elements are filled with zeros
+// on loads and clipped on stores.
 CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                           const uint32_t* box, bool swizzle128 = true);
+                           const uint32_t* box, int swizzle_bytes = 128);
 
 }  // namespace elattn_gpu
