@@ -40,7 +40,10 @@
 #include "ptx_sm100.cuh"
 #include "tmap.h"
 
+#include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 
 namespace elattn_gpu {
 
@@ -55,6 +58,10 @@ constexpr int kChunkBytes = 4096;  // 32 rows x 64 d_m
 constexpr int kThreads = 384;
 constexpr int kSBuf = 4;  // S accumulators in TMEM
 constexpr int kEpiWarpBytes = 4096;  // per-warp epilogue stage (64 q x 32 d bf16), aliases P
+// partial record of a split input, per (slot, CTA rank): m[64], l[64], then per O unit the
+// 128 softmax threads' 64 fp32 fragment values (float4-interleaved by thread)
+constexpr int kPartFloatsHdr = 128;
+constexpr int kPartFloatsUnit = 128 * 64;
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max grows by > 2^8
 
 // Tuning knobs (runtime so they can be swept):
@@ -127,20 +134,76 @@ __device__ __forceinline__ int tiles_of(const int* npi, int b, int n_stride) {
     return (n_b >= 1 && n_b <= n_stride) ? (n_b + kNT - 1) / kNT : 0;
 }
 
+// Work schedule of one cluster.  STREAM-K (uniform context length, T tiles per input) —
+// the B*T tiles are cut into contiguous chunks of W tiles, one per cluster, so every
+// cluster streams the same amount of H whatever B is (no wave tail, and small batches
+// still use every SM).  An input cut by a chunk boundary is processed as SEGMENTS by
+// consecutive clusters; each writes a partial record (unnormalised O, running max m, sum
+// l) and el_decode_merge_kernel combines them in cluster order (deterministic).
+// Otherwise (full last round, or ragged n_per_input): whole inputs, cluster c takes c,
+// c+ncl, ...
+struct SplitArgs {
+    int T;           // tiles per input (uniform mode), 0 = ragged / strided whole inputs
+    int W;           // tiles per cluster chunk (uniform mode)
+    float* part;     // partial records [2 * ncl slots][2 ranks][kPartFloats]
+};
+struct Sched {
+    int T, W, B, ncl, n_stride;
+    const int* npi;
+    int g, g_end, b;
+    bool first;
+    __device__ Sched(const SplitArgs& sa, int cl, int ncl_, int B_, int n_stride_, const int* npi_)
+        : T(sa.T), W(sa.W), B(B_), ncl(ncl_), n_stride(n_stride_), npi(npi_), first(true) {
+        if (T > 0) {
+            g = cl * W;
+            g_end = min(B * T, g + W);
+        } else {
+            g = g_end = 0;
+        }
+        b = cl;
+    }
+    // next segment: input bb, tiles [j0, j1) of its Tb; kind -1 = whole input, 0 = first
+    // segment of this cluster's chunk, 1 = last segment (partial-record slot 2*cl + kind)
+    __device__ bool next(int& bb, int& j0, int& j1, int& Tb, int& kind) {
+        if (T > 0) {
+            if (g >= g_end) return false;
+            bb = g / T;
+            j0 = g - bb * T;
+            j1 = min(T, j0 + (g_end - g));
+            Tb = T;
+            g += j1 - j0;
+            kind = (j0 == 0 && j1 == T) ? -1 : (first ? 0 : 1);
+            first = false;
+            return true;
+        }
+        for (; b < B; b += ncl) {
+            Tb = tiles_of(npi, b, n_stride);
+            if (Tb == 0) continue;
+            bb = b;
+            j0 = 0;
+            j1 = Tb;
+            kind = -1;
+            b += ncl;
+            return true;
+        }
+        return false;
+    }
+};
+
 template <int UNITS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     el_decode_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_h,
                         const __grid_constant__ CUtensorMap tm_c,
                         const __nv_bfloat16* __restrict__ qp_rows, const int* __restrict__ n_per_input, int B,
                         int rows, int n_stride, int d_m, float scale_log2, __nv_bfloat16* __restrict__ ctx,
-                        unsigned long long* __restrict__ trace, DecodeTuning tune) {
+                        unsigned long long* __restrict__ trace, DecodeTuning tune, SplitArgs sa) {
     using L = DecLayout<UNITS>;
     constexpr int kRing = L::kRing;
     // optional per-tile clock64 trace of the first cluster (testing hook); G = cluster tile index
 #define ELA_TRACE(ev, G)                                                                          \
     do {                                                                                          \
         if (trace != nullptr && blockIdx.x < 2 && (G) < 64)                                       \
-            trace[(blockIdx.x * 24 + (ev)) * 64 + (G)] = clock64();                               \
+            trace[(blockIdx.x * 32 + (ev)) * 64 + (G)] = clock64();                               \
     } while (0)
     constexpr int kTmemCols = 512;
     constexpr uint32_t kTmemS = L::kTmemS;
@@ -221,12 +284,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // ================= TMA producer =================
         if (ptx::elect_one()) {
             int G = 0, li = 0;
-            for (int b = cl; b < B; b += ncl) {
-                const int T = tiles_of(n_per_input, b, n_stride);
-                if (T == 0) continue;
-                for (int j = 0; j < T; ++j) {
-                    const int Gt = G + j;
-                    if (tune.l2_ahead > 0 && j + tune.l2_ahead < T)
+            Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+            int b, j0, j1, Tb, kind;
+            while (sc.next(b, j0, j1, Tb, kind)) {
+                const int T = j1 - j0;
+                int nb = -1;  // input of the next segment (its q' is prefetched into L2)
+                {
+                    Sched pk = sc;
+                    int a0, a1, a2, a3;
+                    if (!pk.next(nb, a0, a1, a2, a3)) nb = -1;
+                }
+                for (int jj = 0; jj < T; ++jj) {
+                    const int j = j0 + jj, Gt = G + jj;
+                    if (tune.l2_ahead > 0 && j + tune.l2_ahead < Tb)
                         for (int c = 0; c < 2 * UNITS; ++c)
                             ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, b);
                     for (int u = 0; u < UNITS; ++u) {
@@ -241,12 +311,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, b,
                                          ptx::kEvictFirst);
                     }
-                    if (j == 0 && b + ncl < B) {
-                        // warm L2 with the NEXT input's q' (this CTA's d_m half) so the
-                        // input transition does not wait on HBM latency
-                        for (int c = 0; c < 2 * UNITS; ++c) ptx::tma_prefetch_2d(&tm_q, dm_off + 64 * c, (b + ncl) * rows);
+                    if (jj == 0 && nb >= 0 && nb != b) {
+                        // warm L2 with the NEXT segment's q' (this CTA's d_m half) so the
+                        // transition does not wait on HBM latency
+                        for (int c = 0; c < 2 * UNITS; ++c) ptx::tma_prefetch_2d(&tm_q, dm_off + 64 * c, nb * rows);
                     }
-                    if (j == 0 && L::kQSmemUnits > 0) {
+                    if (jj == 0 && L::kQSmemUnits > 0) {
                         // this input's smem half of q', once the previous input's S no longer reads it
                         if (li > 0) ptx::mbar_wait(q_empty, (li - 1) & 1);
                         ELA_TRACE(22, li);
@@ -270,9 +340,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint64_t dQ = ptx::sdesc_sw128(ptx::smem_u32(sq), 0, 1024);
         const int parity_mine = warp == 1 ? 0 : 1;
         int G = 0, li = 0;
-        for (int b = cl; b < B; b += ncl) {
-            const int T = tiles_of(n_per_input, b, n_stride);
-            if (T == 0) continue;
+        Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+        int b, j0, j1, Tb, kind;
+        while (sc.next(b, j0, j1, Tb, kind)) {
+            const int T = j1 - j0;
             if (L::kQSmemUnits > 0) ptx::mbar_wait(q_full, li & 1);
             ptx::mbar_wait(q_tmem_full, li & 1);
             if (warp == 1 && lane == 0) ELA_TRACE(16, li);
@@ -328,10 +399,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint64_t dRingMN = ptx::sdesc_sw128(ptx::smem_u32(ring), kChunkBytes, 1024);
         const uint64_t dP = ptx::sdesc_sw128(ptx::smem_u32(sP), 0, 1024);
         int G = 0, li = 0;
-        for (int b = cl; b < B; b += ncl) {
-            const int T = tiles_of(n_per_input, b, n_stride);
-            if (T == 0) continue;
-            for (int j = 0; j < T; ++j) {
+        Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+        int b, j0, j1, Tb, kind;
+        while (sc.next(b, j0, j1, Tb, kind)) {
+            const int T = j1 - j0;
+            for (int j = 0; j < T; ++j) {  // j: tile index within the segment
                 const int Gt = G + j, pb = Gt & 1;
                 if (lane == 0) ELA_TRACE(4, Gt);
                 ptx::mbar_wait(&p_full[pb], (Gt >> 1) & 1);
@@ -400,9 +472,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             qv_b = bb;
         };
         int G = 0, li = 0;
-        for (int b = cl; b < B; b += ncl) {
-            const int T = tiles_of(n_per_input, b, n_stride);
-            if (T == 0) continue;
+        Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+        int b, j0, j1, Tb, kind;
+        while (sc.next(b, j0, j1, Tb, kind)) {
+            const int T = j1 - j0;
             {
                 if (qv_b != b) q_load(b);
                 if (li > 0) ptx::mbar_wait(q_empty, (li - 1) & 1);  // previous input's S done
@@ -415,7 +488,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(q_tmem_full);
                 if (warp == 6 && lane == 0) ELA_TRACE(18, li);
-                if (b + ncl < B) q_load(b + ncl);  // in flight while this input streams
+                {
+                    Sched pk = sc;  // the next segment's q' is in flight while this one streams
+                    int nb, a0, a1, a2, a3;
+                    if (pk.next(nb, a0, a1, a2, a3) && nb != b) q_load(nb);
+                }
             }
             for (int j = 0; j < T; ++j) {
                 const int Gt = G + j, sb = Gt & 1, sbuf = Gt & (kSBuf - 1);
@@ -457,16 +534,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float neg_inf = -INFINITY;
         // total tiles of this cluster (to stop arming recv_full past the end)
         int G_total = 0;
-        for (int b = cl; b < B; b += ncl) G_total += tiles_of(n_per_input, b, n_stride);
+        int b, j0, j1, Tb, kind;
+        {
+            Sched pk(sa, cl, ncl, B, n_stride, n_per_input);
+            while (pk.next(b, j0, j1, Tb, kind)) G_total += j1 - j0;
+        }
         int G = 0, li = 0;
-        for (int b = cl; b < B; b += ncl) {
-            const int T = tiles_of(n_per_input, b, n_stride);
-            if (T == 0) continue;
+        Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+        while (sc.next(b, j0, j1, Tb, kind)) {
+            const int T = j1 - j0;
             const int n_b = n_per_input ? n_per_input[b] : n_stride;
-            const bool zero_tail = (n_per_input != nullptr) && (T * kNT > n_b);
+            const bool zero_tail = (n_per_input != nullptr) && (Tb * kNT > n_b);
             float m_a = neg_inf, m_b = neg_inf, l_a = 0.f, l_b = 0.f;  // running max (raw units), sums
-            for (int j = 0; j < T; ++j) {
-                const int Gt = G + j, sb = Gt & 1, sbuf = Gt & (kSBuf - 1);
+            for (int jj = 0; jj < T; ++jj) {
+                const int j = j0 + jj;  // tile index within the input
+                const int Gt = G + jj, sb = Gt & 1, sbuf = Gt & (kSBuf - 1);
                 const uint32_t par = (Gt >> 1) & 1;
                 if (warp == 2 && lane == 0) ELA_TRACE(10, Gt);
                 ptx::mbar_wait(&s_full[sbuf], (Gt / kSBuf) & 1);
@@ -560,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         *reinterpret_cast<uint32_t*>(P + rb * 128 + ((k ^ (rb & 7)) << 4) + 2 * cpair) = pb[k];
                     }
                 }
-                if (zero_tail && j == T - 1) {
+                if (zero_tail && j == Tb - 1) {
                     // rows n_b.. of the last tile are in-bounds padding of H_b: zero them
                     // before they meet P = 0 in the MMA (0 * NaN would poison O).
                     const int r0 = n_b - j * kNT;
@@ -578,7 +660,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // consume o_done phases in order (one per tile) so the parity wait is exact;
                 // O(Gt-1) was issued a full stage ago, so this rarely blocks
                 if (Gt > 0) ptx::mbar_wait(o_done, (Gt - 1) & 1);
-                if (any && j > 0) {
+                if (any && jj > 0) {
                     // lazy rescale of the running O^T columns (O(Gt-1) complete): O *= alpha
                     ptx::tc_fence_after();
 #pragma unroll 1
@@ -611,40 +693,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // buffers, which are free once O is complete), stored by one TMA store per
             // warp and unit.  No CTA-wide barrier per unit; the next input streams meanwhile.
             if (warp == 2 && lane == 0) ELA_TRACE(14, li);
-            if ((lane & 3) == 0) {
-                s_l[ra] = 1.f / l_a;
-                s_l[rb] = 1.f / l_b;
-            }
-            softmax_bar_sync();
-            float inv_l[16];  // 1/l for this thread's columns q = 8k + 2(t%4) + {0,1}
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const float2 v = *reinterpret_cast<const float2*>(s_l + 8 * k + cpair);
-                inv_l[2 * k] = v.x, inv_l[2 * k + 1] = v.y;
-            }
-            ptx::mbar_wait(o_full, li & 1);  // all O MMAs done: P buffers are free as stages
-            ptx::tc_fence_after();
-            if (warp == 2 && lane == 0) ELA_TRACE(19, li);
             uint8_t* my_stage = sP + (warp - 2) * kEpiWarpBytes;
             // stmatrix row address of lane l: matrix j = l/8 (d 8j..8j+7), row i = l%8 (q = 8k+i);
             // SWIZZLE_64B: 16-byte chunk j of 64-byte row q sits at chunk j ^ ((q >> 1) & 3)
             const uint32_t stm_i = lane & 7, stm_j = lane >> 3;
             const uint32_t stm_base = ptx::smem_u32(my_stage) + stm_i * 64;
-            for (int m = 0; m < UNITS; ++m) {
-                uint32_t lo[32], hi[32];  // lanes d 0..15 and 16..31 of this warp's quadrant
-                ptx::tmem_ld_16x256b_x8(t_lane + m * 64, lo);
-                ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16) + m * 64, hi);
-                ptx::tmem_ld_wait();
-                if (m == 0 && warp == 2 && lane == 0) ELA_TRACE(21, li);
-                if (m == UNITS - 1) {  // O read out: the next input may overwrite it
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(o_free);
-                }
+            const int tid = int(threadIdx.x) - 64;  // 0..127 over the softmax warps
+            // unit m of the output: fp32 fragments lo/hi (lanes d 0..15 / 16..31 of the quadrant)
+            // scaled by sc[] (per query column of this thread) -> bf16 -> stage -> TMA store
+            auto emit_unit = [&](int m, const uint32_t(&lo)[32], const uint32_t(&hi)[32], const float(&sc)[16]) {
+                if (warp == 2 && lane == 0) ELA_TRACE(24, li * 4 + m);
                 if (m > 0) {  // the previous unit's TMA store must have read the stage
                     if (lane == 0) ptx::bulk_wait_group_read<0>();
                     __syncwarp();
                 }
+                if (warp == 2 && lane == 0) ELA_TRACE(25, li * 4 + m);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {  // query columns 8k..8k+7
                     uint32_t f[4];
@@ -654,8 +717,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int half = 0; half < 2; ++half) {
                             const uint32_t* r = src[h2] + 4 * k + 2 * half;
-                            f[2 * h2 + half] = pack_bf16x2(__uint_as_float(r[0]) * inv_l[2 * k],
-                                                           __uint_as_float(r[1]) * inv_l[2 * k + 1]);
+                            f[2 * h2 + half] = pack_bf16x2(__uint_as_float(r[0]) * sc[2 * k],
+                                                           __uint_as_float(r[1]) * sc[2 * k + 1]);
                         }
                     const uint32_t q = 8u * k + stm_i;
                     ptx::stmatrix_x4_trans(stm_base + k * 512 + ((stm_j ^ ((q >> 1) & 3u)) << 4), f[0], f[1], f[2],
@@ -663,9 +726,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
+                if (warp == 2 && lane == 0) ELA_TRACE(26, li * 4 + m);
                 if (lane == 0) {
                     ptx::tma_store_2d(&tm_c, my_stage, dm_off + m * 128 + int(qd) * 32, b * rows);
                     ptx::bulk_commit_group();
+                }
+            };
+            if (kind < 0) {
+                // whole input: normalise by 1/l and write
+                if ((lane & 3) == 0) {
+                    s_l[ra] = 1.f / l_a;
+                    s_l[rb] = 1.f / l_b;
+                }
+                softmax_bar_sync();
+                float inv_l[16];  // 1/l for this thread's columns q = 8k + 2(t%4) + {0,1}
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float2 v = *reinterpret_cast<const float2*>(s_l + 8 * k + cpair);
+                    inv_l[2 * k] = v.x, inv_l[2 * k + 1] = v.y;
+                }
+                ptx::mbar_wait(o_full, li & 1);  // all O MMAs done: P buffers are free as stages
+                ptx::tc_fence_after();
+                if (warp == 2 && lane == 0) ELA_TRACE(19, li);
+                // software-pipelined: unit m+1 streams out of TMEM while unit m is
+                // converted, staged and stored (two register sets, fully unrolled)
+                uint32_t fr[2][2][32];  // [set][lo/hi][32]
+                ptx::tmem_ld_16x256b_x8(t_lane, fr[0][0]);
+                ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16), fr[0][1]);
+                ptx::tmem_ld_wait();
+                if (warp == 2 && lane == 0) ELA_TRACE(21, li);
+#pragma unroll
+                for (int m = 0; m < UNITS; ++m) {
+                    if (m + 1 < UNITS) {
+                        ptx::tmem_ld_16x256b_x8(t_lane + (m + 1) * 64, fr[(m + 1) & 1][0]);
+                        ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16) + (m + 1) * 64, fr[(m + 1) & 1][1]);
+                    }
+                    if (m == UNITS - 1) {  // O read out: the next segment may overwrite it
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(o_free);
+                    }
+                    if (warp == 2 && lane == 0) ELA_TRACE(27, li * 4 + m);
+                    emit_unit(m, fr[m & 1][0], fr[m & 1][1], inv_l);
+                    if (m + 1 < UNITS) ptx::tmem_ld_wait();
+                }
+            } else {
+                // segment of a split input: write its partial record (running max m and
+                // sum l per query row, unnormalised O^T in this thread's fragment order);
+                // el_decode_merge_kernel combines the records after this kernel
+                constexpr int kPF = kPartFloatsHdr + UNITS * kPartFloatsUnit;
+                float* rec = sa.part + (int64_t(2 * cl + kind) * 2 + rank) * kPF;
+                if ((lane & 3) == 0) {
+                    rec[ra] = m_a;
+                    rec[rb] = m_b;
+                    rec[64 + ra] = l_a;
+                    rec[64 + rb] = l_b;
+                }
+                ptx::mbar_wait(o_full, li & 1);
+                ptx::tc_fence_after();
+#pragma unroll 1
+                for (int m = 0; m < UNITS; ++m) {
+                    uint32_t lo[32], hi[32];
+                    ptx::tmem_ld_16x256b_x8(t_lane + m * 64, lo);
+                    ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16) + m * 64, hi);
+                    ptx::tmem_ld_wait();
+                    if (m == UNITS - 1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(o_free);
+                    }
+                    float4* body = reinterpret_cast<float4*>(rec + kPartFloatsHdr + m * kPartFloatsUnit);
+#pragma unroll
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        body[(0 * 8 + i4) * 128 + tid] =
+                            make_float4(__uint_as_float(lo[4 * i4]), __uint_as_float(lo[4 * i4 + 1]),
+                                        __uint_as_float(lo[4 * i4 + 2]), __uint_as_float(lo[4 * i4 + 3]));
+                        body[(1 * 8 + i4) * 128 + tid] =
+                            make_float4(__uint_as_float(hi[4 * i4]), __uint_as_float(hi[4 * i4 + 1]),
+                                        __uint_as_float(hi[4 * i4 + 2]), __uint_as_float(hi[4 * i4 + 3]));
+                    }
                 }
             }
             if (warp == 2 && lane == 0) ELA_TRACE(23, li);
@@ -705,6 +844,118 @@ int num_sms_decode() {
     return n;
 }
 
+// Per-stream scratch for split-input partial records, grown on demand.
+struct DecodeScratch {
+    float* part = nullptr;
+    size_t part_bytes = 0;
+};
+std::mutex g_scratch_mu;
+std::unordered_map<cudaStream_t, DecodeScratch> g_scratch;
+
+float* split_scratch(cudaStream_t st, size_t part_bytes) {
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    DecodeScratch& s = g_scratch[st];
+    if (s.part_bytes < part_bytes) {
+        ELA_CHECK_CUDA(cudaStreamSynchronize(st));  // previous launches may still use the old buffer
+        if (s.part) cudaFree(s.part);
+        s.part = nullptr;
+        s.part_bytes = 0;
+        ELA_CHECK_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.part), part_bytes));
+        s.part_bytes = part_bytes;
+    }
+    return s.part;
+}
+
+// Combines the partial records of every split input (stream-K) into C rows.
+// CTA (chunk boundary k, rank r, unit m), 256 threads; only the CTA of the first boundary
+// inside an input works.  Phase 1 (one thread per query row q): M = max_s m_s, per-segment
+// weights w_s = 2^{(m_s - M) c} and 1/L, L = sum_s l_s w_s, into smem.  Phase 2: the unit's
+// 2048 float4 fragments (written by the decode kernel's softmax thread t as lanes d rows
+// 32 qd + t/4 + {0,8,16,24}, query columns 8k + 2(t%4) + {0,1}, qd = (t/32 + 2) & 3) are
+// loaded for all segments at once, O = sum_s w_s O_s, scaled by 1/L, staged as a
+// [64 q][128 d] bf16 tile and written with 16-byte stores.  Segment order is fixed
+// (cluster order), so the result does not depend on timing.
+constexpr int kMaxSegs = 8;
+template <int UNITS>
+__global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __restrict__ part, int T, int W, int ncl,
+                                                              int rows, int d_m, float scale_log2,
+                                                              __nv_bfloat16* __restrict__ ctx) {
+    constexpr int kPF = kPartFloatsHdr + UNITS * kPartFloatsUnit;
+    const int k = int(blockIdx.x) + 1, rank = int(blockIdx.y), m = int(blockIdx.z);
+    const int64_t gk = int64_t(k) * W;
+    const int b = int(gk / T);
+    if (gk % T == 0 || int64_t(k - 1) * W > int64_t(b) * T) return;  // not a split, or not b's first boundary
+    const int c_first = int((int64_t(b) * T) / W);
+    const int nseg = min(kMaxSegs, int((int64_t(b) * T + T - 1) / W) - c_first + 1);
+    __shared__ const float* s_rec[kMaxSegs];
+    __shared__ float s_w[kMaxSegs][64];
+    __shared__ float s_inv[64];
+    __shared__ __align__(16) __nv_bfloat16 tile[64][128 + 8];
+    const int tid = int(threadIdx.x);
+    if (tid < nseg) {
+        const int c2 = c_first + tid;
+        const int kd = (int64_t(c2) * W >= int64_t(b) * T) ? 0 : 1;  // b's segment is c2's first?
+        s_rec[tid] = part + (int64_t(2 * c2 + kd) * 2 + rank) * kPF;
+    }
+    __syncthreads();
+    if (tid < 64) {
+        float ms[kMaxSegs], ls[kMaxSegs], M = -INFINITY, L = 0.f;
+#pragma unroll
+        for (int s = 0; s < kMaxSegs; ++s)
+            if (s < nseg) {
+                ms[s] = __ldcg(s_rec[s] + tid);
+                ls[s] = __ldcg(s_rec[s] + 64 + tid);
+                M = fmaxf(M, ms[s]);
+            }
+#pragma unroll
+        for (int s = 0; s < kMaxSegs; ++s)
+            if (s < nseg) {
+                const float w = ptx::ex2((ms[s] - M) * scale_log2);
+                s_w[s][tid] = w;
+                L += ls[s] * w;
+            }
+        s_inv[tid] = 1.f / L;
+    }
+    __syncthreads();
+    // fragment float4 e = (h * 8 + i4) * 128 + t of the unit; this thread takes e = tid + 256 j
+    constexpr int kPer = 2 * 8 * 128 / 256;
+    float4 acc[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < nseg; ++s) {
+        const float4* body = reinterpret_cast<const float4*>(s_rec[s] + kPartFloatsHdr + m * kPartFloatsUnit);
+        float4 v[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) v[j] = __ldcg(body + tid + 256 * j);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const int e = tid + 256 * j, t = e & 127, i4 = (e >> 7) & 7;
+            const int q0 = 8 * i4 + 2 * (t & 3);
+            const float w0 = s_w[s][q0], w1 = s_w[s][q0 + 1];
+            acc[j].x += v[j].x * w0, acc[j].y += v[j].y * w1, acc[j].z += v[j].z * w0, acc[j].w += v[j].w * w1;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int e = tid + 256 * j, t = e & 127, i4 = (e >> 7) & 7, h = e >> 10;
+        const int qd = ((t >> 5) + 2) & 3, q0 = 8 * i4 + 2 * (t & 3);
+        const int d0 = 32 * qd + 16 * h + ((t & 31) >> 2);  // regs x,y: d0; z,w: d0 + 8
+        tile[q0][d0] = __float2bfloat16_rn(acc[j].x * s_inv[q0]);
+        tile[q0 + 1][d0] = __float2bfloat16_rn(acc[j].y * s_inv[q0 + 1]);
+        tile[q0][d0 + 8] = __float2bfloat16_rn(acc[j].z * s_inv[q0]);
+        tile[q0 + 1][d0 + 8] = __float2bfloat16_rn(acc[j].w * s_inv[q0 + 1]);
+    }
+    __syncthreads();
+    const int dm_off = rank * (d_m / 2) + m * 128;
+    for (int e = tid; e < rows * 16; e += 256) {
+        const int q = e >> 4, v = e & 15;
+        *reinterpret_cast<uint4*>(ctx + (int64_t(b) * rows + q) * d_m + dm_off + 8 * v) =
+            *reinterpret_cast<const uint4*>(&tile[q][8 * v]);
+    }
+}
+
+constexpr int kMinChunkTiles = 8;  // bounds the segments per input (merge cost) at small B
+
 template <int UNITS>
 void launch_units(const void* qp, const void* H, const int* npi, int B, int rows, int n_stride, int d_m,
                   float scale_log2, void* ctx, cudaStream_t st) {
@@ -726,12 +977,44 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     auto kern = el_decode_tc_kernel<UNITS>;
     constexpr uint32_t smem = DecLayout<UNITS>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    // persistent: one cluster per pair of SMs (or per input when there are fewer)
-    const int clusters = B < num_sms_decode() / 2 ? B : num_sms_decode() / 2;
+    // persistent: one cluster per pair of SMs
+    const int max_cl = num_sms_decode() / 2;
+    int clusters;
+    SplitArgs sa{};
+    // Whole inputs strided over the clusters unless the last round would leave more than
+    // half of the clusters idle: then stream-K (every input-segment transition costs a
+    // pipeline drain, so splitting only pays when the tail is short; measured on B200).
+    const int last_round = B % max_cl;
+    const bool stream_k = npi == nullptr && last_round != 0 && 2 * last_round < max_cl;
+    if (stream_k) {
+        // stream-K over B*T tiles: chunks of W tiles (>= kMinChunkTiles), one per cluster
+        const int T = (n_stride + kNT - 1) / kNT;
+        const int64_t TT = int64_t(B) * T;
+        int64_t ncl = std::min<int64_t>(max_cl, std::max<int64_t>(1, TT / kMinChunkTiles));
+        // chunks of >= T/(kMaxSegs-1) tiles keep every input within kMaxSegs segments
+        const int64_t W = std::max<int64_t>((TT + ncl - 1) / ncl, (T + kMaxSegs - 2) / (kMaxSegs - 1));
+        ncl = (TT + W - 1) / W;
+        ELA_REQUIRE(TT < (int64_t(1) << 30), ELATTN_ERR_UNSUPPORTED, "tcgen05 decode: too many tiles");
+        if (W % T != 0) {  // some inputs are split across clusters: partial records
+            constexpr size_t kPF = kPartFloatsHdr + size_t(UNITS) * kPartFloatsUnit;
+            sa.part = split_scratch(st, size_t(2 * ncl) * 2 * kPF * sizeof(float));
+        }
+        sa.T = T;
+        sa.W = int(W);
+        clusters = int(ncl);
+    } else {
+        sa.T = 0;  // whole inputs, strided over the clusters
+        clusters = B < max_cl ? B : max_cl;
+    }
     kern<<<dim3(2 * clusters), kThreads, smem, st>>>(tq, th, tc, static_cast<const __nv_bfloat16*>(qp), npi, B, rows,
                                                      n_stride, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx),
-                                                     g_decode_trace, g_tuning);
+                                                     g_decode_trace, g_tuning, sa);
     ELA_CHECK_LAUNCH();
+    if (sa.part != nullptr && clusters > 1) {
+        el_decode_merge_kernel<UNITS><<<dim3(clusters - 1, 2, UNITS), 256, 0, st>>>(
+            sa.part, sa.T, sa.W, clusters, rows, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx));
+        ELA_CHECK_LAUNCH();
+    }
 }
 
 }  // namespace

@@ -152,3 +152,37 @@ def test_decode_ragged_garbage_padding(kernel):
     assert torch.isfinite(ctx.float()).all()
     err = (ctx.float() - want).abs().max().item() / want.abs().max().item()
     assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("B,rows,n,d_m", [
+    (1, 64, 1024, 1024),    # one input split over several clusters (stream-K, 4 segments)
+    (20, 64, 1024, 1024),   # short last round -> stream-K chunks cut inputs
+    (75, 64, 1024, 1024),   # 74 clusters + 1: stream-K
+    (3, 64, 2000, 1024),    # long context: many segments per input (kMaxSegs guard)
+    (2, 16, 130, 512),      # rows < 64 and a masked last tile in a split input
+])
+def test_decode_stream_k_schedules(B, rows, n, d_m):
+    """The stream-K schedule (inputs split across clusters, partial records merged by
+    el_decode_merge_kernel) against torch fp32, against the whole-input schedule (the same
+    inputs passed with n_per_input), and run-to-run determinism."""
+    import torch
+
+    L, capi = _testing_lib()
+    g = torch.Generator(device="cuda").manual_seed(B * 7 + n)
+    qp = (torch.randn(B * rows, d_m, generator=g, device="cuda") * 0.3).to(torch.bfloat16)
+    H = (torch.rand(B, n, d_m, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for npi in (None, None, torch.full((B,), n, dtype=torch.int32, device="cuda")):
+        ctx = torch.full((B * rows, d_m), float("nan"), device="cuda", dtype=torch.bfloat16)
+        capi.check(L.elattn_gpu_testing_decode_bf16(qp.data_ptr(), H.data_ptr(),
+                                                    npi.data_ptr() if npi is not None else None, B, rows, n, d_m,
+                                                    0.125, ctx.data_ptr(), 1, st))
+        torch.cuda.synchronize()
+        outs.append(ctx.float())
+    want = decode_ref(qp, H, rows, 0.125)
+    for o in outs:
+        assert torch.isfinite(o).all()
+        assert (o - want).abs().max().item() / want.abs().max().item() < 2e-2
+    assert torch.equal(outs[0], outs[1])  # deterministic merge order
+    assert (outs[0] - outs[2]).abs().max().item() / want.abs().max().item() < 1e-2

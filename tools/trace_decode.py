@@ -24,7 +24,7 @@ B, rows, n, d_m = a.B, 64, a.n, 1024
 qp = (torch.randn(B * rows, d_m, device="cuda") * 0.3).to(torch.bfloat16)
 H = (torch.rand(B, n, d_m, device="cuda") * 2 - 1).to(torch.bfloat16)
 ctx = torch.empty_like(qp)
-tr = torch.zeros(2 * 24 * 64, dtype=torch.int64, device="cuda")
+tr = torch.zeros(2 * 32 * 64, dtype=torch.int64, device="cuda")
 st = torch.cuda.current_stream().cuda_stream
 for i in range(3):
     L.elattn_gpu_testing_set_decode_trace(tr.data_ptr() if i == 2 else None)
@@ -32,7 +32,7 @@ for i in range(3):
                                                 ctx.data_ptr(), 1, st))
 L.elattn_gpu_testing_set_decode_trace(None)
 torch.cuda.synchronize()
-t = tr.view(2, 24, 64).cpu().numpy()
+t = tr.view(2, 32, 64).cpu().numpy()
 t0 = t[0][t[0] > 0].min()
 for cta in range(1):
     print("cta", cta)

@@ -26,7 +26,7 @@ a = ap.parse_args()
 L = capi.lib()
 L.elattn_gpu_testing_set_decode_trace.argtypes = [ctypes.c_void_p]
 L.elattn_gpu_testing_decode_bf16.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4 + [ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
-NEV, NT = 24, 64
+NEV, NT = 32, 64
 SPANS = [  # (name, end event, start event)
     ("cadence: P(G) posted - P(G-1) posted", 13, -13),
     ("producer: wait for ring slot", 1, 0),
@@ -83,3 +83,9 @@ for B in a.B:
         r = lambda e, i: int(t[0, e, i] - base) if t[0, e, i] else None  # noqa: E731
         print(f"   li={li}: 0 | {r(3, li * T - 1)} {r(17, li)} {r(18, li)} {r(22, li)} {r(16, li)} "
               f"{r(13, li * T)} {r(19, li - 1)} {r(21, li - 1)} {r(23, li - 1)} {r(15, li - 1)} {r(20, li)}")
+    # epilogue units of input li=1 (full inputs only): tmem-ld done / stage free / staged / (next)
+    print("  epilogue units li=1 (rel. to o_full): m: ld_done wait_start stage_free staged")
+    base = t[0, 19, 1]
+    for m in range(4):
+        i = 4 + m
+        print(f"   m={m}: {int(t[0, 27, i] - base)} {int(t[0, 24, i] - base)} {int(t[0, 25, i] - base)} {int(t[0, 26, i] - base)}")
