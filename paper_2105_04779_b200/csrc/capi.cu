@@ -10,6 +10,8 @@
 #include <memory>
 #include <vector>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,6 +27,8 @@ struct elattn_gpu_params_s {
     float* bk = nullptr;  // [h*d_k]
     float* bv = nullptr;  // [h*d_k] (zero when include_value_bias == 0)
     float* bo = nullptr;  // [d_m]
+    void* bq16 = nullptr;  // bf16 copies of bq / bo for the cuBLASLt bias epilogue (bf16 path only)
+    void* bo16 = nullptr;
 };
 
 namespace elattn_gpu {
@@ -90,7 +94,7 @@ float* upload_f32(const std::vector<double>& v) {
 void free_params(elattn_gpu_params_s* p) {
     if (!p) return;
     for (void* ptr : {p->WqT, p->Wk, p->WvT, p->WoT, (void*)p->bq, (void*)p->bk, (void*)p->bv,
-                      (void*)p->bo})
+                      (void*)p->bo, p->bq16, p->bo16})
         if (ptr) cudaFree(ptr);
     delete p;
 }
@@ -134,8 +138,20 @@ size_t step_workspace(const elattn_gpu_params_s* p, int64_t R) {
     return align256(R * hk * e) * 2 + align256(R * hm * e) * 2;
 }
 
+// Dense projections (Z == 1) go to cuBLASLt; the head-batched EL GEMMs to our tcgen05
+// kernel.  ELATTN_DENSE_GEMM=tc forces the tcgen05 kernel for the dense ones too.
+bool dense_via_lt() {
+    static const bool v = [] {
+        const char* e = getenv("ELATTN_DENSE_GEMM");
+        return !(e && std::string(e) == "tc");
+    }();
+    return v;
+}
+
 void gemm(const elattn_gpu_params_s* p, const GemmArgs& g, cudaStream_t st) {
-    if (p->dtype == ELATTN_DTYPE_BF16 && tc_gemm_supported(g))
+    if (p->dtype == ELATTN_DTYPE_BF16 && g.Z == 1 && dense_via_lt() && lt_gemm_supported(g))
+        launch_lt_gemm(g, st);
+    else if (p->dtype == ELATTN_DTYPE_BF16 && tc_gemm_supported(g))
         launch_tc_gemm(g, st);
     else
         launch_simt_gemm(p->dtype, g, st);
@@ -146,7 +162,7 @@ void query_expansion(const elattn_gpu_params_s* p, const void* Y, int64_t R, voi
                      cudaStream_t st) {
     const int h = p->h, d_m = p->d_m, d_k = p->d_k, hk = h * d_k;
     GemmArgs a{};
-    a.A = Y, a.lda = d_m, a.B = p->WqT, a.ldb = d_m, a.C = Q, a.ldc = hk, a.bias = p->bq;
+    a.A = Y, a.lda = d_m, a.B = p->WqT, a.ldb = d_m, a.C = Q, a.ldc = hk, a.bias = p->bq, a.bias16 = p->bq16;
     a.M = int(R), a.N = hk, a.K = d_m, a.Z = 1, a.alpha = 1.f;
     gemm(p, a, st);
     const size_t e = dtype_bytes(p->dtype);
@@ -171,7 +187,7 @@ void output_projection(const elattn_gpu_params_s* p, const void* C, int64_t R, v
     a.M = int(R), a.N = d_k, a.K = d_m, a.Z = h, a.alpha = 1.f;
     gemm(p, a, st);
     GemmArgs b{};
-    b.A = V, b.lda = hk, b.B = p->WoT, b.ldb = hk, b.C = out, b.ldc = d_m, b.bias = p->bo;
+    b.A = V, b.lda = hk, b.B = p->WoT, b.ldb = hk, b.C = out, b.ldc = d_m, b.bias = p->bo, b.bias16 = p->bo16;
     b.M = int(R), b.N = d_m, b.K = hk, b.Z = 1, b.alpha = 1.f;
     gemm(p, b, st);
 }
@@ -254,6 +270,10 @@ int elattn_gpu_params_create(int h, int d_m, int d_k, int dtype, int include_key
         p->bk = upload_f32(vbk);
         p->bv = upload_f32(vbv);
         p->bo = upload_f32(vbo);
+        if (dtype == ELATTN_DTYPE_BF16) {
+            p->bq16 = upload(vbq, ELATTN_DTYPE_BF16);
+            p->bo16 = upload(vbo, ELATTN_DTYPE_BF16);
+        }
         *out = p.release();
     });
 }

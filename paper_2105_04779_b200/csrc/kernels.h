@@ -22,6 +22,7 @@ struct GemmArgs {
     int64_t sbz;
     int M, N, K, Z;
     float alpha;
+    const void* bias16;  // optional bf16 copy of bias (cuBLASLt's bias epilogue needs D's type)
 };
 void launch_simt_gemm(int dtype, const GemmArgs& g, cudaStream_t st);
 
@@ -39,6 +40,12 @@ void launch_el_decode_simt(int dtype, const void* qp, const void* H, const int* 
 // N % 16 == 0.  Returns false if the shape is outside its envelope.
 bool tc_gemm_supported(const GemmArgs& g);
 void launch_tc_gemm(const GemmArgs& g, cudaStream_t st);
+
+// Plain (Z == 1) bf16 GEMM + bias through cuBLASLt (blas_lt.cu): used for the two dense
+// projections Y.W_Q + b_Q and V.W_O + b_O.  cuBLASLt's bias epilogue takes the bias in
+// the output type, so the bf16 path stores b_Q and b_O in bf16 (GemmArgs::bias16).
+bool lt_gemm_supported(const GemmArgs& g);
+void launch_lt_gemm(const GemmArgs& g, cudaStream_t st);
 
 // Testing hook: when non-null, the tcgen05 decode writes clock64 stamps of its
 // first cluster: trace[(cta*24 + event)*64 + tile].

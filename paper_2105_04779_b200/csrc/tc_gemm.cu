@@ -8,12 +8,15 @@
 //
 // Persistent, warp-specialised: one CTA per SM walks 128 x BN output tiles
 // (n fastest, so consecutive tiles reuse the A block from L2).
-//   warp 0      TMA producer: 128x64 / BNx64 bf16 K-slices (SWIZZLE_128B) through a
-//               4-stage mbarrier ring;
+//   warp 0      TMA producer: 128x64 / BNx64 bf16 K-slices (SWIZZLE_128B) through an
+//               mbarrier ring;
 //   warp 1      MMA issuer (tcgen05.mma M=128 N=BN K=16, fp32 accumulator in TMEM,
 //               double-buffered so the epilogue of tile t overlaps the MMAs of t+1);
-//   warps 2..5  epilogue: tcgen05.ld -> alpha/bias -> bf16 -> padded smem stage ->
-//               coalesced 16-byte global stores.
+//   warps 2..9  epilogue, two warps per TMEM lane quadrant (column halves):
+//               tcgen05.ld -> alpha/bias -> bf16 -> SWIZZLE_128B smem stage (double
+//               buffered) -> TMA tensor store (3-D maps, so head-strided outputs such
+//               as q' rows r*h + i are written directly).  The write-bound shapes
+//               (q' = Q_i.Wk_i^T: K = 64, 42 MB out at B = 320) live in this epilogue.
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx_sm100.cuh"
@@ -24,18 +27,23 @@ namespace elattn_gpu {
 namespace {
 
 constexpr int kBM = 128, kBK = 64;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 template <int BN>
 struct GemmSmem {
-    static constexpr int kStages = BN >= 128 ? 5 : 7;  // deepest ring that fits next to the stage
     static constexpr uint32_t kABytes = kBM * kBK * 2;
     static constexpr uint32_t kBBytes = BN * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    static constexpr int kPitch = BN * 2 + 16;  // staged output row (bytes), +16 spreads banks
-    static constexpr uint32_t kStageOff = kStages * kStageBytes;
-    static constexpr uint32_t kBarOff = kStageOff + kBM * kPitch;
+    static constexpr uint32_t kOutBox = kBM * 128;           // one 128-row x 64-col SW128 box (16 KB)
+    static constexpr uint32_t kOutBytes = (BN / 64) * kOutBox;  // one output stage
+    static constexpr uint32_t kFixed = 2 * kOutBytes + 256 + 1024;
+    static constexpr int kStagesFit = int((232448u - kFixed) / kStageBytes);
+    static constexpr int kStages = kStagesFit < 8 ? kStagesFit : 8;
+    static constexpr uint32_t kOutOff = kStages * kStageBytes;
+    static constexpr uint32_t kBarOff = kOutOff + 2 * kOutBytes;
     static constexpr uint32_t kTotal = kBarOff + 256 + 1024;  // + barriers + alignment slack
+    static_assert(kTotal <= 232448, "smem");
 };
 
 struct GemmParams {
@@ -44,12 +52,10 @@ struct GemmParams {
     float alpha;
     const float* bias;
     int64_t sbz;
-    __nv_bfloat16* C;
-    int64_t ldc, sCz;
-    int a_zm, b_zm;  // 1: tensor map coordinate order is (k, z, m) instead of (k, m, z)
+    int a_zm, b_zm, c_zm;  // 1: tensor map coordinate order is (k, z, m) instead of (k, m, z)
 };
 
-__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -58,14 +64,15 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, GemmParams p) {
     using S = GemmSmem<BN>;
     constexpr int kStages = S::kStages;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B, by offsetting the __shared__ array itself so
     // the compiler keeps the shared address space (LDS/STS, not generic LD/ST)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* stage = smem + S::kStageOff;
+    uint8_t* out_stage = smem + S::kOutOff;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOff);
     uint64_t* empty = full + kStages;
     uint64_t* acc_full = empty + kStages;  // [2] MMA -> epilogue
@@ -88,13 +95,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ptx::elect_one()) {
             ptx::prefetch_tmap(&tmA);
             ptx::prefetch_tmap(&tmB);
+            ptx::prefetch_tmap(&tmC);
             for (int s = 0; s < kStages; ++s) {
                 ptx::mbar_init(&full[s], 1);
                 ptx::mbar_init(&empty[s], 1);
             }
             for (int i = 0; i < 2; ++i) {
                 ptx::mbar_init(&acc_full[i], 1);
-                ptx::mbar_init(&acc_empty[i], 4);
+                ptx::mbar_init(&acc_empty[i], kEpiWarps);
             }
             ptx::fence_mbar_init();
         }
@@ -160,67 +168,72 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
         }
     } else {
-        // ---- epilogue warps 2..5: TMEM lane quadrant = warp % 4 -> output rows
-        const uint32_t qd = warp & 3;
-        const int r_local = int(qd) * 32 + int(lane);
-        const int tid = int(threadIdx.x) - 64;
+        // ---- epilogue warps 2..9: quadrant qd = warp % 4 (TMEM lanes / tile rows
+        // 32 qd..), column half ch = (warp - 2) / 4 (tile columns ch*BN/2 ..)
+        const uint32_t qd = warp & 3, ch = (warp - 2) >> 2;
+        const int row = int(qd) * 32 + int(lane);  // row within the tile
+        const bool leader = warp == 2 && lane == 0;
+        constexpr int kHalf = BN / 2;
         int local = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
             int z, m0, n0;
             tile_coords(t, z, m0, n0);
             const int ab = local & 1;
+            uint8_t* stage = out_stage + ab * S::kOutBytes;
             ptx::mbar_wait(&acc_full[ab], (local >> 1) & 1);
             ptx::tc_fence_after();
-            const uint32_t t_row = tmem + ((qd * 32) << 16) + ab * BN;
+            // the TMA store that last used this stage (tile local-2) must have read it
+            if (leader) ptx::bulk_wait_group_read<1>();
+            epi_bar_sync();
+            const uint32_t t_row = tmem + ((qd * 32) << 16) + ab * BN + ch * kHalf;
             const float* bias = p.bias ? p.bias + z * p.sbz : nullptr;
-            epi_bar_sync();  // the stage is free (previous tile's global stores done)
-#pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+#pragma unroll
+            for (int c0 = 0; c0 < kHalf; c0 += 32) {
                 uint32_t r[32];
-                ptx::tmem_ld16(t_row + c0, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
-                ptx::tmem_ld16(t_row + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+                ptx::tmem_ld32(t_row + c0, r);
                 ptx::tmem_ld_wait();
-                if (c0 + 32 >= BN) {
-                    // accumulator fully read: let the MMA warp reuse it
+                if (c0 + 32 >= kHalf) {
+                    // this warp's part of the accumulator is read: the MMA warp may reuse it
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
                 }
-                const int n = n0 + c0;
+                const int col = int(ch) * kHalf + c0;  // tile column of r[0]
                 uint32_t packed[16];
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {
                     float v0 = __uint_as_float(r[j]) * p.alpha, v1 = __uint_as_float(r[j + 1]) * p.alpha;
                     if (bias) {
-                        v0 += (n + j < p.N) ? bias[n + j] : 0.f;
-                        v1 += (n + j + 1 < p.N) ? bias[n + j + 1] : 0.f;
+                        const int n = n0 + col + j;
+                        v0 += (n < p.N) ? __ldg(bias + n) : 0.f;
+                        v1 += (n + 1 < p.N) ? __ldg(bias + n + 1) : 0.f;
                     }
                     packed[j / 2] = pack2(v0, v1);
                 }
-                uint8_t* dst = stage + r_local * S::kPitch + c0 * 2;
+                // SWIZZLE_128B box (64 columns): 16-byte chunk c of row r at c ^ (r & 7)
+                uint8_t* box = stage + (col >> 6) * S::kOutBox + row * 128;
+                const int cbase = (col & 63) >> 3;
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    *reinterpret_cast<uint4*>(dst + 16 * q) =
+                    *reinterpret_cast<uint4*>(box + (((cbase + q) ^ (row & 7)) << 4)) =
                         make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
             }
+            ptx::fence_proxy_async_smem();
             epi_bar_sync();
-            constexpr int kVecPerRow = BN / 8;  // 16-byte vectors per output row
-            const bool full_n = (n0 + BN <= p.N);
-#pragma unroll 4
-            for (int idx = tid; idx < kBM * kVecPerRow; idx += 128) {
-                const int rr = idx / kVecPerRow, cv = idx % kVecPerRow;
-                const int row = m0 + rr, n = n0 + cv * 8;
-                if (row >= p.M) continue;
-                __nv_bfloat16* Crow = p.C + z * p.sCz + int64_t(row) * p.ldc;
-                const uint8_t* src = stage + rr * S::kPitch + cv * 16;
-                if (full_n || n + 8 <= p.N) {
-                    *reinterpret_cast<uint4*>(Crow + n) = *reinterpret_cast<const uint4*>(src);
-                } else {
-                    for (int j = 0; j < 8 && n + j < p.N; ++j)
-                        Crow[n + j] = reinterpret_cast<const __nv_bfloat16*>(src)[j];
+            if (leader) {
+#pragma unroll
+                for (int bx = 0; bx < BN / 64; ++bx) {
+                    if (n0 + 64 * bx >= p.N) break;
+                    const int c0 = n0 + 64 * bx;
+                    if (p.c_zm)
+                        ptx::tma_store_3d(&tmC, stage + bx * S::kOutBox, c0, z, m0);
+                    else
+                        ptx::tma_store_3d(&tmC, stage + bx * S::kOutBox, c0, m0, z);
                 }
+                ptx::bulk_commit_group();
             }
         }
+        if (leader) ptx::bulk_wait_group<0>();
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -264,17 +277,18 @@ template <int BN>
 void launch_bn(const GemmArgs& g, cudaStream_t st) {
     GemmParams p{};
     p.M = g.M, p.N = g.N, p.K = g.K, p.Z = g.Z, p.alpha = g.alpha, p.bias = g.bias, p.sbz = g.sbz;
-    p.C = static_cast<__nv_bfloat16*>(g.C), p.ldc = g.ldc, p.sCz = g.sCz;
     p.tiles_m = int(ceil_div(g.M, kBM));
     p.tiles_n = int(ceil_div(g.N, BN));
     CUtensorMap ta = operand_map(g.A, g.lda, g.sAz, g.M, g.K, g.Z, kBM, &p.a_zm);
     CUtensorMap tb = operand_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, BN, &p.b_zm);
+    // output C[z][m][n]: boxes of 64 columns x 128 rows (SWIZZLE_128B), clipped at M / N
+    CUtensorMap tc = operand_map(g.C, g.ldc, g.sCz, g.M, g.N, g.Z, kBM, &p.c_zm);
     auto kern = tc_gemm_kernel<BN>;
     constexpr uint32_t smem = GemmSmem<BN>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const int tiles = p.Z * p.tiles_m * p.tiles_n;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, kThreads, smem, st>>>(ta, tb, p);
+    kern<<<grid, kThreads, smem, st>>>(ta, tb, tc, p);
     ELA_CHECK_LAUNCH();
 }
 

@@ -34,28 +34,51 @@ Wk = torch.randn(h, d_m, d_k, device=dev).to(bf)
 WvT = torch.randn(h, d_k, d_m, device=dev).to(bf)
 WoT = torch.randn(d_m, h * d_k, device=dev).to(bf)
 bias = torch.randn(max(h * d_k, d_m), device=dev)
-st = torch.cuda.current_stream().cuda_stream
 shapes = {
     "Q=Y.Wq": (Y, d_m, 0, WqT, d_m, 0, Q, h * d_k, 0, bias, 0, R, h * d_k, d_m, 1),
     "q'=Q_i.Wk_i^T": (Q, h * d_k, d_k, Wk, d_k, d_m * d_k, qp, h * d_m, d_m, None, 0, R, d_m, d_k, h),
     "V_i=C_i.Wv_i": (ctx, h * d_m, d_m, WvT, d_m, d_k * d_m, V, h * d_k, d_k, bias, d_k, R, d_k, d_m, h),
     "out=V.Wo": (V, h * d_k, 0, WoT, h * d_k, 0, out, d_m, 0, bias, 0, R, d_m, h * d_k, 1),
 }
+
+
+def graph_time(fn, reps):
+    """device time per call: `reps` calls captured in one CUDA graph, replayed (no host gaps)"""
+    gs = torch.cuda.Stream()
+    gs.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(gs):
+        fn()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=gs):
+            for _ in range(reps):
+                fn()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3
+
+
 for name, (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z) in shapes.items():
     def run():
         capi.check(L.elattn_gpu_testing_gemm_bf16(A.data_ptr(), lda, sAz, Bm.data_ptr(), ldb, sBz, C.data_ptr(), ldc,
                                                   sCz, bs.data_ptr() if bs is not None else None, sbz, M, N, K, Z,
-                                                  1.0, 1, st))
-    for _ in range(3):
-        run()
+                                                  1.0, 1, torch.cuda.current_stream().cuda_stream))
+    run()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.reps):
-        run()
-    e1.record()
-    torch.cuda.synchronize()
-    us = e0.elapsed_time(e1) / a.reps * 1e3
+    us = graph_time(run, a.reps)
     byt = (M * K * Z + N * K * Z + M * N * Z) * 2
     print(json.dumps({"gemm": name, "us": round(us, 2), "GBps": round(byt / us / 1e3, 1),
                       "TFLOPs": round(2 * M * N * K * Z / us / 1e6, 1)}))
+
+# cuBLAS (torch.matmul) on the two plain shapes, for reference
+for name, (A, Bm) in {"cublas Q=Y.Wq": (Y, WqT), "cublas out=V.Wo": (V, WoT)}.items():
+    us = graph_time(lambda: torch.matmul(A, Bm.t()), a.reps)
+    print(json.dumps({"gemm": name, "us": round(us, 2)}))
+qh = Q.view(R, h, d_k).transpose(0, 1)  # [h, R, d_k]
+us = graph_time(lambda: torch.bmm(qh, Wk.transpose(1, 2)), a.reps)
+print(json.dumps({"gemm": "cublas q' (bmm, [h][R][d_m] layout)", "us": round(us, 2)}))
