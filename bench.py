@@ -244,19 +244,14 @@ def gpu_arm(args):
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     H = (torch.rand((B, n, d_m), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
     Y0 = (torch.rand((B * x, d_m), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
-    bufs = [torch.empty_like(Y0) for _ in range(2)]
-    ws_need = layers[0].dev.workspace_size(B, x, n)
-    ws = torch.empty(ws_need, dtype=torch.uint8, device=dev)
-    for ly in layers:
-        ly._ws = ws  # one shared stream-ordered workspace
-
+    # the public batched decoder-step API: L layers over the shared H, captured once into
+    # a CUDA graph by the library (elattn_gpu_decoder_create), replayed per step
+    dec = E.DecoderStep(layers, H, B, x)
+    dec.Y.copy_(Y0)
     stream = torch.cuda.current_stream()
 
-    def step(y_in):
-        y = y_in
-        for l in range(L):
-            y = layers[l].step(y, H, out=bufs[l % 2], stream=stream)
-        return y
+    def step():
+        return dec.run(stream=stream)
 
     def barrier():
         if world > 1:
@@ -264,7 +259,7 @@ def gpu_arm(args):
         torch.cuda.synchronize()
 
     for _ in range(max(args.warmup, 3)):
-        step(Y0)
+        step()
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -273,7 +268,7 @@ def gpu_arm(args):
     barrier()
     e0.record(stream)
     for _ in range(args.steps):
-        step(Y0)
+        step()
     e1.record(stream)
     barrier()
     launches = int(capi.lib().elattn_gpu_launch_count())
@@ -314,16 +309,15 @@ def gpu_arm(args):
     # ---- e2e through the public API: pinned host Y in, output back, every step
     Yh = torch.empty(B * x, d_m, dtype=torch.bfloat16, pin_memory=True).copy_(Y0.cpu())
     Oh = torch.empty(B * x, d_m, dtype=torch.bfloat16, pin_memory=True)
-    Yd = torch.empty_like(Y0)
     for _ in range(2):
-        Yd.copy_(Yh, non_blocking=True)
-        Oh.copy_(step(Yd), non_blocking=True)
+        dec.Y.copy_(Yh, non_blocking=True)
+        Oh.copy_(step(), non_blocking=True)
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for _ in range(args.steps):
-        Yd.copy_(Yh, non_blocking=True)
-        Oh.copy_(step(Yd), non_blocking=True)
+        dec.Y.copy_(Yh, non_blocking=True)
+        Oh.copy_(step(), non_blocking=True)
     f1.record(stream)
     barrier()
     e2e_ms = f0.elapsed_time(f1) / args.steps
@@ -336,7 +330,8 @@ def gpu_arm(args):
     # (input sharding: rank r owns inputs [r*B, (r+1)*B) of the global batch)
     from paper_2105_04779_b200.sharding import gather_outputs, shard_range
 
-    out = step(Y0)
+    dec.Y.copy_(Y0)
+    out = step()
     assert shard_range(world * B, rank, world) == (rank * B, (rank + 1) * B)
     full = gather_outputs(out, world * B, x) if world > 1 else out
     finite = bool(torch.isfinite(full.float()).all())
@@ -364,8 +359,9 @@ def gpu_arm(args):
             "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * x * d_m * 2,
                     "d2h_bytes_per_step": B * x * d_m * 2,
-                    "note": "through ElAttentionLayer.step (C ABI); Y H2D from pinned host + output D2H "
-                            "every step; H (encoder state) resident, as in the reference's DecoderState"},
+                    "note": "through DecoderStep.run (C ABI elattn_gpu_decoder_run, one CUDA-graph "
+                            "launch per step); Y H2D from pinned host + output D2H every step; H "
+                            "(encoder state) resident, as in the reference's DecoderState"},
             "roofline": {"bound": "hbm", "achieved": dec_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": dec_gbs / hbm, "traffic": traffic_from_profile(B, n, d_m), "peak_source": peak_src,
                          "kernel": "fused EL decode (stage 2)", "kernel_ms": dec_ms,

@@ -146,6 +146,29 @@ size_t elattn_gpu_workspace_size(elattn_gpu_params_t params, int B, int g, int n
  */
 int elattn_gpu_decode_kernel_kind(elattn_gpu_params_t params, int g);
 
+/*
+ * Batched decoder step.  Replaces the reference's decoder-step loop
+ * (model.hpp:357-385: for every lane, for every layer, el_attention(yc,
+ * encoder_output, cross_attn) at :373-377; lanes iterated by decoding.hpp:259-260) for
+ * all B*x lanes at once: out = layer_{L-1}( ... layer_0(Y) ... ), each layer an
+ * elattn_gpu_el_attention_step over the SAME encoder states H (one per input, shared by
+ * every layer, beam and head — EL's cache saving).  The L steps (query expansion, fused
+ * decode, projections) are captured once into a CUDA graph on a private stream and
+ * replayed by elattn_gpu_decoder_run, so a step costs one graph launch on the host.
+ *   layers       L params handles (same h, d_m, d_k, dtype)
+ *   H            [B][n][d_m] device, n_per_input device int[B] or NULL (as in _step)
+ *   Y_in, out    [B*x][d_m] device buffers bound at creation: write Y_in, run, read out
+ *                (out may alias Y_in)
+ * Errors: PARAM (null / mismatched layers), SHAPE, STATE (n < 1), OOM, CUDA.
+ */
+typedef struct elattn_gpu_decoder_s* elattn_gpu_decoder_t;
+int elattn_gpu_decoder_create(const elattn_gpu_params_t* layers, int L, const void* H, const int* n_per_input,
+                              int B, int x, int n, const void* Y_in, void* out, elattn_gpu_decoder_t* dec);
+int elattn_gpu_decoder_run(elattn_gpu_decoder_t dec, elattn_stream_t stream);
+int elattn_gpu_decoder_destroy(elattn_gpu_decoder_t dec);
+/* our own kernels launched by one run (the graph's kernel nodes outside cuBLASLt) */
+int64_t elattn_gpu_decoder_kernels_per_run(elattn_gpu_decoder_t dec);
+
 /* Device-kernel launches issued by this thread since the last reset (for bench
  * accounting of gpu_launches). */
 int64_t elattn_gpu_launch_count(void);

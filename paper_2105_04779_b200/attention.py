@@ -27,6 +27,7 @@ from . import capi
 from .capi import DTYPE_BF16, DTYPE_F32, ParamError, ShapeError, StateError
 
 __all__ = [
+    "DecoderStep",
     "Rng", "seeded_uniform", "AttentionParams", "ElQuery", "DeviceParams", "ElAttentionLayer",
     "build_el_query", "fold_el_queries", "el_attention", "el_attention_folded",
     "DTYPE_F32", "DTYPE_BF16",
@@ -288,6 +289,60 @@ class ElAttentionLayer:
             self.dev.handle, qprime.data_ptr(), None, H.data_ptr(), npi, B, g, n, out.data_ptr(),
             ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
         return out
+
+
+class DecoderStep:
+    """Batched decoder step over L EL cross-attention layers sharing one encoder state
+    per input — the reference's per-lane, per-layer ``el_attention`` loop
+    (model.hpp:357-385, lanes from decoding.hpp:259-260) for all B*x lanes at once:
+    ``out = layer_{L-1}(... layer_0(Y) ...)``.  Captured once into a CUDA graph by the
+    library (``elattn_gpu_decoder_create``); ``run()`` replays it.
+
+    ``Y`` and ``out`` are bound device buffers: write the step's query rows into ``self.Y``
+    (or pass them to ``run``), read the result from ``self.out``.
+    """
+
+    def __init__(self, layers: Sequence[ElAttentionLayer], H, B: int, x: int, n_per_input=None):
+        torch = _torch()
+        if not layers:
+            raise ParamError("DecoderStep: need at least one layer")
+        l0 = layers[0]
+        l0._check(H, None, "H")
+        if H.dim() != 3 or H.shape[0] != B:
+            raise ShapeError("DecoderStep: H must be [B, n, d_m]")
+        self.layers = list(layers)  # keep the params handles alive
+        self.H, self.npi = H, n_per_input
+        self.B, self.x, self.n = B, x, int(H.shape[1])
+        d_m = l0.dev.d_m
+        self.Y = torch.zeros(B * x, d_m, dtype=_tdtype(l0.dtype), device="cuda")
+        self.out = torch.empty_like(self.Y)
+        handles = (ctypes.c_void_p * len(layers))(*[ly.dev.handle for ly in layers])
+        h = ctypes.c_void_p()
+        npi = n_per_input.data_ptr() if n_per_input is not None else None
+        capi.check(capi.lib().elattn_gpu_decoder_create(handles, len(layers), H.data_ptr(), npi, B, x, self.n,
+                                                        self.Y.data_ptr(), self.out.data_ptr(), ctypes.byref(h)))
+        self.handle = h.value
+        self.kernels_per_run = int(capi.lib().elattn_gpu_decoder_kernels_per_run(self.handle))
+
+    def run(self, Y=None, stream=None):
+        """One decoder step on ``stream``; optional ``Y`` [B*x, d_m] is copied into the
+        bound input first.  Returns the bound output tensor."""
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        if Y is not None:
+            with torch.cuda.stream(st):
+                self.Y.copy_(Y, non_blocking=True)
+        capi.check(capi.lib().elattn_gpu_decoder_run(self.handle, _stream_ptr(st)))
+        return self.out
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                capi.lib().elattn_gpu_decoder_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
 
 
 # ---------------------------------------------------------------------------

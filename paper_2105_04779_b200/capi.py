@@ -30,6 +30,10 @@ EXPORTED_SYMBOLS = (
     "elattn_gpu_workspace_size",
     "elattn_gpu_decode_kernel_kind",
     "elattn_gpu_launch_count",
+    "elattn_gpu_decoder_create",
+    "elattn_gpu_decoder_run",
+    "elattn_gpu_decoder_destroy",
+    "elattn_gpu_decoder_kernels_per_run",
     "elattn_gpu_reset_launch_count",
 )
 
@@ -95,6 +99,12 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.elattn_gpu_workspace_size.restype = sz
     lib.elattn_gpu_decode_kernel_kind.argtypes = [vp, i32]
     lib.elattn_gpu_launch_count.restype = i64
+    lib.elattn_gpu_decoder_create.argtypes = [ctypes.POINTER(vp), i32, vp, vp, i32, i32, i32, vp, vp,
+                                              ctypes.POINTER(vp)]
+    lib.elattn_gpu_decoder_run.argtypes = [vp, vp]
+    lib.elattn_gpu_decoder_destroy.argtypes = [vp]
+    lib.elattn_gpu_decoder_kernels_per_run.argtypes = [vp]
+    lib.elattn_gpu_decoder_kernels_per_run.restype = i64
     for name in EXPORTED_SYMBOLS:
         fn = getattr(lib, name)
         if fn.restype is ctypes.c_int and name not in ("elattn_gpu_decode_kernel_kind",):

@@ -104,4 +104,13 @@ void launch_lt_gemm(const GemmArgs& g, cudaStream_t st) {
                                 kWorkspace, st));
 }
 
+void release_lt_stream(cudaStream_t st) {
+    LtState& S = state();
+    std::lock_guard<std::mutex> lock(S.mu);
+    auto it = S.workspace.find(st);
+    if (it == S.workspace.end()) return;
+    if (it->second) cudaFree(it->second);
+    S.workspace.erase(it);
+}
+
 }  // namespace elattn_gpu

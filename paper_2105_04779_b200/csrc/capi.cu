@@ -421,3 +421,125 @@ extern "C" int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H,
         }
     });
 }
+
+// ---------------------------------------------------------------- batched decoder step
+struct elattn_gpu_decoder_s {
+    std::vector<elattn_gpu_params_t> layers;
+    int B = 0, x = 0, n = 0;
+    cudaStream_t st = nullptr;  // private capture stream (owns its per-stream scratch)
+    void* ybuf[2] = {nullptr, nullptr};
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
+};
+
+namespace elattn_gpu {
+void release_stream_scratch(cudaStream_t st);  // el_decode_tc.cu
+void release_lt_stream(cudaStream_t st);       // blas_lt.cu
+}  // namespace elattn_gpu
+
+namespace {
+void decoder_free(elattn_gpu_decoder_s* d) {
+    if (!d) return;
+    if (d->exec) cudaGraphExecDestroy(d->exec);
+    if (d->graph) cudaGraphDestroy(d->graph);
+    for (void* p : {d->ybuf[0], d->ybuf[1], d->ws})
+        if (p) cudaFree(p);
+    if (d->st) {
+        cudaStreamSynchronize(d->st);
+        elattn_gpu::release_stream_scratch(d->st);
+        elattn_gpu::release_lt_stream(d->st);
+        cudaStreamDestroy(d->st);
+    }
+    delete d;
+}
+
+// one step: L layers, ping-pong intermediate rows, last layer writes `out`
+void decoder_enqueue(elattn_gpu_decoder_s* d, const void* H, const int* npi, const void* Y_in, void* out) {
+    const elattn_gpu_params_s* p0 = d->layers[0];
+    const int64_t R = int64_t(d->B) * d->x;
+    const size_t e = dtype_bytes(p0->dtype);
+    const size_t qb = size_t(R) * p0->h * p0->d_k * e, qpb = size_t(R) * p0->h * p0->d_m * e;
+    char* base = static_cast<char*>(d->ws);
+    void* Q = base;
+    void* qp = base + align256(qb);
+    void* C = base + align256(qb) + align256(qpb);
+    void* V = base + align256(qb) + 2 * align256(qpb);
+    const void* y = Y_in;
+    const int L = int(d->layers.size());
+    for (int l = 0; l < L; ++l) {
+        void* dst = (l == L - 1) ? out : d->ybuf[l & 1];
+        const elattn_gpu_params_s* p = d->layers[l];
+        query_expansion(p, y, R, Q, qp, d->st);
+        decode(p, qp, H, npi, d->B, d->x * p->h, d->n, C, d->st);
+        output_projection(p, C, R, V, dst, d->st);
+        y = dst;
+    }
+}
+}  // namespace
+
+extern "C" int elattn_gpu_decoder_create(const elattn_gpu_params_t* layers, int L, const void* H,
+                                         const int* n_per_input, int B, int x, int n, const void* Y_in, void* out,
+                                         elattn_gpu_decoder_t* dec) {
+    return guarded([&] {
+        ELA_REQUIRE(dec != nullptr, ELATTN_ERR_PARAM, "decoder_create: null output handle pointer");
+        *dec = nullptr;
+        ELA_REQUIRE(layers != nullptr && L >= 1, ELATTN_ERR_PARAM, "decoder_create: need at least one layer");
+        ELA_REQUIRE(B >= 1 && x >= 1, ELATTN_ERR_SHAPE, "decoder_create: B and x must be >= 1");
+        ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "decoder_create: empty context");
+        ELA_REQUIRE(H && Y_in && out, ELATTN_ERR_PARAM, "decoder_create: null buffer");
+        const elattn_gpu_params_s* p0 = layers[0];
+        ELA_REQUIRE(p0 != nullptr, ELATTN_ERR_PARAM, "decoder_create: null layer");
+        for (int l = 0; l < L; ++l) {
+            const elattn_gpu_params_s* p = layers[l];
+            ELA_REQUIRE(p && p->h == p0->h && p->d_m == p0->d_m && p->d_k == p0->d_k && p->dtype == p0->dtype,
+                        ELATTN_ERR_PARAM, "decoder_create: layers must share h, d_m, d_k and dtype");
+        }
+        std::unique_ptr<elattn_gpu_decoder_s, void (*)(elattn_gpu_decoder_s*)> d(new elattn_gpu_decoder_s,
+                                                                                 decoder_free);
+        d->layers.assign(layers, layers + L);
+        d->B = B, d->x = x, d->n = n;
+        const int64_t R = int64_t(B) * x;
+        const size_t rows_bytes = size_t(R) * p0->d_m * dtype_bytes(p0->dtype);
+        ELA_CHECK_CUDA(cudaStreamCreateWithFlags(&d->st, cudaStreamNonBlocking));
+        ELA_CHECK_CUDA(cudaMalloc(&d->ybuf[0], rows_bytes));
+        ELA_CHECK_CUDA(cudaMalloc(&d->ybuf[1], rows_bytes));
+        d->ws_bytes = step_workspace(p0, R);
+        ELA_CHECK_CUDA(cudaMalloc(&d->ws, d->ws_bytes));
+        // eager run first: allocates this stream's scratch (split records, cuBLASLt
+        // workspace) outside the capture, and surfaces launch errors directly
+        decoder_enqueue(d.get(), H, n_per_input, Y_in, out);
+        ELA_CHECK_CUDA(cudaStreamSynchronize(d->st));
+        const int64_t before = g_launches;
+        ELA_CHECK_CUDA(cudaStreamBeginCapture(d->st, cudaStreamCaptureModeThreadLocal));
+        try {
+            decoder_enqueue(d.get(), H, n_per_input, Y_in, out);
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(d->st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        d->kernels = g_launches - before;
+        g_launches = before;
+        ELA_CHECK_CUDA(cudaStreamEndCapture(d->st, &d->graph));
+        ELA_CHECK_CUDA(cudaGraphInstantiate(&d->exec, d->graph, 0));
+        *dec = d.release();
+    });
+}
+
+extern "C" int elattn_gpu_decoder_run(elattn_gpu_decoder_t dec, elattn_stream_t stream) {
+    return guarded([&] {
+        ELA_REQUIRE(dec != nullptr, ELATTN_ERR_PARAM, "decoder_run: null handle");
+        ELA_CHECK_CUDA(cudaGraphLaunch(dec->exec, reinterpret_cast<cudaStream_t>(stream)));
+        count_launch(int(dec->kernels));
+    });
+}
+
+extern "C" int elattn_gpu_decoder_destroy(elattn_gpu_decoder_t dec) {
+    return guarded([&] { decoder_free(dec); });
+}
+
+extern "C" int64_t elattn_gpu_decoder_kernels_per_run(elattn_gpu_decoder_t dec) { return dec ? dec->kernels : -1; }

@@ -954,6 +954,18 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
     }
 }
 
+}  // namespace
+
+void release_stream_scratch(cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    auto it = g_scratch.find(st);
+    if (it == g_scratch.end()) return;
+    if (it->second.part) cudaFree(it->second.part);
+    g_scratch.erase(it);
+}
+
+namespace {
+
 constexpr int kMinChunkTiles = 8;  // bounds the segments per input (merge cost) at small B
 
 template <int UNITS>

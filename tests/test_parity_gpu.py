@@ -201,3 +201,43 @@ def test_bf16_full_size_strided_subset(gpu):
         Hb = Hd[b:b + 1].double().cpu().numpy()
         want = O.el_layer_step(pr, Yb, Hb, c["x"])
         assert rel_err(out[b * c["x"]:(b + 1) * c["x"]], want) <= TOL[1], b
+
+
+@pytest.mark.parametrize("npi_mode", [False, True])
+def test_decoder_step_graph_matches_layer_chain(gpu, npi_mode):
+    """DecoderStep (L layers captured into one CUDA graph) == chaining layer.step L times,
+    bit-exactly, on replay after replay; and the 2-layer chain matches the oracle."""
+    import torch
+
+    E = gpu
+    c = BART_CFG
+    B, L, n = 3, 3, 200
+    layers = [E.ElAttentionLayer(E.AttentionParams.random(c["h"], c["d_m"], c["d_k"], E.Rng(40 + l)), E.DTYPE_BF16)
+              for l in range(L)]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    H = (torch.rand((B, n, c["d_m"]), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    npi = torch.tensor([200, 17, 130], dtype=torch.int32, device="cuda") if npi_mode else None
+    dec = E.DecoderStep(layers, H, B, c["x"], npi)
+    assert dec.kernels_per_run >= 3 * L  # q' GEMM, decode, V GEMM per layer (+ merge if split)
+    for it in range(2):
+        Y = (torch.rand((B * c["x"], c["d_m"]), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+        got = dec.run(Y).clone()
+        torch.cuda.synchronize()
+        y = Y
+        for ly in layers:
+            y = ly.step(y, H, npi)
+        torch.cuda.synchronize()
+        assert torch.equal(got, y), it
+    # oracle for the first two layers of the chain
+    dec2 = E.DecoderStep(layers[:2], H, B, c["x"], npi)
+    out = dec2.run(Y).double().cpu().numpy()
+    pr = [round_params(O.params_random(c["h"], c["d_m"], c["d_k"], O.OracleRng(40 + l)), E.DTYPE_BF16)
+          for l in range(2)]
+    from paper_2105_04779_b200.attention import round_to_dtype
+
+    Hh = H.double().cpu().numpy()
+    y = Y.double().cpu().numpy()
+    nl = npi.cpu().numpy() if npi is not None else None
+    for l in range(2):
+        y = round_to_dtype(O.el_layer_step(pr[l], y, Hh, c["x"], nl), E.DTYPE_BF16)
+    assert rel_err(out, y) <= TOL[1]
