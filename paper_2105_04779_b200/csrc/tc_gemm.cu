@@ -35,13 +35,18 @@ struct GemmSmem {
     static constexpr uint32_t kABytes = kBM * kBK * 2;
     static constexpr uint32_t kBBytes = BN * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    static constexpr uint32_t kOutBox = kBM * 128;           // one 128-row x 64-col SW128 box (16 KB)
-    static constexpr uint32_t kOutBytes = (BN / 64) * kOutBox;  // one output stage
-    static constexpr uint32_t kFixed = 2 * kOutBytes + 256 + 1024;
+    // epilogue: every warp stages its own 32 rows x BN/2 columns as 32-row x 64-column
+    // SWIZZLE_128B boxes (4 KB each) and stores them itself, double buffered
+    static constexpr int kBoxCols = BN / 2 < 64 ? BN / 2 : 64;  // 64 (SW128) or 32 (SW64)
+    static constexpr uint32_t kWarpBox = 32 * kBoxCols * 2;
+    static constexpr uint32_t kWarpStage = (BN / 2) / kBoxCols * kWarpBox;
+    static constexpr int kOutStages = 2;
+    static constexpr uint32_t kOutBytes = kEpiWarps * kOutStages * kWarpStage;
+    static constexpr uint32_t kFixed = kOutBytes + 256 + 1024;
     static constexpr int kStagesFit = int((232448u - kFixed) / kStageBytes);
     static constexpr int kStages = kStagesFit < 8 ? kStagesFit : 8;
     static constexpr uint32_t kOutOff = kStages * kStageBytes;
-    static constexpr uint32_t kBarOff = kOutOff + 2 * kOutBytes;
+    static constexpr uint32_t kBarOff = kOutOff + kOutBytes;
     static constexpr uint32_t kTotal = kBarOff + 256 + 1024;  // + barriers + alignment slack
     static_assert(kTotal <= 232448, "smem");
 };
@@ -55,7 +60,6 @@ struct GemmParams {
     int a_zm, b_zm, c_zm;  // 1: tensor map coordinate order is (k, z, m) instead of (k, m, z)
 };
 
-__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -83,10 +87,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
     const int num_k = p.K / kBK;
     const int num_tiles = p.Z * p.tiles_m * p.tiles_n;
+    // z (head) fastest: the CTAs running concurrently touch the SAME rows r of the
+    // head-interleaved layouts (q' / C rows r*h + i), so their 128-byte row pieces land
+    // in the same DRAM pages instead of 32 KB apart
     auto tile_coords = [&](int t, int& z, int& m0, int& n0) {
-        const int per_z = p.tiles_m * p.tiles_n;
-        z = t / per_z;
-        const int r = t % per_z;
+        z = t % p.Z;
+        const int r = t / p.Z;
         m0 = (r / p.tiles_n) * kBM;
         n0 = (r % p.tiles_n) * BN;
     };
@@ -169,71 +175,77 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ---- epilogue warps 2..9: quadrant qd = warp % 4 (TMEM lanes / tile rows
-        // 32 qd..), column half ch = (warp - 2) / 4 (tile columns ch*BN/2 ..)
+        // 32 qd..), column half ch = (warp - 2) / 4 (tile columns ch*BN/2 ..).  Each warp
+        // is independent: TMEM -> registers -> its own SWIZZLE_128B stage -> its own TMA
+        // store (boxes of 32 rows x 64 columns); no CTA-wide barrier in the tile loop.
         const uint32_t qd = warp & 3, ch = (warp - 2) >> 2;
-        const int row = int(qd) * 32 + int(lane);  // row within the tile
-        const bool leader = warp == 2 && lane == 0;
         constexpr int kHalf = BN / 2;
+        uint8_t* my_stage = out_stage + (warp - 2) * S::kOutStages * S::kWarpStage;
         int local = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
             int z, m0, n0;
             tile_coords(t, z, m0, n0);
             const int ab = local & 1;
-            uint8_t* stage = out_stage + ab * S::kOutBytes;
+            uint8_t* stage = my_stage + (local % S::kOutStages) * S::kWarpStage;
             ptx::mbar_wait(&acc_full[ab], (local >> 1) & 1);
             ptx::tc_fence_after();
-            // the TMA store that last used this stage (tile local-2) must have read it
-            if (leader) ptx::bulk_wait_group_read<1>();
-            epi_bar_sync();
             const uint32_t t_row = tmem + ((qd * 32) << 16) + ab * BN + ch * kHalf;
+            uint32_t rr[kHalf];  // this warp's 32 rows x kHalf columns, one TMEM round trip
+#pragma unroll
+            for (int c0 = 0; c0 < kHalf; c0 += 32) ptx::tmem_ld32(t_row + c0, *reinterpret_cast<uint32_t(*)[32]>(&rr[c0]));
+            ptx::tmem_ld_wait();
+            // this warp's part of the accumulator is read: the MMA warp may reuse it
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                ptx::mbar_arrive(&acc_empty[ab]);
+                ptx::bulk_wait_group_read<S::kOutStages - 1>();  // this stage's previous store has read it
+            }
+            __syncwarp();
             const float* bias = p.bias ? p.bias + z * p.sbz : nullptr;
 #pragma unroll
             for (int c0 = 0; c0 < kHalf; c0 += 32) {
-                uint32_t r[32];
-                ptx::tmem_ld32(t_row + c0, r);
-                ptx::tmem_ld_wait();
-                if (c0 + 32 >= kHalf) {
-                    // this warp's part of the accumulator is read: the MMA warp may reuse it
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
-                }
-                const int col = int(ch) * kHalf + c0;  // tile column of r[0]
+                const uint32_t* r = rr + c0;
                 uint32_t packed[16];
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {
                     float v0 = __uint_as_float(r[j]) * p.alpha, v1 = __uint_as_float(r[j + 1]) * p.alpha;
                     if (bias) {
-                        const int n = n0 + col + j;
+                        const int n = n0 + int(ch) * kHalf + c0 + j;
                         v0 += (n < p.N) ? __ldg(bias + n) : 0.f;
                         v1 += (n + 1 < p.N) ? __ldg(bias + n + 1) : 0.f;
                     }
                     packed[j / 2] = pack2(v0, v1);
                 }
-                // SWIZZLE_128B box (64 columns): 16-byte chunk c of row r at c ^ (r & 7)
-                uint8_t* box = stage + (col >> 6) * S::kOutBox + row * 128;
-                const int cbase = (col & 63) >> 3;
+                // 32-row box of kBoxCols columns: SWIZZLE_128B (16-byte chunk c of row l at
+                // c ^ (l & 7)) for 64 columns, SWIZZLE_64B (c ^ ((l >> 1) & 3)) for 32
+                constexpr int kBoxCols = S::kBoxCols;
+                uint8_t* box = stage + (c0 / kBoxCols) * S::kWarpBox + lane * (kBoxCols * 2);
+                const int cbase = (c0 % kBoxCols) >> 3;
+                const int sw = kBoxCols == 64 ? int(lane & 7) : int((lane >> 1) & 3);
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    *reinterpret_cast<uint4*>(box + (((cbase + q) ^ (row & 7)) << 4)) =
+                    *reinterpret_cast<uint4*>(box + (((cbase + q) ^ sw) << 4)) =
                         make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
             }
             ptx::fence_proxy_async_smem();
-            epi_bar_sync();
-            if (leader) {
+            __syncwarp();
+            if (lane == 0) {
 #pragma unroll
-                for (int bx = 0; bx < BN / 64; ++bx) {
-                    if (n0 + 64 * bx >= p.N) break;
-                    const int c0 = n0 + 64 * bx;
+                for (int bx = 0; bx < kHalf / S::kBoxCols; ++bx) {
+                    const int c0 = n0 + int(ch) * kHalf + S::kBoxCols * bx;
+                    if (c0 >= p.N) break;
+                    const int r0 = m0 + int(qd) * 32;
                     if (p.c_zm)
-                        ptx::tma_store_3d(&tmC, stage + bx * S::kOutBox, c0, z, m0);
+                        ptx::tma_store_3d(&tmC, stage + bx * S::kWarpBox, c0, z, r0);
                     else
-                        ptx::tma_store_3d(&tmC, stage + bx * S::kOutBox, c0, m0, z);
+                        ptx::tma_store_3d(&tmC, stage + bx * S::kWarpBox, c0, r0, z);
                 }
                 ptx::bulk_commit_group();
             }
         }
-        if (leader) ptx::bulk_wait_group<0>();
+        if (lane == 0) ptx::bulk_wait_group<0>();
+        __syncwarp();
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -246,22 +258,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 3-D map over an operand X[z][r][k] (r = M or N rows, k contiguous):
 // returns the map and whether coordinates are ordered (k, z, r).
 CUtensorMap operand_map(const void* base, int64_t ld, int64_t sz, int rows, int K, int Z, uint32_t box_rows,
-                        int* zr_order) {
+                        int* zr_order, int box_k = kBK) {
+    const int swz = box_k * 2;  // 128-byte rows -> SWIZZLE_128B, 64-byte -> SWIZZLE_64B
     const uint64_t ld_b = uint64_t(ld) * 2;
     uint64_t sz_b = uint64_t(sz) * 2;
     if (Z == 1 || sz == 0) sz_b = ld_b * uint64_t(rows);
     if (sz_b < ld_b && Z > 1) {  // keep strides monotonic: dims (k, z, r)
         const uint64_t dims[3] = {uint64_t(K), uint64_t(Z), uint64_t(rows)};
         const uint64_t strides[2] = {sz_b, ld_b};
-        const uint32_t box[3] = {uint32_t(kBK), 1, box_rows};
+        const uint32_t box[3] = {uint32_t(box_k), 1, box_rows};
         *zr_order = 1;
-        return make_tmap_bf16(base, 3, dims, strides, box);
+        return make_tmap_bf16(base, 3, dims, strides, box, swz);
     }
     const uint64_t dims[3] = {uint64_t(K), uint64_t(rows), uint64_t(Z)};
     const uint64_t strides[2] = {ld_b, sz_b};
-    const uint32_t box[3] = {uint32_t(kBK), box_rows, 1};
+    const uint32_t box[3] = {uint32_t(box_k), box_rows, 1};
     *zr_order = 0;
-    return make_tmap_bf16(base, 3, dims, strides, box);
+    return make_tmap_bf16(base, 3, dims, strides, box, swz);
 }
 
 int num_sms() {
@@ -281,8 +294,9 @@ void launch_bn(const GemmArgs& g, cudaStream_t st) {
     p.tiles_n = int(ceil_div(g.N, BN));
     CUtensorMap ta = operand_map(g.A, g.lda, g.sAz, g.M, g.K, g.Z, kBM, &p.a_zm);
     CUtensorMap tb = operand_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, BN, &p.b_zm);
-    // output C[z][m][n]: boxes of 64 columns x 128 rows (SWIZZLE_128B), clipped at M / N
-    CUtensorMap tc = operand_map(g.C, g.ldc, g.sCz, g.M, g.N, g.Z, kBM, &p.c_zm);
+    // output C[z][m][n]: boxes of 32 rows x kBoxCols columns (one epilogue warp's piece),
+    // clipped at M / N
+    CUtensorMap tc = operand_map(g.C, g.ldc, g.sCz, g.M, g.N, g.Z, 32, &p.c_zm, GemmSmem<BN>::kBoxCols);
     auto kern = tc_gemm_kernel<BN>;
     constexpr uint32_t smem = GemmSmem<BN>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

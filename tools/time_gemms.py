@@ -14,6 +14,8 @@ from paper_2105_04779_b200 import capi  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--B", type=int, default=320)
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--only", default=None, help="substring of the GEMM name to run")
+ap.add_argument("--no-cublas", action="store_true")
 a = ap.parse_args()
 L = capi.lib()
 vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
@@ -64,6 +66,8 @@ def graph_time(fn, reps):
 
 
 for name, (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z) in shapes.items():
+    if a.only and a.only not in name:
+        continue
     def run():
         capi.check(L.elattn_gpu_testing_gemm_bf16(A.data_ptr(), lda, sAz, Bm.data_ptr(), ldb, sBz, C.data_ptr(), ldc,
                                                   sCz, bs.data_ptr() if bs is not None else None, sbz, M, N, K, Z,
@@ -76,6 +80,8 @@ for name, (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z) in shape
                       "TFLOPs": round(2 * M * N * K * Z / us / 1e6, 1)}))
 
 # cuBLAS (torch.matmul) on the two plain shapes, for reference
+if a.no_cublas:
+    raise SystemExit(0)
 for name, (A, Bm) in {"cublas Q=Y.Wq": (Y, WqT), "cublas out=V.Wo": (V, WoT)}.items():
     us = graph_time(lambda: torch.matmul(A, Bm.t()), a.reps)
     print(json.dumps({"gemm": name, "us": round(us, 2)}))
