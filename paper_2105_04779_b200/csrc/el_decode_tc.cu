@@ -129,8 +129,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
-__device__ __forceinline__ int tiles_of(const int* npi, int b, int n_stride) {
-    const int n_b = npi ? npi[b] : n_stride;
+// b is a VIRTUAL input: inputs with more than 64 query rows (beam > 4 at 16 heads) are
+// processed as rows/64 virtual inputs of 64 rows each that share H_{b / vchunks}.
+__device__ __forceinline__ int tiles_of(const int* npi, int b, int n_stride, int vchunks) {
+    const int n_b = npi ? npi[b / vchunks] : n_stride;
     return (n_b >= 1 && n_b <= n_stride) ? (n_b + kNT - 1) / kNT : 0;
 }
 
@@ -146,14 +148,15 @@ struct SplitArgs {
     int T;           // tiles per input (uniform mode), 0 = ragged / strided whole inputs
     int W;           // tiles per cluster chunk (uniform mode)
     float* part;     // partial records [2 * ncl slots][2 ranks][kPartFloats]
+    int vchunks;     // virtual inputs per real input (query rows / 64 when rows > 64)
 };
 struct Sched {
-    int T, W, B, ncl, n_stride;
+    int T, W, B, ncl, n_stride, vchunks;
     const int* npi;
     int g, g_end, b;
     bool first;
     __device__ Sched(const SplitArgs& sa, int cl, int ncl_, int B_, int n_stride_, const int* npi_)
-        : T(sa.T), W(sa.W), B(B_), ncl(ncl_), n_stride(n_stride_), npi(npi_), first(true) {
+        : T(sa.T), W(sa.W), B(B_), ncl(ncl_), n_stride(n_stride_), vchunks(sa.vchunks), npi(npi_), first(true) {
         if (T > 0) {
             g = cl * W;
             g_end = min(B * T, g + W);
@@ -177,7 +180,7 @@ struct Sched {
             return true;
         }
         for (; b < B; b += ncl) {
-            Tb = tiles_of(npi, b, n_stride);
+            Tb = tiles_of(npi, b, n_stride, vchunks);
             if (Tb == 0) continue;
             bb = b;
             j0 = 0;
@@ -298,7 +301,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const int j = j0 + jj, Gt = G + jj;
                     if (tune.l2_ahead > 0 && j + tune.l2_ahead < Tb)
                         for (int c = 0; c < 2 * UNITS; ++c)
-                            ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, b);
+                            ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, b / sa.vchunks);
                     for (int u = 0; u < UNITS; ++u) {
                         const int g = Gt * UNITS + u, s = g % kRing;
                         if (u == 0) ELA_TRACE(0, Gt);
@@ -307,9 +310,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         uint8_t* dst = ring + s * kUnitBytes;
                         ptx::mbar_arrive_expect_tx(&unit_full[s], kUnitBytes);
                         const int col = dm_off + 128 * u;
-                        ptx::tma_load_3d(dst, &tm_h, &unit_full[s], col, j * kNT, b, ptx::kEvictFirst);
-                        ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, b,
-                                         ptx::kEvictFirst);
+                        // sibling virtual inputs (same H_b, running on neighbouring clusters)
+                        // re-read the tile from L2: keep it there
+                        const uint64_t pol = sa.vchunks > 1 ? ptx::kEvictNormal : ptx::kEvictFirst;
+                        ptx::tma_load_3d(dst, &tm_h, &unit_full[s], col, j * kNT, b / sa.vchunks, pol);
+                        ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, b / sa.vchunks,
+                                         pol);
                     }
                     if (jj == 0 && nb >= 0 && nb != b) {
                         // warm L2 with the NEXT segment's q' (this CTA's d_m half) so the
@@ -543,7 +549,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
         while (sc.next(b, j0, j1, Tb, kind)) {
             const int T = j1 - j0;
-            const int n_b = n_per_input ? n_per_input[b] : n_stride;
+            const int n_b = n_per_input ? n_per_input[b / sa.vchunks] : n_stride;
             const bool zero_tail = (n_per_input != nullptr) && (Tb * kNT > n_b);
             float m_a = neg_inf, m_b = neg_inf, l_a = 0.f, l_b = 0.f;  // running max (raw units), sums
             for (int jj = 0; jj < T; ++jj) {
@@ -818,7 +824,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         // inputs whose context length is out of contract: loud NaN rows
         for (int b = cl; b < B; b += ncl) {
-            if (tiles_of(n_per_input, b, n_stride) != 0) continue;
+            if (tiles_of(n_per_input, b, n_stride, sa.vchunks) != 0) continue;
             const int tid = int(threadIdx.x) - 64;
             for (int e = tid; e < rows * dm_half; e += 128)
                 ctx[(int64_t(b) * rows + e / dm_half) * d_m + dm_off + e % dm_half] =
@@ -971,13 +977,19 @@ constexpr int kMinChunkTiles = 8;  // bounds the segments per input (merge cost)
 template <int UNITS>
 void launch_units(const void* qp, const void* H, const int* npi, int B, int rows, int n_stride, int d_m,
                   float scale_log2, void* ctx, cudaStream_t st) {
+    // > 64 query rows per input: rows/64 virtual inputs of 64 rows each (q' and C rows are
+    // contiguous per input, so virtual input v owns rows [64 v, 64 v + 64)); H_b is shared
+    const int vchunks = rows > kRowsQ ? rows / kRowsQ : 1;
+    const int B_h = B;
+    B *= vchunks;
+    rows /= vchunks;
     // q' viewed as [B*rows][d_m]; box 64 rows (rows < 64 pad with the next input's
     // rows or OOB zeros; only the first `rows` outputs are written).
     const uint64_t qdims[2] = {uint64_t(d_m), uint64_t(B) * rows};
     const uint64_t qstr[1] = {uint64_t(d_m) * 2};
     const uint32_t qbox[2] = {64, kRowsQ};
     CUtensorMap tq = make_tmap_bf16(qp, 2, qdims, qstr, qbox);
-    const uint64_t hdims[3] = {uint64_t(d_m), uint64_t(n_stride), uint64_t(B)};
+    const uint64_t hdims[3] = {uint64_t(d_m), uint64_t(n_stride), uint64_t(B_h)};
     const uint64_t hstr[2] = {uint64_t(d_m) * 2, uint64_t(n_stride) * d_m * 2};
     const uint32_t hbox[3] = {64, kNT, 1};
     CUtensorMap th = make_tmap_bf16(H, 3, hdims, hstr, hbox);
@@ -1013,9 +1025,11 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
         }
         sa.T = T;
         sa.W = int(W);
+        sa.vchunks = vchunks;
         clusters = int(ncl);
     } else {
         sa.T = 0;  // whole inputs, strided over the clusters
+        sa.vchunks = vchunks;
         clusters = B < max_cl ? B : max_cl;
     }
     kern<<<dim3(2 * clusters), kThreads, smem, st>>>(tq, th, tc, static_cast<const __nv_bfloat16*>(qp), npi, B, rows,
@@ -1032,13 +1046,17 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
 }  // namespace
 
 bool el_decode_tc_supported(int rows_per_input, int d_m) {
-    return rows_per_input >= 1 && rows_per_input <= kRowsQ && d_m % 256 == 0 && d_m >= 256 && d_m <= 1024;
+    // > 64 rows: as virtual inputs of 64 rows sharing H (multiples of 64 only, so every
+    // virtual input is full and the output boxes never cross an input)
+    const bool rows_ok = (rows_per_input >= 1 && rows_per_input <= kRowsQ) ||
+                         (rows_per_input % kRowsQ == 0 && rows_per_input <= 8 * kRowsQ);
+    return rows_ok && d_m % 256 == 0 && d_m >= 256 && d_m <= 1024;
 }
 
 void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B, int rows_per_input,
                          int n_stride, int d_m, float scale, void* ctx, cudaStream_t st) {
     ELA_REQUIRE(el_decode_tc_supported(rows_per_input, d_m), ELATTN_ERR_UNSUPPORTED,
-                "tcgen05 decode: rows <= 64 and d_m in {256, 512, 768, 1024}");
+                "tcgen05 decode: rows <= 64 or a multiple of 64 (<= 512), d_m in {256, 512, 768, 1024}");
     ELA_REQUIRE((reinterpret_cast<uintptr_t>(qp) & 15) == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(ctx) & 15) == 0,
                 ELATTN_ERR_PARAM, "tcgen05 decode: q', H and C must be 16-byte aligned");

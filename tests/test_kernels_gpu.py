@@ -88,6 +88,7 @@ def decode_ref(qp, H, rows, scale, npi=None):
 @pytest.mark.parametrize("kernel", [1, 0])
 @pytest.mark.parametrize("B,rows,n,d_m", [
     (1, 64, 32, 512), (2, 64, 1024, 1024), (3, 16, 77, 1024), (2, 48, 300, 256), (5, 64, 129, 768),
+    (2, 128, 300, 1024), (3, 192, 1024, 512), (80, 192, 256, 1024),  # beam 8 / 12: virtual inputs
 ])
 def test_decode_vs_torch(kernel, B, rows, n, d_m):
     import torch
@@ -186,3 +187,26 @@ def test_decode_stream_k_schedules(B, rows, n, d_m):
         assert (o - want).abs().max().item() / want.abs().max().item() < 2e-2
     assert torch.equal(outs[0], outs[1])  # deterministic merge order
     assert (outs[0] - outs[2]).abs().max().item() / want.abs().max().item() < 1e-2
+
+
+def test_decode_virtual_inputs_ragged():
+    """rows > 64 (beam 12) with ragged n_per_input: every virtual input takes its real
+    input's context length."""
+    import torch
+
+    L, capi = _testing_lib()
+    B, rows, n, d_m = 3, 192, 200, 1024
+    g = torch.Generator(device="cuda").manual_seed(13)
+    qp = (torch.randn(B * rows, d_m, generator=g, device="cuda") * 0.3).to(torch.bfloat16)
+    H = (torch.rand(B, n, d_m, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    npi = torch.tensor([200, 5, 97], dtype=torch.int32, device="cuda")
+    Hg = H.clone()
+    for b in range(B):
+        Hg[b, int(npi[b]):] = float("nan")
+    ctx = torch.empty(B * rows, d_m, device="cuda", dtype=torch.bfloat16)
+    capi.check(L.elattn_gpu_testing_decode_bf16(qp.data_ptr(), Hg.data_ptr(), npi.data_ptr(), B, rows, n, d_m,
+                                                0.125, ctx.data_ptr(), 1, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = decode_ref(qp, H, rows, 0.125, npi)
+    assert torch.isfinite(ctx.float()).all()
+    assert (ctx.float() - want).abs().max().item() / want.abs().max().item() < 2e-2
