@@ -62,6 +62,7 @@ constexpr int kEpiWarpBytes = 4096;  // per-warp epilogue stage (64 q x 32 d bf1
 // 128 softmax threads' 64 fp32 fragment values (float4-interleaved by thread)
 constexpr int kPartFloatsHdr = 128;
 constexpr int kPartFloatsUnit = 128 * 64;
+constexpr int kQPrefetchTiles = 8;  // next segment's q' is prefetched into L2 this many tiles ahead
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max grows by > 2^8
 
 // Tuning knobs (runtime so they can be swept):
@@ -317,9 +318,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, b / sa.vchunks,
                                          pol);
                     }
-                    if (jj == 0 && nb >= 0 && nb != b) {
-                        // warm L2 with the NEXT segment's q' (this CTA's d_m half) so the
-                        // transition does not wait on HBM latency
+                    if (jj == (T > kQPrefetchTiles ? T - kQPrefetchTiles : 0) && nb >= 0 && nb != b) {
+                        // warm L2 with the NEXT segment's q' (this CTA's d_m half) a few tiles
+                        // before the transition (earlier, the streaming H evicts it again)
                         for (int c = 0; c < 2 * UNITS; ++c) ptx::tma_prefetch_2d(&tm_q, dm_off + 64 * c, nb * rows);
                     }
                     if (jj == 0 && L::kQSmemUnits > 0) {
