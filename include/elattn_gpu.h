@@ -169,6 +169,24 @@ int elattn_gpu_decoder_destroy(elattn_gpu_decoder_t dec);
 /* our own kernels launched by one run (the graph's kernel nodes outside cuBLASLt) */
 int64_t elattn_gpu_decoder_kernels_per_run(elattn_gpu_decoder_t dec);
 
+/*
+ * Per-lane hidden-state caches for decoder-only EL self-attention (BASELINE config 4, the
+ * "hidden-state-only cache").  A cache is caller-owned device
+ * memory [lanes][n_max][d_m] (dtype) plus a device int[lanes] of lengths; attention over
+ * it is elattn_gpu_el_attention_step(params, Y, cache, lengths, lanes, 1, n_max, ...).
+ *   append: cache[l][len[l]] = Y[l], ++len[l]   (a full lane's length becomes n_max + 1,
+ *           i.e. NaN rows on the next step — loud, like an out-of-range n_per_input)
+ *   gather: DecoderState::gather_lanes (model.hpp:291-306) on the device: dst lane i =
+ *           copy of src lane parent[i] (rows 0..len-1); parents may repeat; an out-of-range
+ *           parent gives the lane length n_max + 1 (loud).  rows_hint = expected length
+ *           (sizes the grid only).  src and dst must not overlap.
+ */
+int elattn_gpu_cache_append(void* cache, const void* Y, int* lengths, int lanes, int n_max, int d_m, int dtype,
+                            elattn_stream_t stream);
+int elattn_gpu_cache_gather(const void* src, const int* src_lengths, void* dst, int* dst_lengths,
+                            const int* parent, int lanes_in, int lanes_out, int n_max, int d_m, int dtype,
+                            int rows_hint, elattn_stream_t stream);
+
 /* Device-kernel launches issued by this thread since the last reset (for bench
  * accounting of gpu_launches). */
 int64_t elattn_gpu_launch_count(void);

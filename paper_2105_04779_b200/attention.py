@@ -28,6 +28,7 @@ from .capi import DTYPE_BF16, DTYPE_F32, ParamError, ShapeError, StateError
 
 __all__ = [
     "DecoderStep",
+    "HiddenStateCache",
     "Rng", "seeded_uniform", "AttentionParams", "ElQuery", "DeviceParams", "ElAttentionLayer",
     "build_el_query", "fold_el_queries", "el_attention", "el_attention_folded",
     "DTYPE_F32", "DTYPE_BF16",
@@ -343,6 +344,57 @@ class DecoderStep:
             except Exception:
                 pass
             self.handle = None
+
+
+class HiddenStateCache:
+    """Per-lane hidden-state caches for decoder-only EL self-attention (BASELINE config 4,
+    the "hidden-state-only cache": each lane attends over its own history of layer inputs,
+    no per-head K/V).  Layer l keeps ``cache[l]`` [lanes, n_max, d_m] and device lengths
+    ``lengths[l]`` [lanes]; ``attend`` is the batched EL step with x = 1 over it.
+    ``gather(parent)`` is DecoderState::gather_lanes (model.hpp:291-306) on the device.
+    """
+
+    def __init__(self, layers: int, lanes: int, n_max: int, d_m: int, dtype: int = DTYPE_BF16):
+        torch = _torch()
+        self.dtype, self.lanes, self.n_max, self.d_m = dtype, lanes, n_max, d_m
+        self.cache = torch.zeros(layers, lanes, n_max, d_m, dtype=_tdtype(dtype), device="cuda")
+        self.lengths = torch.zeros(layers, lanes, dtype=torch.int32, device="cuda")
+        self._spare = None
+
+    def append(self, layer: int, Y, stream=None):
+        """cache[layer][l][len] = Y[l]; ++len (device side)."""
+        torch = _torch()
+        if tuple(Y.shape) != (self.lanes, self.d_m) or Y.dtype != _tdtype(self.dtype):
+            raise ShapeError("HiddenStateCache.append: Y must be [lanes, d_m] of the cache dtype")
+        Y = Y.contiguous()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        capi.check(capi.lib().elattn_gpu_cache_append(self.cache[layer].data_ptr(), Y.data_ptr(),
+                                                      self.lengths[layer].data_ptr(), self.lanes, self.n_max,
+                                                      self.d_m, self.dtype, _stream_ptr(st)))
+
+    def attend(self, layer_params: ElAttentionLayer, layer: int, Y, out=None, stream=None):
+        """EL self-attention of every lane's query row over its own cache."""
+        return layer_params.step(Y, self.cache[layer], self.lengths[layer], out=out, stream=stream)
+
+    def gather(self, parent, rows_hint: Optional[int] = None, stream=None):
+        """New lane i = old lane parent[i] in every layer (beam reorder / expansion with the
+        same lane count)."""
+        torch = _torch()
+        parent = torch.as_tensor(parent, dtype=torch.int32).cuda().contiguous()
+        if parent.numel() != self.lanes:
+            raise ShapeError("HiddenStateCache.gather: one parent per lane")
+        if self._spare is None:
+            self._spare = (torch.empty_like(self.cache), torch.empty_like(self.lengths))
+        dst, dlen = self._spare
+        st = stream if stream is not None else torch.cuda.current_stream()
+        hint = rows_hint if rows_hint is not None else self.n_max
+        for l in range(self.cache.shape[0]):
+            capi.check(capi.lib().elattn_gpu_cache_gather(
+                self.cache[l].data_ptr(), self.lengths[l].data_ptr(), dst[l].data_ptr(), dlen[l].data_ptr(),
+                parent.data_ptr(), self.lanes, self.lanes, self.n_max, self.d_m, self.dtype, hint,
+                _stream_ptr(st)))
+        self._spare = (self.cache, self.lengths)
+        self.cache, self.lengths = dst, dlen
 
 
 # ---------------------------------------------------------------------------

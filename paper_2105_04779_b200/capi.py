@@ -34,6 +34,8 @@ EXPORTED_SYMBOLS = (
     "elattn_gpu_decoder_run",
     "elattn_gpu_decoder_destroy",
     "elattn_gpu_decoder_kernels_per_run",
+    "elattn_gpu_cache_append",
+    "elattn_gpu_cache_gather",
     "elattn_gpu_reset_launch_count",
 )
 
@@ -105,6 +107,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.elattn_gpu_decoder_destroy.argtypes = [vp]
     lib.elattn_gpu_decoder_kernels_per_run.argtypes = [vp]
     lib.elattn_gpu_decoder_kernels_per_run.restype = i64
+    lib.elattn_gpu_cache_append.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
+    lib.elattn_gpu_cache_gather.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(lib, name)
         if fn.restype is ctypes.c_int and name not in ("elattn_gpu_decode_kernel_kind",):

@@ -543,3 +543,28 @@ extern "C" int elattn_gpu_decoder_destroy(elattn_gpu_decoder_t dec) {
 }
 
 extern "C" int64_t elattn_gpu_decoder_kernels_per_run(elattn_gpu_decoder_t dec) { return dec ? dec->kernels : -1; }
+
+// ---------------------------------------------------------------- per-lane hidden-state caches
+extern "C" int elattn_gpu_cache_append(void* cache, const void* Y, int* lengths, int lanes, int n_max, int d_m,
+                                       int dtype, elattn_stream_t stream) {
+    return guarded([&] {
+        ELA_REQUIRE(cache && Y && lengths, ELATTN_ERR_PARAM, "cache_append: null buffer");
+        ELA_REQUIRE(lanes >= 1 && n_max >= 1 && d_m >= 1, ELATTN_ERR_SHAPE, "cache_append: bad shape");
+        ELA_REQUIRE(dtype == ELATTN_DTYPE_F32 || dtype == ELATTN_DTYPE_BF16, ELATTN_ERR_PARAM, "unknown dtype");
+        launch_cache_append(cache, Y, lengths, lanes, n_max, d_m, dtype, reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
+extern "C" int elattn_gpu_cache_gather(const void* src, const int* src_lengths, void* dst, int* dst_lengths,
+                                       const int* parent, int lanes_in, int lanes_out, int n_max, int d_m, int dtype,
+                                       int rows_hint, elattn_stream_t stream) {
+    return guarded([&] {
+        ELA_REQUIRE(src && src_lengths && dst && dst_lengths && parent, ELATTN_ERR_PARAM, "cache_gather: null buffer");
+        ELA_REQUIRE(src != dst, ELATTN_ERR_PARAM, "cache_gather: src and dst must differ");
+        ELA_REQUIRE(lanes_out >= 1, ELATTN_ERR_STATE, "gather_lanes: all lanes dropped");
+        ELA_REQUIRE(lanes_in >= 1 && n_max >= 1 && d_m >= 1, ELATTN_ERR_SHAPE, "cache_gather: bad shape");
+        ELA_REQUIRE(dtype == ELATTN_DTYPE_F32 || dtype == ELATTN_DTYPE_BF16, ELATTN_ERR_PARAM, "unknown dtype");
+        launch_cache_gather(src, src_lengths, dst, dst_lengths, parent, lanes_in, lanes_out, n_max, d_m, dtype,
+                            rows_hint, reinterpret_cast<cudaStream_t>(stream));
+    });
+}

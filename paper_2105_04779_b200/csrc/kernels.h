@@ -1,6 +1,8 @@
 // kernels.h — host-side launchers for every device kernel in the library.
 #pragma once
 
+#include <algorithm>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -46,6 +48,13 @@ void launch_tc_gemm(const GemmArgs& g, cudaStream_t st);
 // the output type, so the bf16 path stores b_Q and b_O in bf16 (GemmArgs::bias16).
 bool lt_gemm_supported(const GemmArgs& g);
 void launch_lt_gemm(const GemmArgs& g, cudaStream_t st);
+
+// Per-lane hidden-state caches (lane_cache.cu).
+void launch_cache_append(void* cache, const void* Y, int* len, int lanes, int n_max, int d_m, int dtype,
+                         cudaStream_t st);
+void launch_cache_gather(const void* src, const int* src_len, void* dst, int* dst_len, const int* parent,
+                         int lanes_in, int lanes_out, int n_max, int d_m, int dtype, int rows_hint,
+                         cudaStream_t st);
 
 // Testing hook: when non-null, the tcgen05 decode writes clock64 stamps of its
 // first cluster: trace[(cta*24 + event)*64 + tile].

@@ -241,3 +241,56 @@ def test_decoder_step_graph_matches_layer_chain(gpu, npi_mode):
     for l in range(2):
         y = round_to_dtype(O.el_layer_step(pr[l], y, Hh, c["x"], nl), E.DTYPE_BF16)
     assert rel_err(out, y) <= TOL[1]
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_hidden_state_cache_self_attention(gpu, dtype):
+    """Decoder-only EL self-attention over per-lane hidden-state caches (config 4 form):
+    append the lane's input, attend over its history (x = 1, ragged lengths), reorder
+    lanes with gather — against the oracle's el_layer_step per lane."""
+    import torch
+
+    E = gpu
+    c = dict(BART_CFG) if dtype == 1 else dict(ORACLE_CFG)
+    lanes, n_max, steps = 6, 40, 5
+    p = O.params_random(c["h"], c["d_m"], c["d_k"], O.OracleRng(77))
+    layer = E.ElAttentionLayer(to_prod(p), dtype)
+    cache = E.HiddenStateCache(1, lanes, n_max, c["d_m"], dtype)
+    td = torch.bfloat16 if dtype == 1 else torch.float32
+    rng = O.OracleRng(78)
+    pr = round_params(p, dtype)
+    from paper_2105_04779_b200.attention import round_to_dtype
+
+    hist = [[] for _ in range(lanes)]  # host mirror of each lane's history
+    # prefix of different lengths per lane
+    for l in range(lanes):
+        for _ in range(1 + l):
+            y = round_to_dtype(rng.uniform((1, c["d_m"])), dtype)
+            hist[l].append(y[0])
+    maxlen = max(len(hh) for hh in hist)
+    for t in range(maxlen):  # ingest lane by lane at its own pace
+        Yt = np.zeros((lanes, c["d_m"]))
+        for l in range(lanes):
+            if t < len(hist[l]):
+                Yt[l] = hist[l][t]
+        Ydev = torch.from_numpy(Yt).to("cuda", td)
+        # lanes that are done get appended garbage we then truncate by resetting lengths
+        cache.append(0, Ydev)
+    cache.lengths[0] = torch.tensor([len(hh) for hh in hist], dtype=torch.int32, device="cuda")
+    for step in range(steps):
+        Y = round_to_dtype(rng.uniform((lanes, c["d_m"])), dtype)
+        cache.append(0, torch.from_numpy(Y).to("cuda", td))
+        for l in range(lanes):
+            hist[l].append(Y[l])
+        out = cache.attend(layer, 0, torch.from_numpy(Y).to("cuda", td)).double().cpu().numpy()
+        for l in range(lanes):
+            Hl = np.stack(hist[l])[None]
+            want = O.el_layer_step(pr, Y[l:l + 1], Hl, 1)
+            assert rel_err(out[l:l + 1], want) <= TOL[dtype], (step, l)
+        parent = [(l * 5 + step) % lanes for l in range(lanes)]  # reorder (parents repeat)
+        cache.gather(parent, rows_hint=n_max)
+        hist = [list(hist[q]) for q in parent]
+        assert cache.lengths[0].cpu().tolist() == [len(hh) for hh in hist]
+        got = cache.cache[0].double().cpu().numpy()
+        for l in range(lanes):
+            assert np.array_equal(got[l, :len(hist[l])], np.stack(hist[l]))
