@@ -66,7 +66,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN>
+template <int BN, bool BIAS, bool SCALE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmParams p) {
@@ -202,18 +202,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::bulk_wait_group_read<S::kOutStages - 1>();  // this stage's previous store has read it
             }
             __syncwarp();
-            const float* bias = p.bias ? p.bias + z * p.sbz : nullptr;
+            // bias of this warp's columns: lane l holds column c0 + l of each 32-column
+            // chunk, broadcast with shuffles (no per-element loads)
+            float bcol[kHalf / 32];
+            if constexpr (BIAS) {
+#pragma unroll
+                for (int c = 0; c < kHalf / 32; ++c) {
+                    const int n = n0 + int(ch) * kHalf + 32 * c + int(lane);
+                    bcol[c] = n < p.N ? __ldg(p.bias + z * p.sbz + n) : 0.f;
+                }
+            }
 #pragma unroll
             for (int c0 = 0; c0 < kHalf; c0 += 32) {
                 const uint32_t* r = rr + c0;
                 uint32_t packed[16];
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {
-                    float v0 = __uint_as_float(r[j]) * p.alpha, v1 = __uint_as_float(r[j + 1]) * p.alpha;
-                    if (bias) {
-                        const int n = n0 + int(ch) * kHalf + c0 + j;
-                        v0 += (n < p.N) ? __ldg(bias + n) : 0.f;
-                        v1 += (n + 1 < p.N) ? __ldg(bias + n + 1) : 0.f;
+                    float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
+                    if constexpr (SCALE) v0 *= p.alpha, v1 *= p.alpha;
+                    if constexpr (BIAS) {
+                        v0 += __shfl_sync(0xffffffffu, bcol[c0 / 32], j);
+                        v1 += __shfl_sync(0xffffffffu, bcol[c0 / 32], j + 1);
                     }
                     packed[j / 2] = pack2(v0, v1);
                 }
@@ -286,7 +295,7 @@ int num_sms() {
     return n;
 }
 
-template <int BN>
+template <int BN, bool BIAS, bool SCALE>
 void launch_bn(const GemmArgs& g, cudaStream_t st) {
     GemmParams p{};
     p.M = g.M, p.N = g.N, p.K = g.K, p.Z = g.Z, p.alpha = g.alpha, p.bias = g.bias, p.sbz = g.sbz;
@@ -297,7 +306,7 @@ void launch_bn(const GemmArgs& g, cudaStream_t st) {
     // output C[z][m][n]: boxes of 32 rows x kBoxCols columns (one epilogue warp's piece),
     // clipped at M / N
     CUtensorMap tc = operand_map(g.C, g.ldc, g.sCz, g.M, g.N, g.Z, 32, &p.c_zm, GemmSmem<BN>::kBoxCols);
-    auto kern = tc_gemm_kernel<BN>;
+    auto kern = tc_gemm_kernel<BN, BIAS, SCALE>;
     constexpr uint32_t smem = GemmSmem<BN>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const int tiles = p.Z * p.tiles_m * p.tiles_n;
@@ -316,11 +325,20 @@ bool tc_gemm_supported(const GemmArgs& g) {
            aligned16(g.B) && aligned16(g.C);
 }
 
+template <int BN>
+void launch_variant(const GemmArgs& g, cudaStream_t st) {
+    const bool bias = g.bias != nullptr, scale = g.alpha != 1.f;
+    if (bias && scale) return launch_bn<BN, true, true>(g, st);
+    if (bias) return launch_bn<BN, true, false>(g, st);
+    if (scale) return launch_bn<BN, false, true>(g, st);
+    return launch_bn<BN, false, false>(g, st);
+}
+
 void launch_tc_gemm(const GemmArgs& g, cudaStream_t st) {
     if (g.N <= 64)
-        launch_bn<64>(g, st);
+        launch_variant<64>(g, st);
     else
-        launch_bn<128>(g, st);
+        launch_variant<128>(g, st);
 }
 
 }  // namespace elattn_gpu
