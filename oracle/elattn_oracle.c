@@ -26,6 +26,9 @@
  *   orc_el_attention_folded    attention.hpp:262-290
  *   orc_fold_el_queries        attention.hpp:293-304
  *   orc_multi_head_attention   attention.hpp:96-113
+ *   orc_kv_append              attention.hpp:134-150 (KvCache::append)
+ *   orc_mixed_self_attention   attention.hpp:309-365 (decoder-only: EL over the shared
+ *                              prefix + MHA over the generated-token cache, joint softmax)
  *   orc_el_layer_step          build_el_query x g + fold + el_attention_folded per
  *                              input (the batched cross-attention step the GPU
  *                              path computes; SURVEY.md §8 math contract)
@@ -377,5 +380,108 @@ int orc_el_layer_step(const orc_params* p, const double* Y, const double* H, con
 done:
     free(q);
     free(s);
+    return rc;
+}
+
+
+/* KvCache::append (attention.hpp:134-150): project one hidden row through every head's
+ * key/value weights (+ biases when enabled) and store it at position t of caches
+ * K, V laid out [h][t_max][d_k]. */
+int orc_kv_append(const orc_params* p, const double* y, double* K, double* V, int64_t t_max, int64_t t) {
+    int rc = validate(p);
+    if (rc) return rc;
+    if (t < 0 || t >= t_max) return ORC_STATE;
+    const int d_m = p->d_m, d_k = p->d_k, h = p->h;
+    double *k = NULL, *v = NULL;
+    ALLOC(k, d_k);
+    ALLOC(v, d_k);
+    for (int i = 0; i < h; ++i) {
+        const int64_t wo = (int64_t)i * d_m * d_k;
+        TRY(mm(y, d_m, p->Wk + wo, d_k, 1, 1, d_m, d_k, k, d_k));
+        if (p->include_key_bias)
+            for (int c = 0; c < d_k; ++c) k[c] = k[c] + p->bk[(int64_t)i * d_k + c];
+        TRY(mm(y, d_m, p->Wv + wo, d_k, 1, 1, d_m, d_k, v, d_k));
+        if (p->include_value_bias)
+            for (int c = 0; c < d_k; ++c) v[c] = v[c] + p->bv[(int64_t)i * d_k + c];
+        for (int c = 0; c < d_k; ++c) {
+            K[((int64_t)i * t_max + t) * d_k + c] = k[c];
+            V[((int64_t)i * t_max + t) * d_k + c] = v[c];
+        }
+    }
+done:
+    free(k);
+    free(v);
+    return rc;
+}
+
+/* mixed_self_attention (attention.hpp:309-365): q [1 x d_m], prefix Hp [t_in x d_m],
+ * generated-token cache K, V [h][t_max][d_k] with t_out valid rows -> out [1 x d_m].
+ * Per head: EL scores over the prefix (+ s_i) and Q_i . K_r over the cache, one joint
+ * softmax; the prefix part goes through Wv_i Wo_i with the value bias scaled by the
+ * prefix probability mass, the cached part (values already biased) through Wo_i. */
+int orc_mixed_self_attention(const orc_params* p, const double* q, const double* Hp, int64_t t_in,
+                             const double* K, const double* V, int64_t t_max, int64_t t_out, double* out) {
+    int rc = validate(p);
+    if (rc) return rc;
+    if (t_in < 1) return ORC_STATE;
+    const int d_m = p->d_m, d_k = p->d_k, h = p->h;
+    const int64_t n = t_in + t_out;
+    double *elq = NULL, *s = NULL, *Qi = NULL, *scores = NULL, *ctx = NULL, *cv = NULL, *head = NULL,
+           *tmp = NULL, *b = NULL, *co = NULL;
+    ALLOC(elq, (int64_t)h * d_m);
+    ALLOC(s, h);
+    ALLOC(Qi, d_k);
+    ALLOC(scores, n);
+    ALLOC(ctx, d_m);
+    ALLOC(cv, d_k);
+    ALLOC(head, d_m);
+    ALLOC(tmp, d_m);
+    ALLOC(b, d_k);
+    ALLOC(co, d_k);
+    TRY(orc_build_el_query(p, q, elq, s));
+    for (int j = 0; j < d_m; ++j) out[j] = 0.0;
+    for (int i = 0; i < h; ++i) {
+        const int64_t wo = (int64_t)i * d_m * d_k;
+        TRY(mm(q, d_m, p->Wq + wo, d_k, 1, 1, d_m, d_k, Qi, d_k)); /* Qi = q Wq_i + bq_i */
+        for (int c = 0; c < d_k; ++c) Qi[c] = Qi[c] + p->bq[(int64_t)i * d_k + c];
+        TRY(mm(elq + (int64_t)i * d_m, d_m, Hp, 1, d_m, 1, d_m, t_in, scores, t_in)); /* prefix scores */
+        for (int64_t j = 0; j < t_in; ++j) scores[j] = scores[j] + s[i];
+        for (int64_t r = 0; r < t_out; ++r) { /* generated-token scores */
+            double sc = 0.0;
+            for (int c = 0; c < d_k; ++c) sc += Qi[c] * K[((int64_t)i * t_max + r) * d_k + c];
+            scores[t_in + r] = sc;
+        }
+        TRY(softmax_rows(scores, 1, n, d_k));
+        double mass = 0.0;
+        for (int64_t j = 0; j < t_in; ++j) mass += scores[j];
+        TRY(mm(scores, t_in, Hp, d_m, 1, 1, t_in, d_m, ctx, d_m)); /* probs_in . Hp */
+        TRY(mm(ctx, d_m, p->Wv + wo, d_k, 1, 1, d_m, d_k, cv, d_k));
+        TRY(mm(cv, d_k, p->Wo + (int64_t)i * d_k * d_m, d_m, 1, 1, d_k, d_m, head, d_m));
+        if (p->include_value_bias) {
+            for (int c = 0; c < d_k; ++c) b[c] = p->bv[(int64_t)i * d_k + c] * mass;
+            TRY(mm(b, d_k, p->Wo + (int64_t)i * d_k * d_m, d_m, 1, 1, d_k, d_m, tmp, d_m));
+            for (int j = 0; j < d_m; ++j) head[j] = head[j] + tmp[j];
+        }
+        if (t_out > 0) {
+            for (int c = 0; c < d_k; ++c) co[c] = 0.0;
+            for (int64_t r = 0; r < t_out; ++r)
+                for (int c = 0; c < d_k; ++c) co[c] += scores[t_in + r] * V[((int64_t)i * t_max + r) * d_k + c];
+            TRY(mm(co, d_k, p->Wo + (int64_t)i * d_k * d_m, d_m, 1, 1, d_k, d_m, tmp, d_m));
+            for (int j = 0; j < d_m; ++j) head[j] = head[j] + tmp[j];
+        }
+        for (int j = 0; j < d_m; ++j) out[j] = out[j] + head[j];
+    }
+    for (int j = 0; j < d_m; ++j) out[j] = out[j] + p->bo[j];
+done:
+    free(elq);
+    free(s);
+    free(Qi);
+    free(scores);
+    free(ctx);
+    free(cv);
+    free(head);
+    free(tmp);
+    free(b);
+    free(co);
     return rc;
 }

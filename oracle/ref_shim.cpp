@@ -13,6 +13,8 @@
 //   el_attention               attention.hpp:239-257
 //   el_attention_folded        attention.hpp:262-290
 //   multi_head_attention       attention.hpp:96-113
+//   KvCache::append            attention.hpp:134-150
+//   mixed_self_attention       attention.hpp:309-365
 //   Rng / seeded_uniform       tensor.hpp:133-150, 236-241
 //   PrecisionGuard             tensor.hpp:25-29
 #include <cstdint>
@@ -221,6 +223,41 @@ int ref_layer_step(void* layer, const double* Y, const double* H, const int* n_p
             return rc[t];
         }
     return 0;
+}
+
+// KvCache built by the reference's own append from t hidden rows; K, V exported as
+// [h][t_max][d_k] (rows t..t_max-1 untouched).
+int ref_kv_build(REF_PARAMS_ARGS, const double* rows, int64_t t, int64_t t_max, double* K, double* V) {
+    try {
+        AttentionParams p = REF_PARAMS;
+        KvCache c(h, d_k);
+        for (int64_t r = 0; r < t; ++r) c.append(from_flat({1, d_m}, rows + r * d_m), p);
+        for (int i = 0; i < h; ++i)
+            for (int64_t r = 0; r < t; ++r)
+                for (int j = 0; j < d_k; ++j) {
+                    K[(int64_t(i) * t_max + r) * d_k + j] = c.K[size_t(i)][size_t(r * d_k + j)];
+                    V[(int64_t(i) * t_max + r) * d_k + j] = c.V[size_t(i)][size_t(r * d_k + j)];
+                }
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// mixed_self_attention with the generated-token cache built from t_out hidden rows by
+// the reference's KvCache::append.
+int ref_mixed_self_attention(REF_PARAMS_ARGS, const double* q, const double* Hp, int64_t t_in,
+                             const double* gen_rows, int64_t t_out, double* out) {
+    try {
+        AttentionParams p = REF_PARAMS;
+        KvCache c(h, d_k);
+        for (int64_t r = 0; r < t_out; ++r) c.append(from_flat({1, d_m}, gen_rows + r * d_m), p);
+        Tensor o = mixed_self_attention(from_flat({1, d_m}, q), from_flat({t_in, d_m}, Hp), c, p);
+        to_flat(o, out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
 }
 
 }  // extern "C"

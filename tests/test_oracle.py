@@ -146,3 +146,33 @@ def test_port_equals_reference_random():
         b = O.el_layer_step(p, Y, H, x, npi, impl="reference", nthreads=2)
         assert np.array_equal(a, b)
         assert rel_err(a, b) == 0.0
+
+
+@pytest.mark.parametrize("kb,vb,t_out", [(1, 1, 3), (1, 1, 0), (0, 1, 2), (1, 0, 4), (0, 0, 1)])
+def test_mixed_self_attention_and_kv_cache_match_reference(kb, vb, t_out):
+    """Decoder-only path: KvCache::append (attention.hpp:134-150) and mixed_self_attention
+    (:309-365) restated in the oracle == the reference's own functions, bit for bit."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built (reference headers absent)")
+    rng = O.OracleRng(900 + 10 * kb + vb + t_out)
+    p = O.params_random(4, 16, 4, rng)
+    p.include_key_bias, p.include_value_bias = bool(kb), bool(vb)
+    q = rng.uniform((1, 16))
+    Hp = rng.uniform((5, 16))
+    gen = rng.uniform((t_out, 16))
+    K, V = O.kv_build(p, gen, t_max=max(t_out, 1))
+    Kr, Vr = O.kv_build(p, gen, t_max=max(t_out, 1), impl="reference")
+    assert np.array_equal(K, Kr) and np.array_equal(V, Vr)
+    out = O.mixed_self_attention(p, q, Hp, gen)
+    ref = O.mixed_self_attention(p, q, Hp, gen, impl="reference")
+    assert np.array_equal(out, ref)
+
+
+def test_mixed_self_attention_reduces_to_el_attention_without_cache():
+    """t_out = 0: the joint softmax is the prefix softmax, so mixed == el_attention."""
+    rng = O.OracleRng(950)
+    p = O.params_random(2, 8, 4, rng)
+    q, Hp = rng.uniform((1, 8)), rng.uniform((6, 8))
+    a = O.mixed_self_attention(p, q, Hp, np.zeros((0, 8)))
+    b = O.el_attention(p, q, Hp)
+    assert np.max(np.abs(a - b)) <= 1e-12
