@@ -187,6 +187,26 @@ int elattn_gpu_cache_gather(const void* src, const int* src_lengths, void* dst, 
                             const int* parent, int lanes_in, int lanes_out, int n_max, int d_m, int dtype,
                             int rows_hint, elattn_stream_t stream);
 
+/*
+ * Decoder-only MIXED self-attention.  Replaces
+ * mixed_self_attention(q, prefix_hidden, gen_cache, p) (attention.hpp:309-365) and
+ * KvCache::append (:134-150) for B inputs x x lanes:
+ *   kv_append: K_i = Y.Wk_i (+ bk_i), V_i = Y.Wv_i (+ bv_i) of every lane's row at position
+ *              t of the generated-token caches Kc, Vc [R][h][t_max][d_k] (dtype), R = B*x.
+ *   mixed:     EL scores over the prefix P [B][n][d_m] (shared by an input's x lanes,
+ *              n_per_input ragged) and multi-head scores over each lane's t_out cached
+ *              rows, one joint softmax, value bias split by the prefix mass; out [R][d_m].
+ *              As in the reference's incremental step (model.hpp:365-367) the caller
+ *              appends the current row first.  Workspace: elattn_gpu_mixed_workspace_size.
+ * Errors: SHAPE, STATE (empty prefix, t_out > t_max, append past t_max), PARAM.
+ */
+int elattn_gpu_kv_append(elattn_gpu_params_t params, const void* Y, int R, void* Kc, void* Vc, int t_max, int t,
+                         elattn_stream_t stream);
+int elattn_gpu_mixed_self_attention(elattn_gpu_params_t params, const void* Y, const void* P, const int* n_per_input,
+                                    int B, int x, int n, const void* Kc, const void* Vc, int t_max, int t_out,
+                                    void* out, void* workspace, size_t workspace_bytes, elattn_stream_t stream);
+size_t elattn_gpu_mixed_workspace_size(elattn_gpu_params_t params, int B, int x);
+
 /* Device-kernel launches issued by this thread since the last reset (for bench
  * accounting of gpu_launches). */
 int64_t elattn_gpu_launch_count(void);

@@ -28,6 +28,9 @@ from .capi import DTYPE_BF16, DTYPE_F32, ParamError, ShapeError, StateError
 
 __all__ = [
     "DecoderStep",
+    "KvCache",
+    "mixed_self_attention",
+    "mixed_self_attention_batched",
     "HiddenStateCache",
     "Rng", "seeded_uniform", "AttentionParams", "ElQuery", "DeviceParams", "ElAttentionLayer",
     "build_el_query", "fold_el_queries", "el_attention", "el_attention_folded",
@@ -397,6 +400,47 @@ class HiddenStateCache:
         self.cache, self.lengths = dst, dlen
 
 
+class KvCache:
+    """Generated-token K/V cache of the decoder-only mixed self-attention — the reference's
+    ``KvCache`` (attention.hpp:118-150) for R lanes on the device: K, V [R, h, t_max, d_k]."""
+
+    def __init__(self, layer: "ElAttentionLayer", R: int, t_max: int):
+        torch = _torch()
+        self.layer, self.R, self.t_max, self.t = layer, R, t_max, 0
+        d = layer.dev
+        self.K = torch.zeros(R, d.h, t_max, d.d_k, dtype=_tdtype(layer.dtype), device="cuda")
+        self.V = torch.zeros_like(self.K)
+
+    def append(self, Y, stream=None):
+        """KvCache::append for every lane's row of Y [R, d_m] (projection through Wk_i, Wv_i
+        + biases, written at position t)."""
+        if self.t >= self.t_max:
+            raise StateError("KvCache: full")
+        self.layer._check(Y, (self.R, self.layer.dev.d_m), "Y")
+        capi.check(capi.lib().elattn_gpu_kv_append(self.layer.dev.handle, Y.data_ptr(), self.R, self.K.data_ptr(),
+                                                   self.V.data_ptr(), self.t_max, self.t, _stream_ptr(stream)))
+        self.t += 1
+
+
+def mixed_self_attention_batched(layer: "ElAttentionLayer", Y, P, cache: KvCache, x: int, n_per_input=None,
+                                 out=None, stream=None):
+    """Batched ``mixed_self_attention`` (attention.hpp:309-365): lanes Y [B*x, d_m], prefix
+    hidden states P [B, n, d_m] shared by an input's x lanes, generated caches ``cache``."""
+    torch = _torch()
+    B, n, d_m = P.shape
+    layer._check(Y, (B * x, d_m), "Y")
+    layer._check(P, None, "prefix")
+    if out is None:
+        out = torch.empty_like(Y)
+    need = capi.lib().elattn_gpu_mixed_workspace_size(layer.dev.handle, B, x)
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+    npi = n_per_input.data_ptr() if n_per_input is not None else None
+    capi.check(capi.lib().elattn_gpu_mixed_self_attention(
+        layer.dev.handle, Y.data_ptr(), P.data_ptr(), npi, B, x, n, cache.K.data_ptr(), cache.V.data_ptr(),
+        cache.t_max, cache.t, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+    return out
+
+
 # ---------------------------------------------------------------------------
 # Reference-shaped host API (fp64 numpy in / out), the drop-in for attention.hpp.
 # ---------------------------------------------------------------------------
@@ -472,4 +516,24 @@ def el_attention(q: np.ndarray, H: np.ndarray, p: AttentionParams | DeviceParams
         raise ShapeError("el_attention: q/H width must equal d_m")
     layer = _layer(p, dtype)
     out = layer.step(_as_device(q, layer.dtype), _as_device(H[None], layer.dtype))
+    return _to_host(out)
+
+
+def mixed_self_attention(q: np.ndarray, prefix_hidden: np.ndarray, gen_rows: np.ndarray,
+                         p: AttentionParams | DeviceParams, dtype: int = DTYPE_F32) -> np.ndarray:
+    """``mixed_self_attention`` (attention.hpp:309-365) for one query: q [1, d_m], prefix
+    hidden states [t_in, d_m], generated-token cache built from ``gen_rows`` [t_out, d_m] by
+    ``KvCache::append`` (:134-150) -> [1, d_m]."""
+    h, d_m, _ = _params_dims(p)
+    q, P = np.asarray(q, np.float64), np.asarray(prefix_hidden, np.float64)
+    gen = np.asarray(gen_rows, np.float64).reshape(-1, d_m)
+    if P.ndim != 2 or P.shape[0] < 1:
+        raise StateError("mixed_self_attention: empty prefix")
+    if q.ndim != 2 or q.shape != (1, d_m) or P.shape[1] != d_m:
+        raise ShapeError("mixed_self_attention: q/prefix width must equal d_m")
+    layer = _layer(p, dtype)
+    cache = KvCache(layer, 1, max(gen.shape[0], 1))
+    for r in range(gen.shape[0]):
+        cache.append(_as_device(gen[r:r + 1], layer.dtype))
+    out = mixed_self_attention_batched(layer, _as_device(q, layer.dtype), _as_device(P[None], layer.dtype), cache, 1)
     return _to_host(out)

@@ -36,6 +36,9 @@ EXPORTED_SYMBOLS = (
     "elattn_gpu_decoder_kernels_per_run",
     "elattn_gpu_cache_append",
     "elattn_gpu_cache_gather",
+    "elattn_gpu_kv_append",
+    "elattn_gpu_mixed_self_attention",
+    "elattn_gpu_mixed_workspace_size",
     "elattn_gpu_reset_launch_count",
 )
 
@@ -109,6 +112,10 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.elattn_gpu_decoder_kernels_per_run.restype = i64
     lib.elattn_gpu_cache_append.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
     lib.elattn_gpu_cache_gather.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp]
+    lib.elattn_gpu_kv_append.argtypes = [vp, vp, i32, vp, vp, i32, i32, vp]
+    lib.elattn_gpu_mixed_self_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, i32, i32, vp, vp, sz, vp]
+    lib.elattn_gpu_mixed_workspace_size.argtypes = [vp, i32, i32]
+    lib.elattn_gpu_mixed_workspace_size.restype = sz
     for name in EXPORTED_SYMBOLS:
         fn = getattr(lib, name)
         if fn.restype is ctypes.c_int and name not in ("elattn_gpu_decode_kernel_kind",):

@@ -20,6 +20,7 @@ struct elattn_gpu_params_s {
     int include_key_bias = 1, include_value_bias = 1;
     // Device buffers, element type `dtype` unless noted.
     void* WqT = nullptr;  // [h*d_k][d_m]
+    void* WkT = nullptr;  // [h][d_k][d_m]: K-major B operand of the K/V-cache append
     void* Wk = nullptr;   // [h][d_m][d_k]
     void* WvT = nullptr;  // [h][d_k][d_m]
     void* WoT = nullptr;  // [d_m][h*d_k]
@@ -93,7 +94,7 @@ float* upload_f32(const std::vector<double>& v) {
 
 void free_params(elattn_gpu_params_s* p) {
     if (!p) return;
-    for (void* ptr : {p->WqT, p->Wk, p->WvT, p->WoT, (void*)p->bq, (void*)p->bk, (void*)p->bv,
+    for (void* ptr : {p->WqT, p->WkT, p->Wk, p->WvT, p->WoT, (void*)p->bq, (void*)p->bk, (void*)p->bv,
                       (void*)p->bo, p->bq16, p->bo16})
         if (ptr) cudaFree(ptr);
     delete p;
@@ -176,8 +177,7 @@ void query_expansion(const elattn_gpu_params_s* p, const void* Y, int64_t R, voi
 }
 
 // (3a) V_{r,i} = C_{r*h+i}.W_V,i + b_V,i ; (3b) out = V.W_O + b_O   (attention.hpp:283-288)
-void output_projection(const elattn_gpu_params_s* p, const void* C, int64_t R, void* V, void* out,
-                       cudaStream_t st) {
+void v_projection(const elattn_gpu_params_s* p, const void* C, int64_t R, void* V, cudaStream_t st) {
     const int h = p->h, d_m = p->d_m, d_k = p->d_k, hk = h * d_k;
     GemmArgs a{};
     a.A = C, a.lda = int64_t(h) * d_m, a.sAz = d_m;
@@ -186,10 +186,20 @@ void output_projection(const elattn_gpu_params_s* p, const void* C, int64_t R, v
     a.bias = p->bv, a.sbz = d_k;
     a.M = int(R), a.N = d_k, a.K = d_m, a.Z = h, a.alpha = 1.f;
     gemm(p, a, st);
+}
+
+void o_projection(const elattn_gpu_params_s* p, const void* V, int64_t R, void* out, cudaStream_t st) {
+    const int d_m = p->d_m, hk = p->h * p->d_k;
     GemmArgs b{};
     b.A = V, b.lda = hk, b.B = p->WoT, b.ldb = hk, b.C = out, b.ldc = d_m, b.bias = p->bo, b.bias16 = p->bo16;
     b.M = int(R), b.N = d_m, b.K = hk, b.Z = 1, b.alpha = 1.f;
     gemm(p, b, st);
+}
+
+void output_projection(const elattn_gpu_params_s* p, const void* C, int64_t R, void* V, void* out,
+                       cudaStream_t st) {
+    v_projection(p, C, R, V, st);
+    o_projection(p, V, R, out, st);
 }
 
 bool use_tc_decode(const elattn_gpu_params_s* p, int rows_per_input) {
@@ -198,12 +208,12 @@ bool use_tc_decode(const elattn_gpu_params_s* p, int rows_per_input) {
 
 // (2) fused decode: C = softmax(q'.H^T / sqrt(d_k)) . H   (attention.hpp:272-280)
 void decode(const elattn_gpu_params_s* p, const void* qp, const void* H, const int* npi, int B,
-            int rows_per_input, int n, void* C, cudaStream_t st) {
+            int rows_per_input, int n, void* C, cudaStream_t st, float2* stats = nullptr) {
     const float scale = float(1.0 / std::sqrt(double(p->d_k)));
     if (use_tc_decode(p, rows_per_input))
-        launch_el_decode_tc(qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st);
+        launch_el_decode_tc(qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats);
     else
-        launch_el_decode_simt(p->dtype, qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st);
+        launch_el_decode_simt(p->dtype, qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats);
 }
 
 void check_handle(const elattn_gpu_params_s* p) {
@@ -242,13 +252,14 @@ int elattn_gpu_params_create(int h, int d_m, int d_k, int dtype, int include_key
         ELA_REQUIRE(Wq && Wk && Wv && Wo && bq && bk && bv && bo, ELATTN_ERR_SHAPE,
                     "AttentionParams: null weight array");
         const size_t H_ = size_t(h), M = size_t(d_m), K = size_t(d_k);
-        std::vector<double> wqT(H_ * K * M), wk(H_ * M * K), wvT(H_ * K * M), woT(M * H_ * K);
+        std::vector<double> wqT(H_ * K * M), wkT(H_ * K * M), wk(H_ * M * K), wvT(H_ * K * M), woT(M * H_ * K);
         for (size_t i = 0; i < H_; ++i)
             for (size_t j = 0; j < M; ++j)
                 for (size_t c = 0; c < K; ++c) {
                     const size_t src = (i * M + j) * K + c;  // [h][d_m][d_k]
                     wqT[(i * K + c) * M + j] = Wq[src];
                     wk[src] = Wk[src];
+                    wkT[(i * K + c) * M + j] = Wk[src];
                     wvT[(i * K + c) * M + j] = Wv[src];
                 }
         for (size_t i = 0; i < H_; ++i)
@@ -264,6 +275,7 @@ int elattn_gpu_params_create(int h, int d_m, int d_k, int dtype, int include_key
         p->include_value_bias = include_value_bias != 0;
         p->WqT = upload(wqT, dtype);
         p->Wk = upload(wk, dtype);
+        p->WkT = upload(wkT, dtype);
         p->WvT = upload(wvT, dtype);
         p->WoT = upload(woT, dtype);
         p->bq = upload_f32(vbq);
@@ -567,4 +579,68 @@ extern "C" int elattn_gpu_cache_gather(const void* src, const int* src_lengths, 
         launch_cache_gather(src, src_lengths, dst, dst_lengths, parent, lanes_in, lanes_out, n_max, d_m, dtype,
                             rows_hint, reinterpret_cast<cudaStream_t>(stream));
     });
+}
+
+// ---------------------------------------------------------------- decoder-only mixed self-attention
+extern "C" int elattn_gpu_kv_append(elattn_gpu_params_t p, const void* Y, int R, void* Kc, void* Vc, int t_max, int t,
+                                    elattn_stream_t stream) {
+    return guarded([&] {
+        check_handle(p);
+        ELA_REQUIRE(Y && Kc && Vc, ELATTN_ERR_PARAM, "kv_append: null buffer");
+        ELA_REQUIRE(R >= 1 && t_max >= 1, ELATTN_ERR_SHAPE, "kv_append: bad shape");
+        ELA_REQUIRE(t >= 0 && t < t_max, ELATTN_ERR_STATE, "kv_append: cache full");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const int h = p->h, d_m = p->d_m, d_k = p->d_k;
+        const size_t e = dtype_bytes(p->dtype);
+        // K_i / V_i of every lane at position t of [R][h][t_max][d_k]  (KvCache::append,
+        // attention.hpp:134-150): one head-batched GEMM each, Y shared by the heads
+        for (int kv = 0; kv < 2; ++kv) {
+            GemmArgs a{};
+            a.A = Y, a.lda = d_m, a.sAz = 0;
+            a.B = kv == 0 ? p->WkT : p->WvT, a.ldb = d_m, a.sBz = int64_t(d_k) * d_m;
+            a.C = static_cast<char*>(kv == 0 ? Kc : Vc) + size_t(t) * d_k * e;
+            a.ldc = int64_t(h) * t_max * d_k, a.sCz = int64_t(t_max) * d_k;
+            a.bias = kv == 0 ? (p->include_key_bias ? p->bk : nullptr) : p->bv, a.sbz = d_k;
+            a.M = R, a.N = d_k, a.K = d_m, a.Z = h, a.alpha = 1.f;
+            gemm(p, a, st);
+        }
+    });
+}
+
+extern "C" int elattn_gpu_mixed_self_attention(elattn_gpu_params_t p, const void* Y, const void* P,
+                                               const int* n_per_input, int B, int x, int n, const void* Kc,
+                                               const void* Vc, int t_max, int t_out, void* out, void* ws,
+                                               size_t ws_bytes, elattn_stream_t stream) {
+    return guarded([&] {
+        check_handle(p);
+        ELA_REQUIRE(B >= 1 && x >= 1, ELATTN_ERR_SHAPE, "mixed_self_attention: B and x must be >= 1");
+        ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "mixed_self_attention: empty prefix");
+        ELA_REQUIRE(t_out >= 0 && t_out <= t_max, ELATTN_ERR_STATE,
+                    "mixed_self_attention: cache does not match params");
+        ELA_REQUIRE(Y && P && out && (t_out == 0 || (Kc && Vc)), ELATTN_ERR_PARAM, "mixed_self_attention: null buffer");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const int64_t R = int64_t(B) * x;
+        const size_t e = dtype_bytes(p->dtype);
+        const size_t qb = size_t(R) * p->h * p->d_k * e, qpb = size_t(R) * p->h * p->d_m * e;
+        const size_t sb = size_t(R) * p->h * sizeof(float2);
+        Scratch scratch(ws, ws_bytes, step_workspace(p, R) + align256(sb), st);
+        void* Q = scratch.take(qb);
+        void* qp = scratch.take(qpb);
+        void* C = scratch.take(qpb);
+        void* V = scratch.take(qb);
+        float2* stats = static_cast<float2*>(scratch.take(sb));
+        query_expansion(p, Y, R, Q, qp, st);
+        decode(p, qp, P, n_per_input, B, x * p->h, n, C, st, stats);
+        v_projection(p, C, R, V, st);
+        if (t_out > 0)
+            launch_mixed_combine(p->dtype, Q, stats, V, Kc, Vc, int(R), p->h, p->d_k, t_max, t_out,
+                                 p->include_key_bias ? p->bk : nullptr, float(1.0 / std::sqrt(double(p->d_k))), st);
+        o_projection(p, V, R, out, st);
+    });
+}
+
+extern "C" size_t elattn_gpu_mixed_workspace_size(elattn_gpu_params_t p, int B, int x) {
+    if (!p || B < 1 || x < 1) return 0;
+    const int64_t R = int64_t(B) * x;
+    return step_workspace(p, R) + align256(size_t(R) * p->h * sizeof(float2));
 }

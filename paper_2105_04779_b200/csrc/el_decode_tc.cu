@@ -200,7 +200,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tm_c,
                         const __nv_bfloat16* __restrict__ qp_rows, const int* __restrict__ n_per_input, int B,
                         int rows, int n_stride, int d_m, float scale_log2, __nv_bfloat16* __restrict__ ctx,
-                        unsigned long long* __restrict__ trace, DecodeTuning tune, SplitArgs sa) {
+                        unsigned long long* __restrict__ trace, DecodeTuning tune, SplitArgs sa,
+                        float2* __restrict__ stats) {
     using L = DecLayout<UNITS>;
     constexpr int kRing = L::kRing;
     // optional per-tile clock64 trace of the first cluster (testing hook); G = cluster tile index
@@ -744,6 +745,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if ((lane & 3) == 0) {
                     s_l[ra] = 1.f / l_a;
                     s_l[rb] = 1.f / l_b;
+                    if (stats != nullptr && rank == 0) {  // softmax stats in log2 units (both CTAs agree)
+                        if (ra < rows) stats[int64_t(b) * rows + ra] = make_float2(m_a * scale_log2, l_a);
+                        if (rb < rows) stats[int64_t(b) * rows + rb] = make_float2(m_b * scale_log2, l_b);
+                    }
                 }
                 softmax_bar_sync();
                 float inv_l[16];  // 1/l for this thread's columns q = 8k + 2(t%4) + {0,1}
@@ -886,7 +891,8 @@ constexpr int kMaxSegs = 8;
 template <int UNITS>
 __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __restrict__ part, int T, int W, int ncl,
                                                               int rows, int d_m, float scale_log2,
-                                                              __nv_bfloat16* __restrict__ ctx) {
+                                                              __nv_bfloat16* __restrict__ ctx,
+                                                              float2* __restrict__ stats) {
     constexpr int kPF = kPartFloatsHdr + UNITS * kPartFloatsUnit;
     const int k = int(blockIdx.x) + 1, rank = int(blockIdx.y), m = int(blockIdx.z);
     const int64_t gk = int64_t(k) * W;
@@ -922,6 +928,8 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
                 L += ls[s] * w;
             }
         s_inv[tid] = 1.f / L;
+        if (stats != nullptr && rank == 0 && m == 0 && tid < rows)
+            stats[int64_t(b) * rows + tid] = make_float2(M * scale_log2, L);
     }
     __syncthreads();
     // fragment float4 e = (h * 8 + i4) * 128 + t of the unit; this thread takes e = tid + 256 j
@@ -977,7 +985,7 @@ constexpr int kMinChunkTiles = 8;  // bounds the segments per input (merge cost)
 
 template <int UNITS>
 void launch_units(const void* qp, const void* H, const int* npi, int B, int rows, int n_stride, int d_m,
-                  float scale_log2, void* ctx, cudaStream_t st) {
+                  float scale_log2, void* ctx, cudaStream_t st, float2* stats) {
     // > 64 query rows per input: rows/64 virtual inputs of 64 rows each (q' and C rows are
     // contiguous per input, so virtual input v owns rows [64 v, 64 v + 64)); H_b is shared
     const int vchunks = rows > kRowsQ ? rows / kRowsQ : 1;
@@ -1035,11 +1043,11 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     }
     kern<<<dim3(2 * clusters), kThreads, smem, st>>>(tq, th, tc, static_cast<const __nv_bfloat16*>(qp), npi, B, rows,
                                                      n_stride, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx),
-                                                     g_decode_trace, g_tuning, sa);
+                                                     g_decode_trace, g_tuning, sa, stats);
     ELA_CHECK_LAUNCH();
     if (sa.part != nullptr && clusters > 1) {
         el_decode_merge_kernel<UNITS><<<dim3(clusters - 1, 2, UNITS), 256, 0, st>>>(
-            sa.part, sa.T, sa.W, clusters, rows, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx));
+            sa.part, sa.T, sa.W, clusters, rows, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx), stats);
         ELA_CHECK_LAUNCH();
     }
 }
@@ -1055,7 +1063,7 @@ bool el_decode_tc_supported(int rows_per_input, int d_m) {
 }
 
 void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B, int rows_per_input,
-                         int n_stride, int d_m, float scale, void* ctx, cudaStream_t st) {
+                         int n_stride, int d_m, float scale, void* ctx, cudaStream_t st, float2* stats) {
     ELA_REQUIRE(el_decode_tc_supported(rows_per_input, d_m), ELATTN_ERR_UNSUPPORTED,
                 "tcgen05 decode: rows <= 64 or a multiple of 64 (<= 512), d_m in {256, 512, 768, 1024}");
     ELA_REQUIRE((reinterpret_cast<uintptr_t>(qp) & 15) == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0 &&
@@ -1069,10 +1077,10 @@ void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, 
     }();
     (void)env_read;
     switch (d_m / 256) {
-        case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st);
-        case 2: return launch_units<2>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st);
-        case 3: return launch_units<3>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st);
-        default: return launch_units<4>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st);
+        case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats);
+        case 2: return launch_units<2>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats);
+        case 3: return launch_units<3>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats);
+        default: return launch_units<4>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats);
     }
 }
 

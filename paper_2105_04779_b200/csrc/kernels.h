@@ -33,9 +33,12 @@ void launch_key_bias_scalars(int dtype, const void* Q, const float* bk, int R, i
                              float* s, cudaStream_t st);
 
 // SIMT fused EL decode: ctx[b*rows + r] = softmax(q'_r . H_b^T * scale) . H_b.
+// stats (optional, may be null): per query row float2 {m, l} of the softmax in log2
+// units — p_j = 2^(s_j * scale * log2(e) - m) / l — for callers that merge the decode
+// with other score sources (mixed self-attention).
 void launch_el_decode_simt(int dtype, const void* qp, const void* H, const int* n_per_input,
                            int B, int rows_per_input, int n_stride, int d_m, float scale,
-                           void* ctx, cudaStream_t st);
+                           void* ctx, cudaStream_t st, float2* stats = nullptr);
 
 // tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM, bf16 out), same contract as
 // launch_simt_gemm but requires K % 64 == 0, 16-byte aligned rows and
@@ -48,6 +51,11 @@ void launch_tc_gemm(const GemmArgs& g, cudaStream_t st);
 // the output type, so the bf16 path stores b_Q and b_O in bf16 (GemmArgs::bias16).
 bool lt_gemm_supported(const GemmArgs& g);
 void launch_lt_gemm(const GemmArgs& g, cudaStream_t st);
+
+// Mixed self-attention merge (mixed.cu): see the file header.
+void launch_mixed_combine(int dtype, const void* Q, const float2* stats, void* V, const void* Kc, const void* Vc,
+                          int R, int h, int d_k, int64_t t_max, int t_out, const float* bk, float scale,
+                          cudaStream_t st);
 
 // Per-lane hidden-state caches (lane_cache.cu).
 void launch_cache_append(void* cache, const void* Y, int* len, int lanes, int n_max, int d_m, int dtype,
@@ -64,6 +72,6 @@ extern unsigned long long* g_decode_trace;
 bool el_decode_tc_supported(int rows_per_input, int d_m);
 void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B,
                          int rows_per_input, int n_stride, int d_m, float scale, void* ctx,
-                         cudaStream_t st);
+                         cudaStream_t st, float2* stats = nullptr);
 
 }  // namespace elattn_gpu

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
                                                              const int* __restrict__ n_per_input,
                                                              int rows_per_input, int n_stride,
                                                              int d_m, float scale_log2,
-                                                             T* __restrict__ ctx) {
+                                                             T* __restrict__ ctx, float2* __restrict__ stats) {
     extern __shared__ float smem[];
     const int ldq = d_m, ldh = d_m + 1;  // +1: conflict-free column walks of the H tile
     float* sq = smem;                                // [16][d_m]
@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
     if (n < 1 || n > n_stride) {  // ragged length out of contract: loud NaN rows
         for (int e = tid; e < nrows * d_m; e += 256)
             ctx[(row_base + e / d_m) * d_m + e % d_m] = from_f32<T>(__int_as_float(0x7fc00000));
+        if (stats != nullptr && tid < nrows) stats[row_base + tid] = make_float2(__int_as_float(0x7fc00000), 0.f);
         return;
     }
     for (int e = tid; e < kSimtRows * d_m; e += 256) {
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
         if (st_ == 0) {
             s_alpha[sr] = alpha;
             s_l[sr] = l_run;
+            if (stats != nullptr && sr < nrows) stats[row_base + sr] = make_float2(m_run, l_run);
         }
         __syncthreads();
 #pragma unroll
@@ -216,7 +218,8 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
 
 template <typename T, int CPT>
 static void launch_decode_cpt(const void* qp, const void* H, const int* npi, int B, int rows,
-                              int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st) {
+                              int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st,
+                              float2* stats) {
     const size_t smem =
         sizeof(float) * (size_t(kSimtRows) * d_m + size_t(kSimtTile) * (d_m + 1) +
                          kSimtRows * kSimtTile + 2 * kSimtRows);
@@ -224,21 +227,22 @@ static void launch_decode_cpt(const void* qp, const void* H, const int* npi, int
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     dim3 grid(unsigned(ceil_div(rows, kSimtRows)), unsigned(B));
     kern<<<grid, 256, smem, st>>>(static_cast<const T*>(qp), static_cast<const T*>(H), npi, rows,
-                                  n_stride, d_m, scale_log2, static_cast<T*>(ctx));
+                                  n_stride, d_m, scale_log2, static_cast<T*>(ctx), stats);
     ELA_CHECK_LAUNCH();
 }
 
 template <typename T>
 static void launch_decode_t(const void* qp, const void* H, const int* npi, int B, int rows,
-                            int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st) {
+                            int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st,
+                            float2* stats) {
     const int cpt = int(ceil_div(d_m, 256));
     switch (cpt) {
-        case 1: return launch_decode_cpt<T, 1>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
-        case 2: return launch_decode_cpt<T, 2>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
-        case 3: return launch_decode_cpt<T, 3>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
-        case 4: return launch_decode_cpt<T, 4>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
-        case 5: return launch_decode_cpt<T, 5>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
-        case 6: return launch_decode_cpt<T, 6>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st);
+        case 1: return launch_decode_cpt<T, 1>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
+        case 2: return launch_decode_cpt<T, 2>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
+        case 3: return launch_decode_cpt<T, 3>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
+        case 4: return launch_decode_cpt<T, 4>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
+        case 5: return launch_decode_cpt<T, 5>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
+        case 6: return launch_decode_cpt<T, 6>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
         default:
             throw Status{ELATTN_ERR_UNSUPPORTED, "SIMT decode supports d_m <= 1536"};
     }
@@ -246,14 +250,14 @@ static void launch_decode_t(const void* qp, const void* H, const int* npi, int B
 
 void launch_el_decode_simt(int dtype, const void* qp, const void* H, const int* n_per_input,
                            int B, int rows_per_input, int n_stride, int d_m, float scale,
-                           void* ctx, cudaStream_t st) {
+                           void* ctx, cudaStream_t st, float2* stats) {
     const float scale_log2 = scale * 1.4426950408889634f;
     if (dtype == ELATTN_DTYPE_BF16)
         launch_decode_t<__nv_bfloat16>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m,
-                                       scale_log2, ctx, st);
+                                       scale_log2, ctx, st, stats);
     else
         launch_decode_t<float>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2,
-                               ctx, st);
+                               ctx, st, stats);
 }
 
 }  // namespace elattn_gpu

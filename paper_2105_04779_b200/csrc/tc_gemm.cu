@@ -57,7 +57,8 @@ struct GemmParams {
     float alpha;
     const float* bias;
     int64_t sbz;
-    int a_zm, b_zm, c_zm;  // 1: tensor map coordinate order is (k, z, m) instead of (k, m, z)
+    int a_zm, b_zm, c_zm;
+    int a_bcast;  // A shared by every z (sAz == 0): load it with z = 0  // 1: tensor map coordinate order is (k, z, m) instead of (k, m, z)
 };
 
 
@@ -134,10 +135,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* a = smem + s * S::kStageBytes;
                     uint8_t* b = a + S::kABytes;
                     ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
+                    const int za = p.a_bcast ? 0 : z;
                     if (p.a_zm)
-                        ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, z, m0, ptx::kEvictNormal);
+                        ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, za, m0, ptx::kEvictNormal);
                     else
-                        ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, m0, z, ptx::kEvictNormal);
+                        ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, m0, za, ptx::kEvictNormal);
                     if (p.b_zm)
                         ptx::tma_load_3d(b, &tmB, &full[s], kb * kBK, z, n0, ptx::kEvictLast);
                     else
@@ -301,7 +303,8 @@ void launch_bn(const GemmArgs& g, cudaStream_t st) {
     p.M = g.M, p.N = g.N, p.K = g.K, p.Z = g.Z, p.alpha = g.alpha, p.bias = g.bias, p.sbz = g.sbz;
     p.tiles_m = int(ceil_div(g.M, kBM));
     p.tiles_n = int(ceil_div(g.N, BN));
-    CUtensorMap ta = operand_map(g.A, g.lda, g.sAz, g.M, g.K, g.Z, kBM, &p.a_zm);
+    p.a_bcast = (g.Z > 1 && g.sAz == 0) ? 1 : 0;
+    CUtensorMap ta = operand_map(g.A, g.lda, g.sAz, g.M, g.K, p.a_bcast ? 1 : g.Z, kBM, &p.a_zm);
     CUtensorMap tb = operand_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, BN, &p.b_zm);
     // output C[z][m][n]: boxes of 32 rows x kBoxCols columns (one epilogue warp's piece),
     // clipped at M / N

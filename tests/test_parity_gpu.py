@@ -294,3 +294,52 @@ def test_hidden_state_cache_self_attention(gpu, dtype):
         got = cache.cache[0].double().cpu().numpy()
         for l in range(lanes):
             assert np.array_equal(got[l, :len(hist[l])], np.stack(hist[l]))
+
+
+@pytest.mark.parametrize("kb,vb,t_out", [(1, 1, 3), (1, 1, 0), (0, 1, 2), (1, 0, 4), (0, 0, 1)])
+def test_fp32_mixed_self_attention_vs_oracle(gpu, kb, vb, t_out):
+    """Reference-shaped mixed_self_attention (attention.hpp:309-365) on the fp32 path vs the
+    oracle (itself pinned bit-exact to the reference in test_oracle.py)."""
+    E = gpu
+    rng = O.OracleRng(900 + 10 * kb + vb + t_out)
+    p = O.params_random(4, 16, 4, rng)
+    p.include_key_bias, p.include_value_bias = bool(kb), bool(vb)
+    q, Hp, gen = rng.uniform((1, 16)), rng.uniform((5, 16)), rng.uniform((t_out, 16))
+    got = E.mixed_self_attention(q, Hp, gen, to_prod(p), E.DTYPE_F32)
+    want = O.mixed_self_attention(p, q, Hp, gen)
+    assert rel_err(got, want) <= TOL[0]
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_mixed_self_attention_batched_vs_oracle(gpu, dtype):
+    """Batched decoder-only steps: B inputs x x lanes share their input's prefix, each lane
+    appends its row to its own generated cache then attends (model.hpp:365-367)."""
+    import torch
+
+    E = gpu
+    c = dict(BART_CFG) if dtype == 1 else dict(ORACLE_CFG)
+    B, x, n, steps = 3, c["x"], 150, 4
+    p = O.params_random(c["h"], c["d_m"], c["d_k"], O.OracleRng(501))
+    layer = E.ElAttentionLayer(to_prod(p), dtype)
+    td = torch.bfloat16 if dtype == 1 else torch.float32
+    from paper_2105_04779_b200.attention import round_to_dtype
+
+    rng = O.OracleRng(502)
+    P = round_to_dtype(rng.uniform((B, n, c["d_m"])), dtype)
+    npi = np.array([150, 33, 97], dtype=np.int32)
+    Pd = torch.from_numpy(P).to("cuda", td)
+    npd = torch.from_numpy(npi).cuda()
+    cache = E.KvCache(layer, B * x, steps)
+    pr = round_params(p, dtype)
+    gen = [[] for _ in range(B * x)]
+    for step in range(steps):
+        Y = round_to_dtype(rng.uniform((B * x, c["d_m"])), dtype)
+        Yd = torch.from_numpy(Y).to("cuda", td)
+        cache.append(Yd)
+        for r in range(B * x):
+            gen[r].append(Y[r])
+        out = E.mixed_self_attention_batched(layer, Yd, Pd, cache, x, npd).double().cpu().numpy()
+        for r in range(B * x):
+            b = r // x
+            want = O.mixed_self_attention(pr, Y[r:r + 1], P[b, :npi[b]], np.stack(gen[r]))
+            assert rel_err(out[r:r + 1], want) <= TOL[dtype], (step, r)
