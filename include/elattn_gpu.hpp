@@ -7,6 +7,10 @@
 //   elattn::fold_el_queries(queries, h, d_m)              attention.hpp:293-304
 //   elattn::el_attention(q, H, p)                         attention.hpp:239-257
 //   elattn::el_attention_folded(queries, H, s, p)         attention.hpp:262-290
+//   elattn::mixed_self_attention(q, prefix, cache, p)     attention.hpp:309-365
+//
+// plus DecoderStep (the batched, graph-captured decoder step over L layers that replaces
+// the per-lane loop of model.hpp:357-385) for device-resident decode loops.
 //
 // A reference caller switches by changing the namespace (optionally passing a
 // Dtype; the default, f32, meets the 1e-5 parity gate).  The arithmetic runs in
@@ -234,6 +238,63 @@ inline void el_attention_step(const DeviceParams& dp, const void* Y, const void*
     check(elattn_gpu_el_attention_step(dp.handle(), Y, H, n_per_input, B, x, n, out, workspace, workspace_bytes,
                                        reinterpret_cast<elattn_stream_t>(stream)));
 }
+
+// mixed_self_attention (attention.hpp:309-365): the reference's KvCache is uploaded as the
+// generated-token cache [1][h][t][d_k] of elattn_gpu_mixed_self_attention.
+inline Tensor mixed_self_attention(const Tensor& q, const Tensor& prefix_hidden, const KvCache& gen_cache,
+                                   const DeviceParams& dp) {
+    if (prefix_hidden.empty() || prefix_hidden.rows() < 1) throw StateError("mixed_self_attention: empty prefix");
+    if (gen_cache.t > 0 && (gen_cache.h != dp.h() || gen_cache.d_k != dp.d_k))
+        throw StateError("mixed_self_attention: cache does not match params");
+    if (q.rows() != 1 || q.cols() != dp.d_m || prefix_hidden.cols() != dp.d_m)
+        throw ShapeError("mixed_self_attention: q/prefix width must equal d_m");
+    const int t = int(gen_cache.t), t_max = t > 0 ? t : 1, n = int(prefix_hidden.rows());
+    std::vector<double> K(size_t(dp.h()) * t_max * dp.d_k, 0.0), V(K.size(), 0.0);
+    for (int i = 0; i < dp.h() && t > 0; ++i)
+        for (size_t j = 0; j < size_t(t) * dp.d_k; ++j) {
+            K[size_t(i) * t_max * dp.d_k + j] = gen_cache.K[size_t(i)][j];
+            V[size_t(i) * t_max * dp.d_k + j] = gen_cache.V[size_t(i)][j];
+        }
+    detail::DeviceBuffer dq(size_t(dp.d_m), dp.dtype()), dP(size_t(prefix_hidden.size()), dp.dtype()),
+        dK(K.size(), dp.dtype()), dV(V.size(), dp.dtype()), dout(size_t(dp.d_m), dp.dtype());
+    dq.upload(q.data().data());
+    dP.upload(prefix_hidden.data().data());
+    dK.upload(K.data());
+    dV.upload(V.data());
+    check(elattn_gpu_mixed_self_attention(dp.handle(), dq.get(), dP.get(), nullptr, 1, 1, n, dK.get(), dV.get(),
+                                          t_max, t, dout.get(), nullptr, 0, nullptr));
+    check_cuda(cudaDeviceSynchronize());
+    Tensor out({1, dp.d_m});
+    dout.download(out.data().data());
+    return out;
+}
+inline Tensor mixed_self_attention(const Tensor& q, const Tensor& prefix_hidden, const KvCache& gen_cache,
+                                   const AttentionParams& p, Dtype dt = Dtype::f32) {
+    p.validate();
+    DeviceParams dp(p, dt);
+    return mixed_self_attention(q, prefix_hidden, gen_cache, dp);
+}
+
+// Batched decoder step over L layers sharing one encoder state per input (RAII over
+// elattn_gpu_decoder_*): bind device buffers once, then run() per step.
+class DecoderStep {
+   public:
+    DecoderStep(const std::vector<const DeviceParams*>& layers, const void* H, const int* n_per_input, int B, int x,
+                int n, const void* Y_in, void* out) {
+        std::vector<elattn_gpu_params_t> hs;
+        for (const DeviceParams* l : layers) hs.push_back(l->handle());
+        check(elattn_gpu_decoder_create(hs.data(), int(hs.size()), H, n_per_input, B, x, n, Y_in, out, &dec_));
+    }
+    ~DecoderStep() {
+        if (dec_) elattn_gpu_decoder_destroy(dec_);
+    }
+    DecoderStep(const DecoderStep&) = delete;
+    DecoderStep& operator=(const DecoderStep&) = delete;
+    void run(cudaStream_t stream = nullptr) { check(elattn_gpu_decoder_run(dec_, reinterpret_cast<elattn_stream_t>(stream))); }
+
+   private:
+    elattn_gpu_decoder_t dec_ = nullptr;
+};
 
 }  // namespace gpu
 }  // namespace elattn

@@ -170,6 +170,50 @@ int main() {
         const double e = rel_err(gpu::el_attention(q, H, dp), want);
         report("BART-large beam 4, n 300, bf16 tcgen05 path", e <= 2e-2, "rel err " + std::to_string(e));
     }
+    // decoder-only mixed self-attention (attention.hpp:309-365) against the reference,
+    // with the generated-token cache built by the reference's own KvCache::append
+    for (int variant = 0; variant < 3; ++variant) {
+        Rng rng(700 + variant);
+        AttentionParams p = AttentionParams::random(4, 16, 4, rng);
+        p.include_key_bias = variant != 1;
+        p.include_value_bias = variant != 2;
+        Tensor q = random_tensor({1, 16}, 710 + variant), P = random_tensor({5, 16}, 720 + variant);
+        KvCache cache(4, 4);
+        for (int r = 0; r < 3; ++r) cache.append(random_tensor({1, 16}, 730 + 10 * variant + r), p);
+        Tensor want = mixed_self_attention(q, P, cache, p);
+        const double e = rel_err(gpu::mixed_self_attention(q, P, cache, p), want);
+        report("mixed_self_attention fp32 (variant " + std::to_string(variant) + ")", e <= 1e-5,
+               "rel err " + std::to_string(e));
+    }
+    report("mixed_self_attention: empty prefix rejected (StateError)", throws<StateError>([&] {
+               Rng rng(1);
+               AttentionParams p = AttentionParams::random(2, 8, 4, rng);
+               gpu::mixed_self_attention(random_tensor({1, 8}, 3), Tensor(), KvCache(2, 4), p);
+           }));
+    // DecoderStep: 2 layers through the graph == the reference's el_attention chained
+    {
+        Rng r1(41), r2(42);
+        AttentionParams p1 = AttentionParams::random(2, 64, 32, r1), p2 = AttentionParams::random(2, 64, 32, r2);
+        Tensor H = random_tensor({40, 64}, 43), y = random_tensor({3, 64}, 44);
+        gpu::DeviceParams d1(p1), d2(p2);
+        gpu::detail::DeviceBuffer dH(size_t(H.size()), gpu::Dtype::f32), dY(size_t(y.size()), gpu::Dtype::f32),
+            dO(size_t(y.size()), gpu::Dtype::f32);
+        dH.upload(H.data().data());
+        dY.upload(y.data().data());
+        gpu::DecoderStep dec({&d1, &d2}, dH.get(), nullptr, 1, 3, 40, dY.get(), dO.get());
+        dec.run();
+        gpu::check_cuda(cudaDeviceSynchronize());
+        Tensor got({3, 64});
+        dO.download(got.data().data());
+        Tensor want({3, 64});
+        for (int k = 0; k < 3; ++k) {
+            Tensor a = elattn::el_attention(y.row(k), H, p1);
+            Tensor b = elattn::el_attention(a, H, p2);
+            for (int j = 0; j < 64; ++j) want.at(k, j) = b.at(0, j);
+        }
+        const double e = rel_err(got, want);
+        report("DecoderStep (2 layers, CUDA graph) fp32", e <= 1e-5, "rel err " + std::to_string(e));
+    }
     std::printf("%d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
 }
