@@ -285,18 +285,30 @@ def gpu_arm(args):
     ctx = torch.empty_like(qp)
     layers[0].build_el_query(Y0, qp, stream=stream)
     L0 = capi.lib()
+    # the decode kernel (+ its stream-K merge) alone: `reps` launches captured into a CUDA
+    # graph on a side stream, replayed between CUDA events on that stream (device time,
+    # no host launch gaps)
+    dstream = torch.cuda.Stream()
+    dstream.wait_stream(stream)
+
     def decode_once():
         capi.check(L0.elattn_gpu_el_attention_decode(layers[0].dev.handle, qp.data_ptr(), H.data_ptr(), None,
-                                                     B, x * h, n, ctx.data_ptr(), stream.cuda_stream))
-    for _ in range(3):
-        decode_once()
-    torch.cuda.synchronize()
+                                                     B, x * h, n, ctx.data_ptr(), dstream.cuda_stream))
     reps = max(args.steps, 10)
+    with torch.cuda.stream(dstream):
+        decode_once()  # allocates this stream's scratch outside the capture
+        torch.cuda.synchronize()
+        dgraph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(dgraph, stream=dstream):
+            for _ in range(reps):
+                decode_once()
     d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    d0.record(stream)
-    for _ in range(reps):
-        decode_once()
-    d1.record(stream)
+    with torch.cuda.stream(dstream):  # CUDAGraph.replay launches on the current stream
+        dgraph.replay()
+        torch.cuda.synchronize()
+        d0.record(dstream)
+        dgraph.replay()
+        d1.record(dstream)
     torch.cuda.synchronize()
     dec_ms = d0.elapsed_time(d1) / reps
     hbm, tf_burst, tf_sust, peak_src = peaks()
