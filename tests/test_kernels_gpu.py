@@ -210,3 +210,37 @@ def test_decode_virtual_inputs_ragged():
     want = decode_ref(qp, H, rows, 0.125, npi)
     assert torch.isfinite(ctx.float()).all()
     assert (ctx.float() - want).abs().max().item() / want.abs().max().item() < 2e-2
+
+
+def test_decode_schedules_agree_over_random_batches():
+    """Stream-K (short last round) and whole-input schedules agree for a sweep of batch
+    sizes / context lengths around the 74-cluster boundaries (first-boundary-in-input and
+    record-slot bookkeeping of the merge), and the result matches torch fp32."""
+    import torch
+
+    L, capi = _testing_lib()
+    rng = np.random.default_rng(5)
+    cases = [(1, 1024), (7, 100), (37, 64), (73, 1024), (74, 300), (75, 1024), (111, 33), (148, 257),
+             (150, 1024), (222, 96)] + [(int(b), int(n)) for b, n in zip(rng.integers(1, 200, 6),
+                                                                       rng.choice([32, 130, 511, 1024], 6))]
+    st = torch.cuda.current_stream().cuda_stream
+    for B, n in cases:
+        rows, d_m = 64, 512
+        g = torch.Generator(device="cuda").manual_seed(B * 31 + n)
+        qp = (torch.randn(B * rows, d_m, generator=g, device="cuda") * 0.3).to(torch.bfloat16)
+        H = (torch.rand(B, n, d_m, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+        outs = []
+        for npi in (None, torch.full((B,), n, dtype=torch.int32, device="cuda")):
+            ctx = torch.full((B * rows, d_m), float("nan"), device="cuda", dtype=torch.bfloat16)
+            capi.check(L.elattn_gpu_testing_decode_bf16(qp.data_ptr(), H.data_ptr(),
+                                                        npi.data_ptr() if npi is not None else None, B, rows, n, d_m,
+                                                        0.125, ctx.data_ptr(), 1, st))
+            torch.cuda.synchronize()
+            outs.append(ctx.float())
+        assert torch.isfinite(outs[0]).all(), (B, n)
+        scale = outs[1].abs().max().item()
+        assert (outs[0] - outs[1]).abs().max().item() / scale < 1e-2, (B, n)
+        sel = torch.tensor(sorted({0, B // 2, B - 1}), device="cuda")
+        want = decode_ref(qp.view(B, rows, d_m)[sel].reshape(-1, d_m), H[sel], rows, 0.125)
+        got = outs[0].view(B, rows, d_m)[sel].reshape(-1, d_m)
+        assert (got - want).abs().max().item() / want.abs().max().item() < 2e-2, (B, n)
