@@ -57,8 +57,8 @@ struct GemmParams {
     float alpha;
     const float* bias;
     int64_t sbz;
-    int a_zm, b_zm, c_zm;
-    int a_bcast;  // A shared by every z (sAz == 0): load it with z = 0  // 1: tensor map coordinate order is (k, z, m) instead of (k, m, z)
+    int a_zm, b_zm, c_zm;  // 1: tensor map coordinate order is (k, z, m) instead of (k, m, z)
+    int a_bcast;  // A shared by every z (sAz == 0): load it with z = 0
 };
 
 
