@@ -58,10 +58,11 @@ constexpr int kChunkBytes = 4096;  // 32 rows x 64 d_m
 constexpr int kThreads = 384;
 constexpr int kSBuf = 4;  // S accumulators in TMEM
 constexpr int kEpiWarpBytes = 4096;  // per-warp epilogue stage (64 q x 32 d bf16), aliases P
-// partial record of a split input, per (slot, CTA rank): m[64], l[64], then per O unit the
-// 128 softmax threads' 64 fp32 fragment values (float4-interleaved by thread)
+// partial record of a split input, per (slot, CTA rank): m[64], l[64] (fp32), then per O
+// unit the 128 softmax threads' 64 unnormalised fragment values in bf16 (4 values = 8 bytes
+// per slot, interleaved by thread so every store / load is coalesced)
 constexpr int kPartFloatsHdr = 128;
-constexpr int kPartFloatsUnit = 128 * 64;
+constexpr int kPartFloatsUnit = 128 * 32;  // 32-bit words: 64 bf16 values per softmax thread
 constexpr int kQPrefetchTiles = 8;  // next segment's q' is prefetched into L2 this many tiles ahead
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max grows by > 2^8
 
@@ -807,15 +808,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(o_free);
                     }
-                    float4* body = reinterpret_cast<float4*>(rec + kPartFloatsHdr + m * kPartFloatsUnit);
+                    uint2* body = reinterpret_cast<uint2*>(rec + kPartFloatsHdr + m * kPartFloatsUnit);
 #pragma unroll
                     for (int i4 = 0; i4 < 8; ++i4) {
                         body[(0 * 8 + i4) * 128 + tid] =
-                            make_float4(__uint_as_float(lo[4 * i4]), __uint_as_float(lo[4 * i4 + 1]),
-                                        __uint_as_float(lo[4 * i4 + 2]), __uint_as_float(lo[4 * i4 + 3]));
+                            make_uint2(pack_bf16x2(__uint_as_float(lo[4 * i4]), __uint_as_float(lo[4 * i4 + 1])),
+                                       pack_bf16x2(__uint_as_float(lo[4 * i4 + 2]), __uint_as_float(lo[4 * i4 + 3])));
                         body[(1 * 8 + i4) * 128 + tid] =
-                            make_float4(__uint_as_float(hi[4 * i4]), __uint_as_float(hi[4 * i4 + 1]),
-                                        __uint_as_float(hi[4 * i4 + 2]), __uint_as_float(hi[4 * i4 + 3]));
+                            make_uint2(pack_bf16x2(__uint_as_float(hi[4 * i4]), __uint_as_float(hi[4 * i4 + 1])),
+                                       pack_bf16x2(__uint_as_float(hi[4 * i4 + 2]), __uint_as_float(hi[4 * i4 + 3])));
                     }
                 }
             }
@@ -938,8 +939,8 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
 #pragma unroll
     for (int j = 0; j < kPer; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < nseg; ++s) {
-        const float4* body = reinterpret_cast<const float4*>(s_rec[s] + kPartFloatsHdr + m * kPartFloatsUnit);
-        float4 v[kPer];
+        const uint2* body = reinterpret_cast<const uint2*>(s_rec[s] + kPartFloatsHdr + m * kPartFloatsUnit);
+        uint2 v[kPer];
 #pragma unroll
         for (int j = 0; j < kPer; ++j) v[j] = __ldcg(body + tid + 256 * j);
 #pragma unroll
@@ -947,7 +948,9 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
             const int e = tid + 256 * j, t = e & 127, i4 = (e >> 7) & 7;
             const int q0 = 8 * i4 + 2 * (t & 3);
             const float w0 = s_w[s][q0], w1 = s_w[s][q0 + 1];
-            acc[j].x += v[j].x * w0, acc[j].y += v[j].y * w1, acc[j].z += v[j].z * w0, acc[j].w += v[j].w * w1;
+            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[j].x));
+            const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[j].y));
+            acc[j].x += a.x * w0, acc[j].y += a.y * w1, acc[j].z += c.x * w0, acc[j].w += c.y * w1;
         }
     }
 #pragma unroll
