@@ -1017,11 +1017,19 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const int max_cl = num_sms_decode() / 2;
     int clusters;
     SplitArgs sa{};
-    // Whole inputs strided over the clusters unless the last round would leave more than
-    // half of the clusters idle: then stream-K (every input-segment transition costs a
-    // pipeline drain, so splitting only pays when the tail is short; measured on B200).
+    // Whole inputs strided over the clusters unless the last round would fill less than 60%
+    // of the clusters: then stream-K (every input-segment transition costs a pipeline drain,
+    // so splitting only pays when the tail is short; measured on B200 for B = 64..320).
     const int last_round = B % max_cl;
-    const bool stream_k = npi == nullptr && last_round != 0 && 2 * last_round < max_cl;
+    // ELATTN_DECODE_SCHED = auto (default) | streamk | whole: tuning override
+    static const int sched_mode = [] {
+        const char* e = getenv("ELATTN_DECODE_SCHED");
+        if (!e) return 0;
+        const std::string v(e);
+        return v == "streamk" ? 1 : v == "whole" ? 2 : 0;
+    }();
+    const bool stream_k = npi == nullptr && last_round != 0 &&
+                          (sched_mode == 1 || (sched_mode == 0 && 5 * last_round < 3 * max_cl));
     if (stream_k) {
         // stream-K over B*T tiles: chunks of W tiles (>= kMinChunkTiles), one per cluster
         const int T = (n_stride + kNT - 1) / kNT;
