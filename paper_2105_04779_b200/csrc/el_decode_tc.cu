@@ -6,9 +6,12 @@
 // HBM exactly once and using every staged tile as BOTH key and value.
 //
 // Work split — thread-block CLUSTERS of 2 CTAs, split along d_m; persistent:
-//   cluster c processes inputs c, c + #clusters, ... as one continuous pipeline (a
-//   cluster-global tile counter drives every ring / buffer phase across inputs, so
-//   the next input's q' and H tiles stream in while the previous input drains).
+//   each cluster walks a list of SEGMENTS (whole inputs c, c + #clusters, ..., or — when
+//   the last round is short — a stream-K chunk of the B*T tiles, whose partial inputs
+//   are combined by el_decode_merge_kernel) as one continuous pipeline: a cluster-global
+//   tile counter drives every ring / buffer phase across segments, so the next segment's
+//   q' and H tiles stream in while the previous one drains.  Inputs with more than 64
+//   query rows run as rows/64 virtual inputs sharing H.
 //   CTA r owns d_m columns [r*d_m/2, (r+1)*d_m/2).  Its EL-Q half q'_r (64 x d_m/2)
 //   is held half in TMEM (as the A operand of the score MMA) and half in smem; H_b
 //   streams through a TMA ring in tiles of 32 rows x d_m/2 (SWIZZLE_128B, 128-column
@@ -21,7 +24,9 @@
 //     O_r^T += H_tile,r^T . P^T          tcgen05.mma M=128 (d_m) N=64 (queries),
 //                                        A = the SAME smem tile read MN-major
 //   O_r (d_m/2 x 64 fp32) lives in TMEM for the whole input; the epilogue divides
-//   by the softmax sums and writes C rows b*rows + q, columns of this CTA's half.
+//   by the softmax sums and writes C rows b*rows + q, columns of this CTA's half
+//   (tcgen05.ld -> stmatrix.trans stage -> TMA store), optionally with the rows'
+//   softmax statistics {m, l} (mixed self-attention).
 // Both CTAs see bit-identical S (fp32 add commutes), so their softmax decisions agree.
 //
 // One thread can issue only ~1 tcgen05.mma per 56 cycles (tools/probes/
