@@ -343,3 +343,15 @@ def test_mixed_self_attention_batched_vs_oracle(gpu, dtype):
             b = r // x
             want = O.mixed_self_attention(pr, Y[r:r + 1], P[b, :npi[b]], np.stack(gen[r]))
             assert rel_err(out[r:r + 1], want) <= TOL[dtype], (step, r)
+
+
+@pytest.mark.parametrize("h,d_m", [(4, 256), (12, 768)])
+def test_bf16_step_other_model_widths(gpu, h, d_m):
+    """d_m = 256 / 768 (UNITS = 1 / 3 of the tcgen05 decode), beam 4 and greedy."""
+    E = gpu
+    for x in (4, 1):
+        p, Y, H = make_case(h, d_m, 64, 300, 3, x, 81 + h, 82 + x)
+        out, layer = run_step(E, p, Y, H, x, E.DTYPE_BF16)
+        assert layer.dev.decode_kernel_kind(x) == 1
+        pr, Yr, Hr = oracle_inputs(p, Y, H, E.DTYPE_BF16)
+        assert rel_err(out, O.el_layer_step(pr, Yr, Hr, x)) <= TOL[1], (h, d_m, x)
