@@ -358,7 +358,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int b, j0, j1, Tb, kind;
         while (sc.next(b, j0, j1, Tb, kind)) {
             const int T = j1 - j0;
-            if (L::kQSmemUnits > 0) ptx::mbar_wait(q_full, li & 1);
+            // the TMEM half of q' (filled from registers) is usually ready before the smem
+            // half (a TMA load after the previous segment's scores drained): start with the
+            // TMEM units and wait for the smem half only when the first smem unit is due
+            bool q_smem_ready = L::kQSmemUnits == 0;
             ptx::mbar_wait(q_tmem_full, li & 1);
             if (warp == 1 && lane == 0) ELA_TRACE(16, li);
             for (int Gt = G + ((G & 1) != parity_mine ? 1 : 0); Gt < G + T; Gt += 2) {
@@ -375,6 +378,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int u = 0; u < UNITS; ++u) {
                     const int g = Gt * UNITS + u, slot = g % kRing;
+                    if (u == L::kQTmemUnits && !q_smem_ready) {
+                        ptx::mbar_wait(q_full, li & 1);
+                        q_smem_ready = true;
+                    }
                     ptx::mbar_wait(&unit_full[slot], (g / kRing) & 1);
                     ptx::tc_fence_after();
                     const uint64_t dB = dRing + uint64_t((slot * kUnitBytes) >> 4);
