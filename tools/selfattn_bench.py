@@ -7,6 +7,10 @@ reorder (gather_lanes on every layer's cache).  Device time per step from CUDA-g
 replays (the graph resets the lengths first, so every replay sees the same n).
 
     python tools/selfattn_bench.py --B 64 --n 128 512 1024
+
+Then the reference's own decoder-only form, mixed self-attention (EL over the prefix shared
+by an input's beams + a per-lane K/V cache of the generated tokens, one joint softmax):
+per step and layer KvCache::append + mixed attention, for a few (prefix, generated) sizes.
 """
 import argparse
 import json
@@ -80,3 +84,27 @@ for n in a.n:
                       "gather_ms_per_step": ms_gather,
                       "gather_GBps": 2 * byt / (ms_gather / 1e3) / 1e9,
                       "cache_GB": cache.cache.numel() * 2 / 1e9}), flush=True)
+
+# ---- the reference's decoder-only EL form: mixed self-attention (EL over the prefix shared
+# by an input's beams + per-lane K/V cache of generated tokens, joint softmax;
+# attention.hpp:309-365), per step: KvCache::append + mixed attention on every layer
+for n_in, t_out in ((512, 64), (512, 256), (1024, 128)):
+    P = (torch.rand((a.B, n_in, d_m), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    caches = [E.KvCache(layers[l], lanes, t_out + 1) for l in range(L)]
+    for c in caches:  # pre-fill t_out - 1 generated rows
+        c.K.copy_((torch.rand(c.K.shape, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+        c.V.copy_((torch.rand(c.V.shape, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+
+    def step_mixed():
+        y = Y
+        for l in range(L):
+            caches[l].t = t_out - 1
+            caches[l].append(y)
+            y = E.mixed_self_attention_batched(layers[l], y, P, caches[l], a.beam, out=outs[l % 2])
+
+    ms = timed(step_mixed)
+    byt = L * (a.B * n_in * d_m * 2 + 2 * lanes * t_out * d_m * 2)  # prefix once per input + K/V of every lane
+    print(json.dumps({"config": "GPT-2 medium decoder-only, mixed self-attention (EL prefix + K/V generated)",
+                      "B": a.B, "beam": a.beam, "lanes": lanes, "layers": L, "prefix_n": n_in, "generated_t": t_out,
+                      "ms_per_step": ms, "tokens_per_s": lanes / (ms / 1e3),
+                      "state_GBps": byt / (ms / 1e3) / 1e9}), flush=True)
