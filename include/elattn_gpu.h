@@ -207,6 +207,17 @@ int elattn_gpu_mixed_self_attention(elattn_gpu_params_t params, const void* Y, c
                                     void* out, void* workspace, size_t workspace_bytes, elattn_stream_t stream);
 size_t elattn_gpu_mixed_workspace_size(elattn_gpu_params_t params, int B, int x);
 
+/*
+ * Beam-search candidate selection on the device (decoding.hpp:186-230).
+ * For each input b: candidates (parent i < roots, token t) with lp_sum = live_lp[b*lanes+i]
+ * + lprobs[(b*lanes+i)*V + t], non-finite log-probs skipped; the k best (k <= 32) in the
+ * reference's candidate_better order (decoding.hpp:163-167: higher lp_sum, then smaller
+ * token, then smaller parent) -> parent/token/lp_sum [B][k] (parent -1 when fewer than k).
+ * roots = 1 on the first step (all lanes identical), = lanes afterwards.
+ */
+int elattn_gpu_beam_candidates(const float* lprobs, const float* live_lp, int B, int lanes, int roots, int V, int k,
+                               int* parent, int* token, float* lp_sum, elattn_stream_t stream);
+
 /* Device-kernel launches issued by this thread since the last reset (for bench
  * accounting of gpu_launches). */
 int64_t elattn_gpu_launch_count(void);

@@ -29,6 +29,8 @@
  *   orc_kv_append              attention.hpp:134-150 (KvCache::append)
  *   orc_mixed_self_attention   attention.hpp:309-365 (decoder-only: EL over the shared
  *                              prefix + MHA over the generated-token cache, joint softmax)
+ *   orc_beam_candidates        beam_search candidate generation + order
+ *                              (decoding.hpp:186-205; candidate_better :163-167)
  *   orc_el_layer_step          build_el_query x g + fold + el_attention_folded per
  *                              input (the batched cross-attention step the GPU
  *                              path computes; SURVEY.md §8 math contract)
@@ -484,4 +486,48 @@ done:
     free(b);
     free(co);
     return rc;
+}
+
+
+/* ------------------------------------------------------------ beam-search candidates */
+typedef struct {
+    int parent, token;
+    double lp_sum;
+} orc_cand;
+
+/* candidate_better (decoding.hpp:163-167) as a qsort order */
+static int cand_cmp(const void* pa, const void* pb) {
+    const orc_cand* a = (const orc_cand*)pa;
+    const orc_cand* b = (const orc_cand*)pb;
+    if (a->lp_sum != b->lp_sum) return a->lp_sum > b->lp_sum ? -1 : 1;
+    if (a->token != b->token) return a->token < b->token ? -1 : 1;
+    return (a->parent > b->parent) - (a->parent < b->parent);
+}
+
+/* decoding.hpp:192-205: for parents i < roots, every finite lprobs[i][tok] gives
+ * (i, tok, live_lp[i] + v); sorted by candidate_better; the first k written (parent -1
+ * beyond the candidate count).  One input; lprobs [lanes][V]. */
+int orc_beam_candidates(const double* lprobs, const double* live_lp, int lanes, int roots, int V, int k,
+                        int* parent, int* token, double* lp_sum) {
+    if (roots < 1 || roots > lanes || V < 1 || k < 1) return ORC_SHAPE;
+    orc_cand* c = (orc_cand*)malloc(sizeof(orc_cand) * (size_t)roots * (size_t)V);
+    if (!c) return ORC_PARAM;
+    size_t n = 0;
+    for (int i = 0; i < roots; ++i)
+        for (int t = 0; t < V; ++t) {
+            const double v = lprobs[(size_t)i * V + t];
+            if (!isfinite(v)) continue;
+            c[n].parent = i, c[n].token = t, c[n].lp_sum = live_lp[i] + v;
+            ++n;
+        }
+    qsort(c, n, sizeof(orc_cand), cand_cmp);
+    for (int r = 0; r < k; ++r) {
+        if ((size_t)r < n) {
+            parent[r] = c[r].parent, token[r] = c[r].token, lp_sum[r] = c[r].lp_sum;
+        } else {
+            parent[r] = -1, token[r] = -1, lp_sum[r] = -INFINITY;
+        }
+    }
+    free(c);
+    return 0;
 }

@@ -17,7 +17,10 @@
 //   mixed_self_attention       attention.hpp:309-365
 //   Rng / seeded_uniform       tensor.hpp:133-150, 236-241
 //   PrecisionGuard             tensor.hpp:25-29
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <limits>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -25,6 +28,7 @@
 #include <vector>
 
 #include "elattn/attention.hpp"
+#include "elattn/decoding.hpp"
 
 using namespace elattn;
 
@@ -254,6 +258,32 @@ int ref_mixed_self_attention(REF_PARAMS_ARGS, const double* q, const double* Hp,
         for (int64_t r = 0; r < t_out; ++r) c.append(from_flat({1, d_m}, gen_rows + r * d_m), p);
         Tensor o = mixed_self_attention(from_flat({1, d_m}, q), from_flat({t_in, d_m}, Hp), c, p);
         to_flat(o, out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// The reference's own candidate record and order (decoding.hpp:157-167) over one input's
+// candidates (decoding.hpp:192-204), first k written.
+int ref_beam_candidates(const double* lprobs, const double* live_lp, int lanes, int roots, int V, int k, int* parent,
+                        int* token, double* lp_sum) {
+    (void)lanes;
+    try {
+        std::vector<elattn::detail::Candidate> cands;
+        for (int i = 0; i < roots; ++i)
+            for (int tok = 0; tok < V; ++tok) {
+                const double v = lprobs[int64_t(i) * V + tok];
+                if (!std::isfinite(v)) continue;
+                cands.push_back({i, tok, live_lp[i] + v});
+            }
+        std::sort(cands.begin(), cands.end(), elattn::detail::candidate_better);
+        for (int r = 0; r < k; ++r) {
+            const bool have = size_t(r) < cands.size();
+            parent[r] = have ? cands[size_t(r)].parent : -1;
+            token[r] = have ? cands[size_t(r)].token : -1;
+            lp_sum[r] = have ? cands[size_t(r)].lp_sum : -std::numeric_limits<double>::infinity();
+        }
         return 0;
     } catch (const std::exception& e) {
         return status_of(e);

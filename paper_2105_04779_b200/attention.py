@@ -28,6 +28,7 @@ from .capi import DTYPE_BF16, DTYPE_F32, ParamError, ShapeError, StateError
 
 __all__ = [
     "DecoderStep",
+    "beam_candidates",
     "KvCache",
     "mixed_self_attention",
     "mixed_self_attention_batched",
@@ -537,3 +538,23 @@ def mixed_self_attention(q: np.ndarray, prefix_hidden: np.ndarray, gen_rows: np.
         cache.append(_as_device(gen[r:r + 1], layer.dtype))
     out = mixed_self_attention_batched(layer, _as_device(q, layer.dtype), _as_device(P[None], layer.dtype), cache, 1)
     return _to_host(out)
+
+
+def beam_candidates(lprobs, live_lp, lanes: int, k: int, roots: Optional[int] = None, stream=None):
+    """Device-side candidate selection of beam_search (decoding.hpp:186-230): lprobs
+    [B*lanes, V] fp32, live_lp [B*lanes] fp32 -> (parent, token, lp_sum), each [B, k], in
+    the reference's candidate_better order (decoding.hpp:163-167)."""
+    torch = _torch()
+    lprobs = lprobs.contiguous().float()
+    live_lp = live_lp.contiguous().float()
+    R, V = lprobs.shape
+    if R % lanes != 0 or live_lp.numel() != R:
+        raise ShapeError("beam_candidates: lprobs rows must be B * lanes and live_lp one per row")
+    B = R // lanes
+    parent = torch.empty(B, k, dtype=torch.int32, device=lprobs.device)
+    token = torch.empty_like(parent)
+    lp_sum = torch.empty(B, k, dtype=torch.float32, device=lprobs.device)
+    capi.check(capi.lib().elattn_gpu_beam_candidates(lprobs.data_ptr(), live_lp.data_ptr(), B, lanes,
+                                                     roots if roots is not None else lanes, V, k, parent.data_ptr(),
+                                                     token.data_ptr(), lp_sum.data_ptr(), _stream_ptr(stream)))
+    return parent, token, lp_sum

@@ -644,3 +644,14 @@ extern "C" size_t elattn_gpu_mixed_workspace_size(elattn_gpu_params_t p, int B, 
     const int64_t R = int64_t(B) * x;
     return step_workspace(p, R) + align256(size_t(R) * p->h * sizeof(float2));
 }
+
+// ---------------------------------------------------------------- beam-search candidates
+extern "C" int elattn_gpu_beam_candidates(const float* lprobs, const float* live_lp, int B, int lanes, int roots, int V,
+                                          int k, int* parent, int* token, float* lp_sum, elattn_stream_t stream) {
+    return guarded([&] {
+        ELA_REQUIRE(lprobs && live_lp && parent && token && lp_sum, ELATTN_ERR_PARAM, "beam_candidates: null buffer");
+        ELA_REQUIRE(B >= 1, ELATTN_ERR_SHAPE, "beam_candidates: B must be >= 1");
+        launch_beam_topk(lprobs, live_lp, B, lanes, roots, V, k, parent, token, lp_sum,
+                         reinterpret_cast<cudaStream_t>(stream));
+    });
+}

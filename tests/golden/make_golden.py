@@ -85,6 +85,26 @@ def ref_case_step(name, cfg, B, param_seed=1, data_seed=2):
     return {f"{name}.npz": f"reference layer step, {meta}"}
 
 
+def beam_inputs(seed=7):
+    """Beam candidate inputs: lanes 4, V 97, log-probs on a 1/4 grid (ties on purpose, exact
+    sums in fp32) with ~10% -inf (masked tokens); three inputs with roots 1, 4, 3."""
+    rng = np.random.default_rng(seed)
+    lp = np.round(rng.uniform(-6, 0, (3, 4, 97)) * 4) / 4
+    lp[rng.random(lp.shape) < 0.1] = -np.inf
+    live = np.round(rng.uniform(-4, 0, (3, 4)) * 4) / 4
+    return lp, live, (1, 4, 3), 10
+
+
+def ref_case_beam():
+    """decoding.hpp:186-205 candidate generation + candidate_better (:163-167) order."""
+    lp, live, roots, k = beam_inputs()
+    outs = [O.beam_candidates(lp[b], live[b], k, roots[b], impl="reference") for b in range(3)]
+    np.savez_compressed(OUT / "beam_candidates.npz", lprobs=lp, live=live, roots=np.array(roots), k=k,
+                        parent=np.stack([o[0] for o in outs]), token=np.stack([o[1] for o in outs]),
+                        lp_sum=np.stack([o[2] for o in outs]))
+    return {"beam_candidates.npz": "beam_search candidates, decoding.hpp:186-205 (order :163-167)"}
+
+
 def main():
     if not O.ref_available():
         raise SystemExit("oracle/_ref not built: run `make -C oracle` with /root/reference present")
@@ -96,6 +116,7 @@ def main():
     manifest.update(ref_case_build_query())
     manifest.update(ref_case_step("step_oracle_cfg", ORACLE_CFG, ORACLE_CFG["B"]))
     manifest.update(ref_case_step("step_bart_b2", BART_CFG, 2))
+    manifest.update(ref_case_beam())
     (OUT / "MANIFEST.json").write_text(json.dumps(manifest, indent=2) + "\n")
     print(json.dumps(manifest, indent=2))
 

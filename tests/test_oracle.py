@@ -176,3 +176,27 @@ def test_mixed_self_attention_reduces_to_el_attention_without_cache():
     a = O.mixed_self_attention(p, q, Hp, np.zeros((0, 8)))
     b = O.el_attention(p, q, Hp)
     assert np.max(np.abs(a - b)) <= 1e-12
+
+
+def test_beam_candidates_golden():
+    """Port of beam_search's candidate order vs the reference's own (decoding.hpp:163-205)."""
+    g = np.load(GOLD / "beam_candidates.npz")
+    k = int(g["k"])
+    for b in range(g["lprobs"].shape[0]):
+        par, tok, lps = O.beam_candidates(g["lprobs"][b], g["live"][b], k, int(g["roots"][b]))
+        assert np.array_equal(par, g["parent"][b]) and np.array_equal(tok, g["token"][b])
+        assert np.array_equal(lps, g["lp_sum"][b])
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built here")
+def test_beam_candidates_port_equals_reference_random():
+    rng = np.random.default_rng(11)
+    for _ in range(25):
+        lanes, V, k = int(rng.integers(1, 9)), int(rng.integers(1, 300)), int(rng.integers(1, 33))
+        roots = int(rng.integers(1, lanes + 1))
+        lp = np.round(rng.uniform(-8, 0, (lanes, V)) * 4) / 4
+        lp[rng.random((lanes, V)) < 0.2] = -np.inf
+        live = np.round(rng.uniform(-5, 0, lanes) * 4) / 4
+        a = O.beam_candidates(lp, live, k, roots)
+        b = O.beam_candidates(lp, live, k, roots, impl="reference")
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))

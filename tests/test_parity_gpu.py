@@ -355,3 +355,49 @@ def test_bf16_step_other_model_widths(gpu, h, d_m):
         assert layer.dev.decode_kernel_kind(x) == 1
         pr, Yr, Hr = oracle_inputs(p, Y, H, E.DTYPE_BF16)
         assert rel_err(out, O.el_layer_step(pr, Yr, Hr, x)) <= TOL[1], (h, d_m, x)
+
+
+# ---------------------------------------------------------------- beam-search candidates
+def _beam_check(E, lp, live, lanes, k, roots):
+    import torch
+
+    B, V = lp.shape[0] // lanes, lp.shape[1]
+    par, tok, lps = E.beam_candidates(torch.from_numpy(lp).float().cuda(), torch.from_numpy(live).float().cuda(),
+                                      lanes, k, roots)
+    torch.cuda.synchronize()
+    par, tok, lps = par.cpu().numpy(), tok.cpu().numpy(), lps.cpu().numpy()
+    for b in range(B):
+        ep, et, el = O.beam_candidates(lp[b * lanes:(b + 1) * lanes], live[b * lanes:(b + 1) * lanes], k, roots)
+        assert np.array_equal(par[b], ep) and np.array_equal(tok[b], et), (b, par[b], ep, tok[b], et)
+        assert np.array_equal(lps[b].astype(np.float64), el)
+
+
+def test_beam_candidates_golden_gpu(gpu):
+    """Device candidate selection vs the reference's own order (decoding.hpp:163-205)."""
+    import torch
+
+    E = gpu
+    g = np.load(GOLD / "beam_candidates.npz")
+    k = int(g["k"])
+    for b in range(g["lprobs"].shape[0]):
+        lp, live = g["lprobs"][b], g["live"][b]
+        par, tok, lps = E.beam_candidates(torch.from_numpy(lp).float().cuda(), torch.from_numpy(live).float().cuda(),
+                                          lp.shape[0], k, int(g["roots"][b]))
+        assert np.array_equal(par.cpu().numpy()[0], g["parent"][b])
+        assert np.array_equal(tok.cpu().numpy()[0], g["token"][b])
+        assert np.array_equal(lps.cpu().numpy()[0].astype(np.float64), g["lp_sum"][b])
+
+
+@pytest.mark.parametrize("lanes,V,k,roots", [(4, 50265, 8, 4), (4, 50265, 8, 1), (12, 50265, 24, 12),
+                                             (5, 1000, 32, 3), (1, 7, 10, 1), (8, 3, 32, 8)])
+def test_beam_candidates_vs_oracle(gpu, lanes, V, k, roots):
+    """BART-vocabulary candidate selection; values on a 1/8 grid (ties, exact fp32 sums),
+    masked (-inf) tokens, fewer finite candidates than k where V*roots is small."""
+    E = gpu
+    rng = np.random.default_rng(lanes * 1000 + V + k)
+    B = 3
+    lp = np.round(rng.uniform(-30, 0, (B * lanes, V)) * 8) / 8
+    lp[rng.random(lp.shape) < 0.05] = -np.inf
+    lp[0, :] = -np.inf  # a fully masked parent
+    live = np.round(rng.uniform(-10, 0, B * lanes) * 8) / 8
+    _beam_check(E, lp, live, lanes, k, roots)
