@@ -651,7 +651,12 @@ extern "C" int elattn_gpu_beam_candidates(const float* lprobs, const float* live
     return guarded([&] {
         ELA_REQUIRE(lprobs && live_lp && parent && token && lp_sum, ELATTN_ERR_PARAM, "beam_candidates: null buffer");
         ELA_REQUIRE(B >= 1, ELATTN_ERR_SHAPE, "beam_candidates: B must be >= 1");
-        launch_beam_topk(lprobs, live_lp, B, lanes, roots, V, k, parent, token, lp_sum,
-                         reinterpret_cast<cudaStream_t>(stream));
+        ELA_REQUIRE(k >= 1 && k <= 32 && V >= 1, ELATTN_ERR_SHAPE, "beam_candidates: 1 <= k <= 32, V >= 1");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const int splits = beam_splits(B, V);
+        const size_t part_bytes = sizeof(uint64_t) * size_t(B) * splits * k;
+        Scratch ws(nullptr, 0, align256(part_bytes), st);
+        auto* part = static_cast<uint64_t*>(ws.take(part_bytes));
+        launch_beam_topk(lprobs, live_lp, B, lanes, roots, V, k, part, splits, parent, token, lp_sum, st);
     });
 }

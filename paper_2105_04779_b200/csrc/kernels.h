@@ -58,8 +58,9 @@ void launch_mixed_combine(int dtype, const void* Q, const float2* stats, void* V
                           cudaStream_t st);
 
 // Beam-search candidate selection (beam.cu).
+int beam_splits(int B, int V);
 void launch_beam_topk(const float* lprobs, const float* live_lp, int B, int lanes, int roots, int V, int k,
-                      int* parent, int* token, float* lp_sum, cudaStream_t st);
+                      uint64_t* part, int splits, int* parent, int* token, float* lp_sum, cudaStream_t st);
 
 // Per-lane hidden-state caches (lane_cache.cu).
 void launch_cache_append(void* cache, const void* Y, int* len, int lanes, int n_max, int d_m, int dtype,
