@@ -1,6 +1,7 @@
 // blas_lt.cu — the two PLAIN projection GEMMs of a layer step (Q = Y.W_Q + b_Q and
-// out = V.W_O + b_O, attention.hpp:205 / :283-288 with el_bias_terms :221-231) through
-// cuBLASLt with a fused bias epilogue.  These are ordinary dense GEMMs (M = B*x rows,
+// out = V.W_O + b_O, attention.hpp:205 / :283-288 with el_bias_terms :221-231) and the
+// per-head V projection (strided batch over heads, :286) through cuBLASLt with a fused
+// bias epilogue.  These are ordinary dense GEMMs (M = B*x rows,
 // N = K = 1024 at BART shapes, 0.5 waves of 128x128 tiles on 148 SMs) where the library
 // is faster than our persistent kernel; the EL-specific GEMMs (head-strided q' expansion,
 // per-head V projection) and the fused decode stay hand-written (tc_gemm.cu,
@@ -41,7 +42,8 @@ struct Plan {
 struct LtState {
     std::mutex mu;
     cublasLtHandle_t handle = nullptr;
-    std::map<std::tuple<int, int, int, int64_t, int64_t, int64_t, bool>, Plan> plans;
+    std::map<std::tuple<int, int, int, int64_t, int64_t, int64_t, bool, int, int64_t, int64_t, int64_t, int64_t>, Plan>
+        plans;
     std::unordered_map<cudaStream_t, void*> workspace;  // one per stream (kernels use it asynchronously)
 };
 
@@ -52,7 +54,7 @@ LtState& state() {
 
 Plan& plan_for(LtState& S, const GemmArgs& g) {
     const bool bias = g.bias != nullptr;
-    auto key = std::make_tuple(g.M, g.N, g.K, g.lda, g.ldb, g.ldc, bias);
+    auto key = std::make_tuple(g.M, g.N, g.K, g.lda, g.ldb, g.ldc, bias, g.Z, g.sAz, g.sBz, g.sCz, g.sbz);
     auto it = S.plans.find(key);
     if (it != S.plans.end()) return it->second;
     Plan p;
@@ -71,6 +73,19 @@ Plan& plan_for(LtState& S, const GemmArgs& g) {
     ELA_CHECK_LT(cublasLtMatrixLayoutCreate(&p.a, CUDA_R_16BF, uint64_t(g.K), uint64_t(g.N), g.ldb));
     ELA_CHECK_LT(cublasLtMatrixLayoutCreate(&p.b, CUDA_R_16BF, uint64_t(g.K), uint64_t(g.M), g.lda));
     ELA_CHECK_LT(cublasLtMatrixLayoutCreate(&p.c, CUDA_R_16BF, uint64_t(g.N), uint64_t(g.M), g.ldc));
+    if (g.Z > 1) {  // strided batch: matrix z at base + z * stride (elements)
+        const int32_t cnt = g.Z;
+        const int64_t sa = g.sBz, sb = g.sAz, sc = g.sCz;
+        for (auto [lay, stride] : {std::pair{p.a, sa}, std::pair{p.b, sb}, std::pair{p.c, sc}}) {
+            ELA_CHECK_LT(cublasLtMatrixLayoutSetAttribute(lay, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &cnt, sizeof(cnt)));
+            ELA_CHECK_LT(cublasLtMatrixLayoutSetAttribute(lay, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &stride,
+                                                          sizeof(stride)));
+        }
+        if (bias) {
+            const int64_t bs = g.sbz;
+            ELA_CHECK_LT(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_BIAS_BATCH_STRIDE, &bs, sizeof(bs)));
+        }
+    }
     cublasLtMatmulPreference_t pref;
     ELA_CHECK_LT(cublasLtMatmulPreferenceCreate(&pref));
     const size_t ws = kWorkspace;
@@ -87,7 +102,7 @@ Plan& plan_for(LtState& S, const GemmArgs& g) {
 }  // namespace
 
 bool lt_gemm_supported(const GemmArgs& g) {
-    return g.Z == 1 && (g.bias == nullptr || g.bias16 != nullptr) && g.M > 0 && g.N > 0 && g.K > 0 && g.lda % 8 == 0 && g.ldb % 8 == 0 && g.ldc % 8 == 0;
+    return g.Z >= 1 && (g.bias == nullptr || g.bias16 != nullptr) && g.M > 0 && g.N > 0 && g.K > 0 && g.lda % 8 == 0 && g.ldb % 8 == 0 && g.ldc % 8 == 0;
 }
 
 void launch_lt_gemm(const GemmArgs& g, cudaStream_t st) {

@@ -28,7 +28,8 @@ struct elattn_gpu_params_s {
     float* bk = nullptr;  // [h*d_k]
     float* bv = nullptr;  // [h*d_k] (zero when include_value_bias == 0)
     float* bo = nullptr;  // [d_m]
-    void* bq16 = nullptr;  // bf16 copies of bq / bo for the cuBLASLt bias epilogue (bf16 path only)
+    void* bq16 = nullptr;  // bf16 copies of bq / bv / bo for the cuBLASLt bias epilogue (bf16 path only)
+    void* bv16 = nullptr;
     void* bo16 = nullptr;
 };
 
@@ -95,7 +96,7 @@ float* upload_f32(const std::vector<double>& v) {
 void free_params(elattn_gpu_params_s* p) {
     if (!p) return;
     for (void* ptr : {p->WqT, p->WkT, p->Wk, p->WvT, p->WoT, (void*)p->bq, (void*)p->bk, (void*)p->bv,
-                      (void*)p->bo, p->bq16, p->bo16})
+                      (void*)p->bo, p->bq16, p->bv16, p->bo16})
         if (ptr) cudaFree(ptr);
     delete p;
 }
@@ -149,6 +150,18 @@ bool dense_via_lt() {
     return v;
 }
 
+// The per-head V projection (K = d_m, N = d_k: 160 tiles of 128 x 64 at B = 320, 1.1 waves
+// on 148 SMs for our persistent kernel) goes to cuBLASLt's strided-batched GEMM, which
+// writes V_i straight into the head-concatenated rows; ELATTN_VPROJ_GEMM=tc keeps it on the
+// tcgen05 kernel.
+bool vproj_via_lt() {
+    static const bool v = [] {
+        const char* e = getenv("ELATTN_VPROJ_GEMM");
+        return !(e && std::string(e) == "tc");
+    }();
+    return v;
+}
+
 void gemm(const elattn_gpu_params_s* p, const GemmArgs& g, cudaStream_t st) {
     if (p->dtype == ELATTN_DTYPE_BF16 && g.Z == 1 && dense_via_lt() && lt_gemm_supported(g))
         launch_lt_gemm(g, st);
@@ -183,9 +196,12 @@ void v_projection(const elattn_gpu_params_s* p, const void* C, int64_t R, void* 
     a.A = C, a.lda = int64_t(h) * d_m, a.sAz = d_m;
     a.B = p->WvT, a.ldb = d_m, a.sBz = int64_t(d_k) * d_m;
     a.C = V, a.ldc = hk, a.sCz = d_k;
-    a.bias = p->bv, a.sbz = d_k;
+    a.bias = p->bv, a.sbz = d_k, a.bias16 = p->bv16;
     a.M = int(R), a.N = d_k, a.K = d_m, a.Z = h, a.alpha = 1.f;
-    gemm(p, a, st);
+    if (p->dtype == ELATTN_DTYPE_BF16 && vproj_via_lt() && lt_gemm_supported(a))
+        launch_lt_gemm(a, st);
+    else
+        gemm(p, a, st);
 }
 
 void o_projection(const elattn_gpu_params_s* p, const void* V, int64_t R, void* out, cudaStream_t st) {
@@ -284,6 +300,7 @@ int elattn_gpu_params_create(int h, int d_m, int d_k, int dtype, int include_key
         p->bo = upload_f32(vbo);
         if (dtype == ELATTN_DTYPE_BF16) {
             p->bq16 = upload(vbq, ELATTN_DTYPE_BF16);
+            p->bv16 = upload(vbv, ELATTN_DTYPE_BF16);
             p->bo16 = upload(vbo, ELATTN_DTYPE_BF16);
         }
         *out = p.release();

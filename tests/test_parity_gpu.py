@@ -218,7 +218,7 @@ def test_decoder_step_graph_matches_layer_chain(gpu, npi_mode):
     H = (torch.rand((B, n, c["d_m"]), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
     npi = torch.tensor([200, 17, 130], dtype=torch.int32, device="cuda") if npi_mode else None
     dec = E.DecoderStep(layers, H, B, c["x"], npi)
-    assert dec.kernels_per_run >= 3 * L  # q' GEMM, decode, V GEMM per layer (+ merge if split)
+    assert dec.kernels_per_run >= 2 * L  # q' GEMM and decode per layer (+ merge if split); Q/V/out on cuBLASLt
     for it in range(2):
         Y = (torch.rand((B * c["x"], c["d_m"]), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
         got = dec.run(Y).clone()

@@ -88,3 +88,6 @@ for name, (A, Bm) in {"cublas Q=Y.Wq": (Y, WqT), "cublas out=V.Wo": (V, WoT)}.it
 qh = Q.view(R, h, d_k).transpose(0, 1)  # [h, R, d_k]
 us = graph_time(lambda: torch.bmm(qh, Wk.transpose(1, 2)), a.reps)
 print(json.dumps({"gemm": "cublas q' (bmm, [h][R][d_m] layout)", "us": round(us, 2)}))
+ch = ctx.view(R, h, d_m).transpose(0, 1)  # [h, R, d_m]
+us = graph_time(lambda: torch.bmm(ch, WvT.transpose(1, 2)), a.reps)
+print(json.dumps({"gemm": "cublas V (bmm, [h][R][d_k] layout)", "us": round(us, 2)}))
