@@ -213,10 +213,14 @@ size_t elattn_gpu_mixed_workspace_size(elattn_gpu_params_t params, int B, int x)
  * + lprobs[(b*lanes+i)*V + t], non-finite log-probs skipped; the k best (k <= 32) in the
  * reference's candidate_better order (decoding.hpp:163-167: higher lp_sum, then smaller
  * token, then smaller parent) -> parent/token/lp_sum [B][k] (parent -1 when fewer than k).
- * roots = 1 on the first step (all lanes identical), = lanes afterwards.
+ * roots = 1 on the first step (all lanes identical), = lanes afterwards.  penalty (may be
+ * NULL): device float[B][V] >= 0 subtracted from every finite log-prob before the sum —
+ * diverse_beam_search's `v -= strength * step_token_counts[tok]` (decoding.hpp:312-316),
+ * called once per group with that group's contiguous lanes.
  */
-int elattn_gpu_beam_candidates(const float* lprobs, const float* live_lp, int B, int lanes, int roots, int V, int k,
-                               int* parent, int* token, float* lp_sum, elattn_stream_t stream);
+int elattn_gpu_beam_candidates(const float* lprobs, const float* live_lp, const float* penalty, int B, int lanes,
+                               int roots, int V, int k, int* parent, int* token, float* lp_sum,
+                               elattn_stream_t stream);
 
 /* Device-kernel launches issued by this thread since the last reset (for bench
  * accounting of gpu_launches). */

@@ -506,17 +506,20 @@ static int cand_cmp(const void* pa, const void* pb) {
 
 /* decoding.hpp:192-205: for parents i < roots, every finite lprobs[i][tok] gives
  * (i, tok, live_lp[i] + v); sorted by candidate_better; the first k written (parent -1
- * beyond the candidate count).  One input; lprobs [lanes][V]. */
-int orc_beam_candidates(const double* lprobs, const double* live_lp, int lanes, int roots, int V, int k,
-                        int* parent, int* token, double* lp_sum) {
+ * beyond the candidate count).  One input; lprobs [lanes][V].  penalty (may be NULL):
+ * [V], subtracted from v after the finiteness test (diverse_beam_search,
+ * decoding.hpp:312-316: v -= strength * step_token_counts[tok]). */
+int orc_beam_candidates(const double* lprobs, const double* live_lp, const double* penalty, int lanes, int roots,
+                        int V, int k, int* parent, int* token, double* lp_sum) {
     if (roots < 1 || roots > lanes || V < 1 || k < 1) return ORC_SHAPE;
     orc_cand* c = (orc_cand*)malloc(sizeof(orc_cand) * (size_t)roots * (size_t)V);
     if (!c) return ORC_PARAM;
     size_t n = 0;
     for (int i = 0; i < roots; ++i)
         for (int t = 0; t < V; ++t) {
-            const double v = lprobs[(size_t)i * V + t];
+            double v = lprobs[(size_t)i * V + t];
             if (!isfinite(v)) continue;
+            if (penalty) v -= penalty[t];
             c[n].parent = i, c[n].token = t, c[n].lp_sum = live_lp[i] + v;
             ++n;
         }

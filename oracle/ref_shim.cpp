@@ -265,16 +265,18 @@ int ref_mixed_self_attention(REF_PARAMS_ARGS, const double* q, const double* Hp,
 }
 
 // The reference's own candidate record and order (decoding.hpp:157-167) over one input's
-// candidates (decoding.hpp:192-204), first k written.
-int ref_beam_candidates(const double* lprobs, const double* live_lp, int lanes, int roots, int V, int k, int* parent,
-                        int* token, double* lp_sum) {
+// candidates (decoding.hpp:192-204; with penalty, diverse_beam_search's :312-316), first k
+// written.
+int ref_beam_candidates(const double* lprobs, const double* live_lp, const double* penalty, int lanes, int roots,
+                        int V, int k, int* parent, int* token, double* lp_sum) {
     (void)lanes;
     try {
         std::vector<elattn::detail::Candidate> cands;
         for (int i = 0; i < roots; ++i)
             for (int tok = 0; tok < V; ++tok) {
-                const double v = lprobs[int64_t(i) * V + tok];
+                double v = lprobs[int64_t(i) * V + tok];
                 if (!std::isfinite(v)) continue;
+                if (penalty) v -= penalty[tok];
                 cands.push_back({i, tok, live_lp[i] + v});
             }
         std::sort(cands.begin(), cands.end(), elattn::detail::candidate_better);

@@ -540,10 +540,12 @@ def mixed_self_attention(q: np.ndarray, prefix_hidden: np.ndarray, gen_rows: np.
     return _to_host(out)
 
 
-def beam_candidates(lprobs, live_lp, lanes: int, k: int, roots: Optional[int] = None, stream=None):
+def beam_candidates(lprobs, live_lp, lanes: int, k: int, roots: Optional[int] = None, stream=None, penalty=None):
     """Device-side candidate selection of beam_search (decoding.hpp:186-230): lprobs
     [B*lanes, V] fp32, live_lp [B*lanes] fp32 -> (parent, token, lp_sum), each [B, k], in
-    the reference's candidate_better order (decoding.hpp:163-167)."""
+    the reference's candidate_better order (decoding.hpp:163-167).  penalty: optional
+    [B, V] fp32 >= 0 subtracted from each finite log-prob (diverse beam search,
+    decoding.hpp:312-316)."""
     torch = _torch()
     lprobs = lprobs.contiguous().float()
     live_lp = live_lp.contiguous().float()
@@ -551,10 +553,15 @@ def beam_candidates(lprobs, live_lp, lanes: int, k: int, roots: Optional[int] = 
     if R % lanes != 0 or live_lp.numel() != R:
         raise ShapeError("beam_candidates: lprobs rows must be B * lanes and live_lp one per row")
     B = R // lanes
+    if penalty is not None:
+        penalty = penalty.contiguous().float()
+        if penalty.numel() != B * V:
+            raise ShapeError("beam_candidates: penalty must be [B, V]")
     parent = torch.empty(B, k, dtype=torch.int32, device=lprobs.device)
     token = torch.empty_like(parent)
     lp_sum = torch.empty(B, k, dtype=torch.float32, device=lprobs.device)
-    capi.check(capi.lib().elattn_gpu_beam_candidates(lprobs.data_ptr(), live_lp.data_ptr(), B, lanes,
+    capi.check(capi.lib().elattn_gpu_beam_candidates(lprobs.data_ptr(), live_lp.data_ptr(),
+                                                     penalty.data_ptr() if penalty is not None else None, B, lanes,
                                                      roots if roots is not None else lanes, V, k, parent.data_ptr(),
                                                      token.data_ptr(), lp_sum.data_ptr(), _stream_ptr(stream)))
     return parent, token, lp_sum

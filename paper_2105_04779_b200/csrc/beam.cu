@@ -2,8 +2,11 @@
 // candidate generation + ordering of beam_search (decoding.hpp:186-230).  For input b,
 // every finite (parent i < roots, token t) gives lp_sum = live_lp[b][i] + lprobs[b][i][t];
 // the k best are returned in the reference's candidate_better order (decoding.hpp:163-167:
-// higher lp_sum first, then smaller token, then smaller parent).  EOS handling, the
-// finished pool and termination stay with the caller (the model's search loop).
+// higher lp_sum first, then smaller token, then smaller parent).  An optional per-input
+// token penalty (>= 0, so the float4 pre-filter on the raw log-probs stays a necessary
+// condition) is subtracted from each finite log-prob first: diverse beam search's
+// `v -= strength * step_token_counts[tok]` (decoding.hpp:312-316), one call per group.
+// EOS handling, the finished pool and termination stay with the caller (the search loop).
 //
 // Candidates are ranked by one 64-bit key (smaller = better): the order-preserving bits of
 // lp_sum inverted, then token, then parent.  Phase 1: CTAs (column split, input) scan their
@@ -129,7 +132,8 @@ __device__ __forceinline__ void block_merge(WarpTopK& wl, uint64_t* stage) {
 // software-pipelined one batch ahead.
 __global__ void __launch_bounds__(kBeamThreads) beam_scan_kernel(const float* __restrict__ lprobs,
                                                                  const float* __restrict__ live_lp, int lanes, int roots,
-                                                                 int V, int k, int cv, uint64_t* __restrict__ part) {
+                                                                 int V, int k, int cv, uint64_t* __restrict__ part,
+                                                                 const float* __restrict__ penalty) {
     __shared__ uint64_t stage[kBeamWarps * 32];
     const int split = blockIdx.x, b = blockIdx.y, splits = gridDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -166,7 +170,8 @@ __global__ void __launch_bounds__(kBeamThreads) beam_scan_kernel(const float* __
             if (split == 0 && lane < head && lane < V) t = lane;
             if (split == splits - 1 && lane >= 4 && lane - 4 < V - tail0 && tail0 + lane - 4 >= head) t = tail0 + lane - 4;
             const float v = t >= 0 ? row[t] : -INFINITY;
-            wl.offer_score(base + v, v, t < 0 ? 0 : t, i);
+            const float pv = penalty != nullptr && t >= 0 ? penalty[int64_t(b) * V + t] : 0.f;
+            wl.offer_score(base + (v - pv), v, t < 0 ? 0 : t, i);
         }
     }
     auto process = [&](int j, const float4 (&cur)[kUnroll]) {
@@ -196,7 +201,8 @@ __global__ void __launch_bounds__(kBeamThreads) beam_scan_kernel(const float* __
 #pragma unroll 1
             for (int e = 0; e < 4; ++e) {
                 const float v = e == 0 ? x.x : (e == 1 ? x.y : (e == 2 ? x.z : x.w));
-                wl.offer_score(base + v, v, t + e, i);
+                const float pv = penalty != nullptr ? penalty[int64_t(b) * V + t + e] : 0.f;
+                wl.offer_score(base + (v - pv), v, t + e, i);
             }
         }
     };
@@ -256,7 +262,8 @@ int beam_splits(int B, int V) {
     return want < 1 ? 1 : (want > cap ? (cap < 1 ? 1 : cap) : want);
 }
 
-void launch_beam_topk(const float* lprobs, const float* live_lp, int B, int lanes, int roots, int V, int k,
+void launch_beam_topk(const float* lprobs, const float* live_lp, const float* penalty, int B, int lanes, int roots,
+                      int V, int k,
                       uint64_t* part, int splits, int* parent, int* token, float* lp_sum,
                       cudaStream_t st) {
     ELA_REQUIRE(k >= 1 && k <= kMaxK, ELATTN_ERR_UNSUPPORTED, "beam_candidates: k must be in [1, 32]");
@@ -264,7 +271,8 @@ void launch_beam_topk(const float* lprobs, const float* live_lp, int B, int lane
                 "beam_candidates: 1 <= roots <= lanes <= 256");
     ELA_REQUIRE(V >= 1 && V < (1 << 24), ELATTN_ERR_SHAPE, "beam_candidates: vocabulary must be < 2^24");
     const int cv = ((V + 3) / 4 + splits - 1) / splits;
-    beam_scan_kernel<<<dim3(splits, B), kBeamThreads, 0, st>>>(lprobs, live_lp, lanes, roots, V, k, cv, part);
+    beam_scan_kernel<<<dim3(splits, B), kBeamThreads, 0, st>>>(lprobs, live_lp, lanes, roots, V, k, cv, part,
+                                                               penalty);
     ELA_CHECK_LAUNCH();
     beam_merge_kernel<<<B, 32, 0, st>>>(part, splits, k, parent, token, lp_sum);
     ELA_CHECK_LAUNCH();

@@ -186,7 +186,14 @@ void query_expansion(const elattn_gpu_params_s* p, const void* Y, int64_t R, voi
     b.C = qp, b.ldc = int64_t(h) * d_m, b.sCz = d_m;          // row r*h + i
     b.M = int(R), b.N = d_m, b.K = d_k, b.Z = h, b.alpha = 1.f;
     (void)e;
-    gemm(p, b, st);
+    static const bool qexp_lt = [] {
+        const char* v = getenv("ELATTN_QEXP_GEMM");
+        return v && std::string(v) == "lt";
+    }();
+    if (qexp_lt && p->dtype == ELATTN_DTYPE_BF16 && lt_gemm_supported(b))
+        launch_lt_gemm(b, st);
+    else
+        gemm(p, b, st);
 }
 
 // (3a) V_{r,i} = C_{r*h+i}.W_V,i + b_V,i ; (3b) out = V.W_O + b_O   (attention.hpp:283-288)
@@ -663,8 +670,9 @@ extern "C" size_t elattn_gpu_mixed_workspace_size(elattn_gpu_params_t p, int B, 
 }
 
 // ---------------------------------------------------------------- beam-search candidates
-extern "C" int elattn_gpu_beam_candidates(const float* lprobs, const float* live_lp, int B, int lanes, int roots, int V,
-                                          int k, int* parent, int* token, float* lp_sum, elattn_stream_t stream) {
+extern "C" int elattn_gpu_beam_candidates(const float* lprobs, const float* live_lp, const float* penalty, int B,
+                                          int lanes, int roots, int V, int k, int* parent, int* token, float* lp_sum,
+                                          elattn_stream_t stream) {
     return guarded([&] {
         ELA_REQUIRE(lprobs && live_lp && parent && token && lp_sum, ELATTN_ERR_PARAM, "beam_candidates: null buffer");
         ELA_REQUIRE(B >= 1, ELATTN_ERR_SHAPE, "beam_candidates: B must be >= 1");
@@ -674,6 +682,6 @@ extern "C" int elattn_gpu_beam_candidates(const float* lprobs, const float* live
         const size_t part_bytes = sizeof(uint64_t) * size_t(B) * splits * k;
         Scratch ws(nullptr, 0, align256(part_bytes), st);
         auto* part = static_cast<uint64_t*>(ws.take(part_bytes));
-        launch_beam_topk(lprobs, live_lp, B, lanes, roots, V, k, part, splits, parent, token, lp_sum, st);
+        launch_beam_topk(lprobs, live_lp, penalty, B, lanes, roots, V, k, part, splits, parent, token, lp_sum, st);
     });
 }

@@ -59,7 +59,8 @@ void launch_mixed_combine(int dtype, const void* Q, const float2* stats, void* V
 
 // Beam-search candidate selection (beam.cu).
 int beam_splits(int B, int V);
-void launch_beam_topk(const float* lprobs, const float* live_lp, int B, int lanes, int roots, int V, int k,
+void launch_beam_topk(const float* lprobs, const float* live_lp, const float* penalty, int B, int lanes, int roots,
+                      int V, int k,
                       uint64_t* part, int splits, int* parent, int* token, float* lp_sum, cudaStream_t st);
 
 // Per-lane hidden-state caches (lane_cache.cu).

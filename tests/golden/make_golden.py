@@ -99,10 +99,16 @@ def ref_case_beam():
     """decoding.hpp:186-205 candidate generation + candidate_better (:163-167) order."""
     lp, live, roots, k = beam_inputs()
     outs = [O.beam_candidates(lp[b], live[b], k, roots[b], impl="reference") for b in range(3)]
+    # diverse-beam token penalties (strength 0.5 x counts 0..2, decoding.hpp:312-316)
+    pen = 0.5 * np.random.default_rng(8).integers(0, 3, (3, lp.shape[2])).astype(np.float64)
+    outp = [O.beam_candidates(lp[b], live[b], k, roots[b], impl="reference", penalty=pen[b]) for b in range(3)]
     np.savez_compressed(OUT / "beam_candidates.npz", lprobs=lp, live=live, roots=np.array(roots), k=k,
                         parent=np.stack([o[0] for o in outs]), token=np.stack([o[1] for o in outs]),
-                        lp_sum=np.stack([o[2] for o in outs]))
-    return {"beam_candidates.npz": "beam_search candidates, decoding.hpp:186-205 (order :163-167)"}
+                        lp_sum=np.stack([o[2] for o in outs]), penalty=pen,
+                        parent_pen=np.stack([o[0] for o in outp]), token_pen=np.stack([o[1] for o in outp]),
+                        lp_sum_pen=np.stack([o[2] for o in outp]))
+    return {"beam_candidates.npz": "beam_search candidates, decoding.hpp:186-205 (order :163-167); "
+                                   "*_pen: with diverse-beam token penalties (:312-316)"}
 
 
 def main():

@@ -186,6 +186,9 @@ def test_beam_candidates_golden():
         par, tok, lps = O.beam_candidates(g["lprobs"][b], g["live"][b], k, int(g["roots"][b]))
         assert np.array_equal(par, g["parent"][b]) and np.array_equal(tok, g["token"][b])
         assert np.array_equal(lps, g["lp_sum"][b])
+        par, tok, lps = O.beam_candidates(g["lprobs"][b], g["live"][b], k, int(g["roots"][b]), penalty=g["penalty"][b])
+        assert np.array_equal(par, g["parent_pen"][b]) and np.array_equal(tok, g["token_pen"][b])
+        assert np.array_equal(lps, g["lp_sum_pen"][b])
 
 
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built here")
@@ -197,6 +200,7 @@ def test_beam_candidates_port_equals_reference_random():
         lp = np.round(rng.uniform(-8, 0, (lanes, V)) * 4) / 4
         lp[rng.random((lanes, V)) < 0.2] = -np.inf
         live = np.round(rng.uniform(-5, 0, lanes) * 4) / 4
-        a = O.beam_candidates(lp, live, k, roots)
-        b = O.beam_candidates(lp, live, k, roots, impl="reference")
+        pen = 0.25 * rng.integers(0, 4, V) if rng.random() < 0.5 else None
+        a = O.beam_candidates(lp, live, k, roots, penalty=pen)
+        b = O.beam_candidates(lp, live, k, roots, impl="reference", penalty=pen)
         assert all(np.array_equal(x, y) for x, y in zip(a, b))

@@ -358,16 +358,18 @@ def test_bf16_step_other_model_widths(gpu, h, d_m):
 
 
 # ---------------------------------------------------------------- beam-search candidates
-def _beam_check(E, lp, live, lanes, k, roots):
+def _beam_check(E, lp, live, lanes, k, roots, pen=None):
     import torch
 
     B, V = lp.shape[0] // lanes, lp.shape[1]
     par, tok, lps = E.beam_candidates(torch.from_numpy(lp).float().cuda(), torch.from_numpy(live).float().cuda(),
-                                      lanes, k, roots)
+                                      lanes, k, roots,
+                                      penalty=torch.from_numpy(pen).float().cuda() if pen is not None else None)
     torch.cuda.synchronize()
     par, tok, lps = par.cpu().numpy(), tok.cpu().numpy(), lps.cpu().numpy()
     for b in range(B):
-        ep, et, el = O.beam_candidates(lp[b * lanes:(b + 1) * lanes], live[b * lanes:(b + 1) * lanes], k, roots)
+        ep, et, el = O.beam_candidates(lp[b * lanes:(b + 1) * lanes], live[b * lanes:(b + 1) * lanes], k, roots,
+                                       penalty=pen[b] if pen is not None else None)
         assert np.array_equal(par[b], ep) and np.array_equal(tok[b], et), (b, par[b], ep, tok[b], et)
         assert np.array_equal(lps[b].astype(np.float64), el)
 
@@ -386,6 +388,12 @@ def test_beam_candidates_golden_gpu(gpu):
         assert np.array_equal(par.cpu().numpy()[0], g["parent"][b])
         assert np.array_equal(tok.cpu().numpy()[0], g["token"][b])
         assert np.array_equal(lps.cpu().numpy()[0].astype(np.float64), g["lp_sum"][b])
+        par, tok, lps = E.beam_candidates(torch.from_numpy(lp).float().cuda(), torch.from_numpy(live).float().cuda(),
+                                          lp.shape[0], k, int(g["roots"][b]),
+                                          penalty=torch.from_numpy(g["penalty"][b][None]).float().cuda())
+        assert np.array_equal(par.cpu().numpy()[0], g["parent_pen"][b])
+        assert np.array_equal(tok.cpu().numpy()[0], g["token_pen"][b])
+        assert np.array_equal(lps.cpu().numpy()[0].astype(np.float64), g["lp_sum_pen"][b])
 
 
 @pytest.mark.parametrize("lanes,V,k,roots", [(4, 50265, 8, 4), (4, 50265, 8, 1), (12, 50265, 24, 12),
@@ -401,3 +409,16 @@ def test_beam_candidates_vs_oracle(gpu, lanes, V, k, roots):
     lp[0, :] = -np.inf  # a fully masked parent
     live = np.round(rng.uniform(-10, 0, B * lanes) * 8) / 8
     _beam_check(E, lp, live, lanes, k, roots)
+
+
+def test_beam_candidates_diverse_penalty(gpu):
+    """Diverse beam search: per-input token penalties strength x counts subtracted before the
+    sum (decoding.hpp:312-316), BART vocabulary, ties on the 1/8 grid."""
+    E = gpu
+    rng = np.random.default_rng(77)
+    B, lanes, V, k = 4, 3, 50265, 6
+    lp = np.round(rng.uniform(-20, 0, (B * lanes, V)) * 8) / 8
+    lp[rng.random(lp.shape) < 0.05] = -np.inf
+    live = np.round(rng.uniform(-6, 0, B * lanes) * 8) / 8
+    pen = 0.5 * rng.integers(0, 3, (B, V)).astype(np.float64)
+    _beam_check(E, lp, live, lanes, k, lanes, pen)
