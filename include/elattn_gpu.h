@@ -186,6 +186,14 @@ int elattn_gpu_cache_append(void* cache, const void* Y, int* lengths, int lanes,
 int elattn_gpu_cache_gather(const void* src, const int* src_lengths, void* dst, int* dst_lengths,
                             const int* parent, int lanes_in, int lanes_out, int n_max, int d_m, int dtype,
                             int rows_hint, elattn_stream_t stream);
+/*
+ * Whole-lane gather of fixed-size per-lane state (e.g. the K/V caches of the mixed form,
+ * [R][h][t_max][d_k]): dst lane i = src lane parent[i], bytes_per_lane a multiple of 16;
+ * an out-of-range parent fills the lane with NaN bytes.  gather_lanes / keep_lanes /
+ * permute_lanes (model.hpp:291-325) are this with the parent list they imply.
+ */
+int elattn_gpu_lane_gather(const void* src, void* dst, const int* parent, int lanes_in, int lanes_out,
+                           int64_t bytes_per_lane, elattn_stream_t stream);
 
 /*
  * Decoder-only MIXED self-attention.  Replaces

@@ -29,6 +29,9 @@ from .capi import DTYPE_BF16, DTYPE_F32, ParamError, ShapeError, StateError
 __all__ = [
     "DecoderStep",
     "beam_candidates",
+    "gather_lane_indices",
+    "keep_lane_indices",
+    "permute_lane_indices",
     "KvCache",
     "mixed_self_attention",
     "mixed_self_attention_batched",
@@ -350,6 +353,47 @@ class DecoderStep:
             self.handle = None
 
 
+def gather_lane_indices(parent, lanes: int) -> np.ndarray:
+    """DecoderState::gather_lanes checks (model.hpp:291-302): new lane i copies old lane
+    parent[i]; parents may repeat and the lane count may change."""
+    idx = np.asarray(parent, dtype=np.int64).reshape(-1)
+    if idx.size == 0:
+        raise StateError("gather_lanes: all lanes dropped")
+    if (idx < 0).any() or (idx >= lanes).any():
+        raise ParamError("gather_lanes: lane index out of range")
+    return idx.astype(np.int32)
+
+
+def keep_lane_indices(keep, lanes: int) -> np.ndarray:
+    """DecoderState::keep_lanes (model.hpp:315-325) as a gather list."""
+    mask = np.asarray(keep, dtype=bool).reshape(-1)
+    if mask.size != lanes:
+        raise ParamError("keep_lanes: mask size must equal beam count")
+    idx = np.nonzero(mask)[0].astype(np.int32)
+    if idx.size == 0:
+        raise StateError("keep_lanes: all lanes dropped")
+    return idx
+
+
+def permute_lane_indices(perm, lanes: int) -> np.ndarray:
+    """DecoderState::permute_lanes (model.hpp:304-314) as a gather list."""
+    idx = np.asarray(perm, dtype=np.int64).reshape(-1)
+    if idx.size != lanes:
+        raise ParamError("permute_lanes: permutation size must equal beam count")
+    if (idx < 0).any() or (idx >= lanes).any() or np.unique(idx).size != lanes:
+        raise ParamError("permute_lanes: not a valid permutation")
+    return idx.astype(np.int32)
+
+
+def _parent_tensor(parent, lanes: int):
+    """Host lists are validated like the reference; device int32 tensors are trusted (an
+    out-of-range parent then gives loud NaN lanes)."""
+    torch = _torch()
+    if isinstance(parent, torch.Tensor) and parent.is_cuda:
+        return parent.to(torch.int32).contiguous()
+    return torch.from_numpy(gather_lane_indices(parent, lanes)).cuda()
+
+
 class HiddenStateCache:
     """Per-lane hidden-state caches for decoder-only EL self-attention (BASELINE config 4,
     the "hidden-state-only cache": each lane attends over its own history of layer inputs,
@@ -381,24 +425,34 @@ class HiddenStateCache:
         return layer_params.step(Y, self.cache[layer], self.lengths[layer], out=out, stream=stream)
 
     def gather(self, parent, rows_hint: Optional[int] = None, stream=None):
-        """New lane i = old lane parent[i] in every layer (beam reorder / expansion with the
-        same lane count)."""
+        """New lane i = old lane parent[i] in every layer (DecoderState::gather_lanes,
+        model.hpp:291-302: beam reorder / expansion; the lane count may change)."""
         torch = _torch()
-        parent = torch.as_tensor(parent, dtype=torch.int32).cuda().contiguous()
-        if parent.numel() != self.lanes:
-            raise ShapeError("HiddenStateCache.gather: one parent per lane")
-        if self._spare is None:
-            self._spare = (torch.empty_like(self.cache), torch.empty_like(self.lengths))
+        parent = _parent_tensor(parent, self.lanes)
+        lanes_out = parent.numel()
+        if self._spare is None or self._spare[0].shape[1] != lanes_out:
+            L = self.cache.shape[0]
+            self._spare = (torch.empty(L, lanes_out, self.n_max, self.d_m, dtype=self.cache.dtype, device="cuda"),
+                           torch.empty(L, lanes_out, dtype=torch.int32, device="cuda"))
         dst, dlen = self._spare
         st = stream if stream is not None else torch.cuda.current_stream()
         hint = rows_hint if rows_hint is not None else self.n_max
         for l in range(self.cache.shape[0]):
             capi.check(capi.lib().elattn_gpu_cache_gather(
                 self.cache[l].data_ptr(), self.lengths[l].data_ptr(), dst[l].data_ptr(), dlen[l].data_ptr(),
-                parent.data_ptr(), self.lanes, self.lanes, self.n_max, self.d_m, self.dtype, hint,
+                parent.data_ptr(), self.lanes, lanes_out, self.n_max, self.d_m, self.dtype, hint,
                 _stream_ptr(st)))
         self._spare = (self.cache, self.lengths)
         self.cache, self.lengths = dst, dlen
+        self.lanes = lanes_out
+
+    def keep(self, mask, rows_hint: Optional[int] = None, stream=None):
+        """DecoderState::keep_lanes (model.hpp:315-325): drop the lanes whose mask is false."""
+        self.gather(keep_lane_indices(mask, self.lanes), rows_hint, stream)
+
+    def permute(self, perm, rows_hint: Optional[int] = None, stream=None):
+        """DecoderState::permute_lanes (model.hpp:304-314)."""
+        self.gather(permute_lane_indices(perm, self.lanes), rows_hint, stream)
 
 
 class KvCache:
@@ -421,6 +475,29 @@ class KvCache:
         capi.check(capi.lib().elattn_gpu_kv_append(self.layer.dev.handle, Y.data_ptr(), self.R, self.K.data_ptr(),
                                                    self.V.data_ptr(), self.t_max, self.t, _stream_ptr(stream)))
         self.t += 1
+
+    def gather(self, parent, stream=None):
+        """Lane i of the new cache = lane parent[i] (gather_lanes, model.hpp:291-302, for the
+        mixed form's per-lane K/V; whole-lane copies on the device, lane count may change)."""
+        torch = _torch()
+        parent = _parent_tensor(parent, self.R)
+        R_out = parent.numel()
+        lane_bytes = self.K[0].numel() * self.K.element_size()
+        st = _stream_ptr(stream)
+        K = torch.empty((R_out,) + tuple(self.K.shape[1:]), dtype=self.K.dtype, device="cuda")
+        V = torch.empty_like(K)
+        for src, dst in ((self.K, K), (self.V, V)):
+            capi.check(capi.lib().elattn_gpu_lane_gather(src.data_ptr(), dst.data_ptr(), parent.data_ptr(), self.R,
+                                                         R_out, lane_bytes, st))
+        self.K, self.V, self.R = K, V, R_out
+
+    def keep(self, mask, stream=None):
+        """keep_lanes (model.hpp:315-325)."""
+        self.gather(keep_lane_indices(mask, self.R), stream)
+
+    def permute(self, perm, stream=None):
+        """permute_lanes (model.hpp:304-314)."""
+        self.gather(permute_lane_indices(perm, self.R), stream)
 
 
 def mixed_self_attention_batched(layer: "ElAttentionLayer", Y, P, cache: KvCache, x: int, n_per_input=None,

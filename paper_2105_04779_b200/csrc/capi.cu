@@ -685,3 +685,14 @@ extern "C" int elattn_gpu_beam_candidates(const float* lprobs, const float* live
         launch_beam_topk(lprobs, live_lp, penalty, B, lanes, roots, V, k, part, splits, parent, token, lp_sum, st);
     });
 }
+
+// ---------------------------------------------------------------- whole-lane gather
+extern "C" int elattn_gpu_lane_gather(const void* src, void* dst, const int* parent, int lanes_in, int lanes_out,
+                                      int64_t bytes_per_lane, elattn_stream_t stream) {
+    return guarded([&] {
+        ELA_REQUIRE(src && dst && parent, ELATTN_ERR_PARAM, "lane_gather: null buffer");
+        ELA_REQUIRE(src != dst, ELATTN_ERR_PARAM, "lane_gather: src and dst must differ");
+        ELA_REQUIRE(lanes_in >= 1 && lanes_out >= 1, ELATTN_ERR_SHAPE, "lane_gather: bad lane counts");
+        launch_lane_gather(src, dst, parent, lanes_in, lanes_out, bytes_per_lane, reinterpret_cast<cudaStream_t>(stream));
+    });
+}

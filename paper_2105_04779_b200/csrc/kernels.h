@@ -64,6 +64,8 @@ void launch_beam_topk(const float* lprobs, const float* live_lp, const float* pe
                       uint64_t* part, int splits, int* parent, int* token, float* lp_sum, cudaStream_t st);
 
 // Per-lane hidden-state caches (lane_cache.cu).
+void launch_lane_gather(const void* src, void* dst, const int* parent, int lanes_in, int lanes_out,
+                        int64_t bytes_per_lane, cudaStream_t st);
 void launch_cache_append(void* cache, const void* Y, int* len, int lanes, int n_max, int d_m, int dtype,
                          cudaStream_t st);
 void launch_cache_gather(const void* src, const int* src_len, void* dst, int* dst_len, const int* parent,

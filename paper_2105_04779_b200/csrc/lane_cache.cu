@@ -10,7 +10,9 @@
 //            which the decode turns into loud NaN rows)
 //   gather : DecoderState::gather_lanes (model.hpp:291-306) on the device — lane i of the
 //            destination becomes a copy of source lane parent[i] (rows 0..len-1) — so beam
-//            reordering never leaves the GPU.
+//            reordering never leaves the GPU (keep_lanes / permute_lanes, model.hpp:305-325,
+//            are gathers with a subset / a permutation as the parent list).
+//   lane_gather: the same for fixed-size per-lane state (K/V caches of the mixed form).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -50,7 +52,34 @@ __global__ void cache_gather_kernel(const V* __restrict__ src, const int* __rest
     if (blockIdx.x == 0 && threadIdx.x == 0) dst_len[lane] = ok ? src_len[p] : n_max + 1;  // bad parent: loud
 }
 
+// Whole-lane gather for fixed-size per-lane state (the mixed self-attention's K/V caches,
+// [R][h][t_max][d_k]): dst lane i = src lane parent[i]; a bad parent fills the lane with
+// 0xFF bytes (NaN in fp32 and bf16 — loud).
+__global__ void lane_gather_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                   const int* __restrict__ parent, int lanes_in, int64_t vec_per_lane) {
+    const int lane = blockIdx.y;
+    const int p = parent[lane];
+    const bool ok = p >= 0 && p < lanes_in;
+    const uint4* s = src + int64_t(ok ? p : 0) * vec_per_lane;
+    uint4* d = dst + int64_t(lane) * vec_per_lane;
+    const uint4 nan4 = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vec_per_lane;
+         i += int64_t(gridDim.x) * blockDim.x)
+        d[i] = ok ? s[i] : nan4;
+}
+
 }  // namespace
+
+void launch_lane_gather(const void* src, void* dst, const int* parent, int lanes_in, int lanes_out,
+                        int64_t bytes_per_lane, cudaStream_t st) {
+    ELA_REQUIRE(bytes_per_lane > 0 && bytes_per_lane % 16 == 0, ELATTN_ERR_SHAPE,
+                "lane_gather: bytes per lane must be a positive multiple of 16");
+    const int64_t vec = bytes_per_lane / 16;
+    const int gx = int(std::min<int64_t>(64, (vec + 4095) / 4096));
+    lane_gather_kernel<<<dim3(gx, lanes_out), 256, 0, st>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst),
+                                                             parent, lanes_in, vec);
+    ELA_CHECK_LAUNCH();
+}
 
 void launch_cache_append(void* cache, const void* Y, int* len, int lanes, int n_max, int d_m, int dtype,
                          cudaStream_t st) {

@@ -422,3 +422,46 @@ def test_beam_candidates_diverse_penalty(gpu):
     live = np.round(rng.uniform(-6, 0, B * lanes) * 8) / 8
     pen = 0.5 * rng.integers(0, 3, (B, V)).astype(np.float64)
     _beam_check(E, lp, live, lanes, k, lanes, pen)
+
+
+def test_lane_bookkeeping_on_device(gpu):
+    """gather (resize) / keep / permute of both cache kinds match the same index operation on
+    the host copies (model.hpp:291-325); device parents out of range give NaN lanes."""
+    import torch
+
+    E = gpu
+    c = BART_CFG
+    p = E.AttentionParams.random(4, 256, 64, E.Rng(9))
+    layer = E.ElAttentionLayer(p, E.DTYPE_BF16)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    # hidden-state cache: 2 layers, 4 lanes, ragged lengths
+    hc = E.HiddenStateCache(2, 4, 16, 256, E.DTYPE_BF16)
+    hc.cache.copy_((torch.rand(hc.cache.shape, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+    hc.lengths.copy_(torch.tensor([[3, 16, 7, 1], [2, 5, 9, 16]], dtype=torch.int32))
+    ref_c, ref_l = hc.cache.clone(), hc.lengths.clone()
+    hc.gather([1, 1, 3, 0, 2])  # expansion to 5 lanes
+    idx = torch.tensor([1, 1, 3, 0, 2], device="cuda")
+    assert torch.equal(hc.lengths, ref_l[:, idx])
+    for l in range(2):
+        for i, pi in enumerate([1, 1, 3, 0, 2]):
+            n = int(ref_l[l, pi])
+            assert torch.equal(hc.cache[l, i, :n], ref_c[l, pi, :n])
+    hc.keep([True, False, True, True, False])
+    assert hc.lanes == 3 and torch.equal(hc.lengths, ref_l[:, torch.tensor([1, 3, 0], device="cuda")])
+    hc.permute([2, 0, 1])
+    assert torch.equal(hc.lengths, ref_l[:, torch.tensor([0, 1, 3], device="cuda")])
+    with pytest.raises(E.StateError):
+        hc.keep([False, False, False])
+    # mixed-form K/V cache
+    kv = E.KvCache(layer, 4, 8)
+    kv.K.copy_((torch.rand(kv.K.shape, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+    kv.V.copy_((torch.rand(kv.V.shape, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+    K0, V0 = kv.K.clone(), kv.V.clone()
+    kv.gather([3, 3, 1])
+    sel = torch.tensor([3, 3, 1], device="cuda")
+    assert kv.R == 3 and torch.equal(kv.K, K0[sel]) and torch.equal(kv.V, V0[sel])
+    kv.keep([False, True, True])
+    assert torch.equal(kv.K, K0[torch.tensor([3, 1], device="cuda")])
+    kv.gather(torch.tensor([0, 7], dtype=torch.int32, device="cuda"))  # device parent 7 is out of range
+    torch.cuda.synchronize()
+    assert torch.isnan(kv.K[1].float()).all() and torch.equal(kv.K[0], K0[3])
