@@ -25,3 +25,20 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+@pytest.mark.gpu
+def test_our_arm_json_line():
+    """bench.py's own arm on the GPU: one JSON line with the contract's keys, our kernels
+    counted, the decode roofline and the overlapped e2e present (small B for speed)."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "3", "--warmup", "3", "--batch", "74",
+                        "--layers", "2", "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "dtype", "data", "config", "e2e", "roofline", "gpu_launches", "clocks"):
+        assert key in line, key
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 74 * 4 * 1024 * 2
+    assert 0 < line["roofline"]["frac"] <= 1.0 and line["roofline"]["bound"] == "hbm"
+    assert line["outputs_finite"] is True
