@@ -234,7 +234,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* q_tmem_full = bars + 2;   // q' TMEM half written by the exchange warps (per input)
     uint64_t* o_full = bars + 3;        // last O MMA of an input complete
     uint64_t* o_free = bars + 4;        // epilogue has read O out of TMEM
-    uint64_t* o_done = bars + 5;        // per tile: O MMAs complete
+    uint64_t* o_done0 = bars + 5;       // per even tile: O MMAs complete
     uint64_t* s_full = bars + 6;        // [4]
     uint64_t* s_empty = s_full + kSBuf;  // [4]
     uint64_t* p_full = s_empty + kSBuf;  // [2]
@@ -243,7 +243,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* recv_free = recv_full + 2;  // [2] arrived by the PEER's softmax warps
     uint64_t* unit_full = recv_free + 2;  // [kRing]
     uint64_t* unit_empty = unit_full + kRing;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(unit_empty + kRing);
+    uint64_t* o_done1 = unit_empty + kRing;  // per odd tile: O MMAs complete
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done1 + 1);
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
     const uint32_t rank = ptx::cluster_ctarank(), peer = rank ^ 1u;
@@ -261,7 +262,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_init(q_tmem_full, 4);
             ptx::mbar_init(o_full, 1);
             ptx::mbar_init(o_free, 4);
-            ptx::mbar_init(o_done, 1);
+            ptx::mbar_init(o_done0, 1);
+            ptx::mbar_init(o_done1, 1);
             for (int i = 0; i < kSBuf; ++i) {
                 ptx::mbar_init(&s_full[i], 1);
                 ptx::mbar_init(&s_empty[i], 5);  // 4 exchange warps + the O issuer (softmax relay)
@@ -447,7 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         ptx::mma_commit(&unit_empty[slot]);
                     }
                     ptx::mma_commit(&p_empty[pb]);
-                    ptx::mma_commit(o_done);
+                    ptx::mma_commit(pb ? o_done1 : o_done0);
                     // P(Gt) observed => the softmax has consumed S(Gt): release its buffer
                     ptx::mbar_arrive(&s_empty[Gt & (kSBuf - 1)]);
                 }
@@ -678,11 +680,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 }
                 const uint32_t any = softmax_bar_or(need);
-                // consume o_done phases in order (one per tile) so the parity wait is exact;
-                // O(Gt-1) was issued a full stage ago, so this rarely blocks
-                if (Gt > 0) ptx::mbar_wait(o_done, (Gt - 1) & 1);
                 if (any && jj > 0) {
-                    // lazy rescale of the running O^T columns (O(Gt-1) complete): O *= alpha
+                    // lazy rescale of the running O^T columns once O(Gt-1) is complete: O *= alpha.
+                    // (o_done has one barrier per tile parity, so waits can be skipped: the
+                    // barrier of Gt-1 cannot be a full phase ahead while P(Gt+1) is unposted)
+                    ptx::mbar_wait((Gt - 1) & 1 ? o_done1 : o_done0, ((Gt - 1) >> 1) & 1);
                     ptx::tc_fence_after();
 #pragma unroll 1
                     for (int m = 0; m < UNITS; ++m) {
