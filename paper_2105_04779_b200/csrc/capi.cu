@@ -676,7 +676,9 @@ extern "C" int elattn_gpu_beam_candidates(const float* lprobs, const float* live
     return guarded([&] {
         ELA_REQUIRE(lprobs && live_lp && parent && token && lp_sum, ELATTN_ERR_PARAM, "beam_candidates: null buffer");
         ELA_REQUIRE(B >= 1, ELATTN_ERR_SHAPE, "beam_candidates: B must be >= 1");
-        ELA_REQUIRE(k >= 1 && k <= 32 && V >= 1, ELATTN_ERR_SHAPE, "beam_candidates: 1 <= k <= 32, V >= 1");
+        ELA_REQUIRE(k >= 1, ELATTN_ERR_PARAM, "beam_candidates: k must be >= 1");
+        ELA_REQUIRE(k <= 32, ELATTN_ERR_UNSUPPORTED, "beam_candidates: k <= 32 (2 x beam for beam <= 16)");
+        ELA_REQUIRE(V >= 1, ELATTN_ERR_SHAPE, "beam_candidates: V must be >= 1");
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         const int splits = beam_splits(B, V);
         const size_t part_bytes = sizeof(uint64_t) * size_t(B) * splits * k;

@@ -465,3 +465,33 @@ def test_lane_bookkeeping_on_device(gpu):
     kv.gather(torch.tensor([0, 7], dtype=torch.int32, device="cuda"))  # device parent 7 is out of range
     torch.cuda.synchronize()
     assert torch.isnan(kv.K[1].float()).all() and torch.equal(kv.K[0], K0[3])
+
+
+def test_beam_candidates_errors_and_edges(gpu):
+    """Reference-style errors at the boundary (k outside [1, 32], roots > lanes, shape
+    mismatch) and edges: fewer finite candidates than k (parent -1 rows), V = 1, 256 lanes."""
+    import torch
+
+    E = gpu
+    lp = torch.zeros(4, 10, device="cuda")
+    live = torch.zeros(4, device="cuda")
+    with pytest.raises(E.UnsupportedError):
+        E.beam_candidates(lp, live, 2, 33)
+    with pytest.raises(E.ParamError):
+        E.beam_candidates(lp, live, 2, 0)
+    with pytest.raises(E.ShapeError):
+        E.beam_candidates(lp, live, 2, 4, roots=3)
+    with pytest.raises(E.ShapeError):
+        E.beam_candidates(lp, live[:3], 2, 4)
+    # only 3 finite candidates for k = 5
+    lp = torch.full((2, 4), float("-inf"), device="cuda")
+    lp[0, 1], lp[0, 3], lp[1, 2] = -1.0, -2.0, -0.5
+    par, tok, lps = E.beam_candidates(lp, torch.tensor([0.0, -1.0], device="cuda"), 2, 5)
+    # candidates (parent, token, lp_sum): (0, 1, -1.0), (1, 2, -1.5), (0, 3, -2.0)
+    assert par.cpu().tolist() == [[0, 1, 0, -1, -1]] and tok.cpu().tolist() == [[1, 2, 3, -1, -1]]
+    assert lps.cpu()[0, :3].tolist() == [-1.0, -1.5, -2.0] and torch.isinf(lps.cpu()[0, 3:]).all()
+    # V = 1 and 256 lanes
+    rng = np.random.default_rng(5)
+    lp1 = np.round(rng.uniform(-4, 0, (512, 1)) * 8) / 8
+    live1 = np.round(rng.uniform(-4, 0, 512) * 8) / 8
+    _beam_check(E, lp1, live1, 256, 16, 256)
