@@ -200,7 +200,7 @@ struct Sched {
     }
 };
 
-template <int UNITS>
+template <int UNITS, bool TRACE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     el_decode_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_h,
                         const __grid_constant__ CUtensorMap tm_c,
@@ -210,11 +210,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         float2* __restrict__ stats) {
     using L = DecLayout<UNITS>;
     constexpr int kRing = L::kRing;
-    // optional per-tile clock64 trace of the first cluster (testing hook); G = cluster tile index
+    // optional per-tile clock64 trace of the first cluster (testing hook); G = cluster tile index.
+    // Compiled only into the TRACE instantiation: the checks cost ~3% in the production kernel.
 #define ELA_TRACE(ev, G)                                                                          \
     do {                                                                                          \
-        if (trace != nullptr && blockIdx.x < 2 && (G) < 64)                                       \
-            trace[(blockIdx.x * 32 + (ev)) * 64 + (G)] = clock64();                               \
+        if constexpr (TRACE)                                                                      \
+            if (trace != nullptr && blockIdx.x < 2 && (G) < 64)                                   \
+                trace[(blockIdx.x * 32 + (ev)) * 64 + (G)] = clock64();                           \
     } while (0)
     constexpr int kTmemCols = 512;
     constexpr uint32_t kTmemS = L::kTmemS;
@@ -1024,7 +1026,7 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const uint64_t cdims[2] = {uint64_t(d_m), uint64_t(B) * rows};
     const uint32_t cbox[2] = {32, uint32_t(rows)};
     CUtensorMap tc = make_tmap_bf16(ctx, 2, cdims, qstr, cbox, 64);
-    auto kern = el_decode_tc_kernel<UNITS>;
+    auto kern = g_decode_trace != nullptr ? el_decode_tc_kernel<UNITS, true> : el_decode_tc_kernel<UNITS, false>;
     constexpr uint32_t smem = DecLayout<UNITS>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // persistent: one cluster per pair of SMs
