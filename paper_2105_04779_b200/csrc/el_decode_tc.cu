@@ -211,7 +211,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     using L = DecLayout<UNITS>;
     constexpr int kRing = L::kRing;
     // optional per-tile clock64 trace of the first cluster (testing hook); G = cluster tile index.
-    // Compiled only into the TRACE instantiation: the checks cost ~3% in the production kernel.
+    // Compiled only into the TRACE (instrumented) instantiation, like the tuning knobs below:
+    // their checks cost ~3% in the production kernel.
 #define ELA_TRACE(ev, G)                                                                          \
     do {                                                                                          \
         if constexpr (TRACE)                                                                      \
@@ -311,7 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 for (int jj = 0; jj < T; ++jj) {
                     const int j = j0 + jj, Gt = G + jj;
-                    if (tune.l2_ahead > 0 && j + tune.l2_ahead < Tb)
+                    if (TRACE && tune.l2_ahead > 0 && j + tune.l2_ahead < Tb)
                         for (int c = 0; c < 2 * UNITS; ++c)
                             ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, b / sa.vchunks);
                     for (int u = 0; u < UNITS; ++u) {
@@ -375,7 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // buffer Gt%4 is free once the exchange warps and (relayed by the O
                 // issuer) the softmax have consumed S(Gt-4)
                 ptx::mbar_wait(&s_empty[sb], ((Gt / kSBuf) & 1) ^ 1);
-                if (tune.s_ahead < kSBuf && Gt >= tune.s_ahead) {
+                if (TRACE && tune.s_ahead < kSBuf && Gt >= tune.s_ahead) {
                     const int jj = Gt - tune.s_ahead;  // bound the lookahead: O(Gt - s_ahead) issued
                     ptx::mbar_wait(&s_empty[jj & (kSBuf - 1)], (jj / kSBuf) & 1);
                 }
@@ -1026,7 +1027,9 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const uint64_t cdims[2] = {uint64_t(d_m), uint64_t(B) * rows};
     const uint32_t cbox[2] = {32, uint32_t(rows)};
     CUtensorMap tc = make_tmap_bf16(ctx, 2, cdims, qstr, cbox, 64);
-    auto kern = g_decode_trace != nullptr ? el_decode_tc_kernel<UNITS, true> : el_decode_tc_kernel<UNITS, false>;
+    // instrumented instantiation (trace hook, lookahead knobs) only when asked for
+    const bool instr = g_decode_trace != nullptr || g_tuning.s_ahead != 4 || g_tuning.l2_ahead != 0;
+    auto kern = instr ? el_decode_tc_kernel<UNITS, true> : el_decode_tc_kernel<UNITS, false>;
     constexpr uint32_t smem = DecLayout<UNITS>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // persistent: one cluster per pair of SMs
