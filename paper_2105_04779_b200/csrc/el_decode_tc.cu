@@ -200,7 +200,7 @@ struct Sched {
     }
 };
 
-template <int UNITS, bool TRACE>
+template <int UNITS, bool TRACE, bool MASK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     el_decode_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_h,
                         const __grid_constant__ CUtensorMap tm_c,
@@ -570,7 +570,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         while (sc.next(b, j0, j1, Tb, kind)) {
             const int T = j1 - j0;
             const int n_b = n_per_input ? n_per_input[b / sa.vchunks] : n_stride;
-            const bool zero_tail = (n_per_input != nullptr) && (Tb * kNT > n_b);
+            // MASK: ragged lengths or n not a multiple of the tile (else no tile is partial)
+            const bool zero_tail = MASK && (n_per_input != nullptr) && (Tb * kNT > n_b);
             float m_a = neg_inf, m_b = neg_inf, l_a = 0.f, l_b = 0.f;  // running max (raw units), sums
             for (int jj = 0; jj < T; ++jj) {
                 const int j = j0 + jj;  // tile index within the input
@@ -598,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     s[4 * k + 2] = __uint_as_float(sr[4 * k + 2]) + v.z;
                     s[4 * k + 3] = __uint_as_float(sr[4 * k + 3]) + v.w;
                 }
-                if (nvalid < kNT) {
+                if (MASK && nvalid < kNT) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -1029,7 +1030,9 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     CUtensorMap tc = make_tmap_bf16(ctx, 2, cdims, qstr, cbox, 64);
     // instrumented instantiation (trace hook, lookahead knobs) only when asked for
     const bool instr = g_decode_trace != nullptr || g_tuning.s_ahead != 4 || g_tuning.l2_ahead != 0;
-    auto kern = instr ? el_decode_tc_kernel<UNITS, true> : el_decode_tc_kernel<UNITS, false>;
+    const bool mask = npi != nullptr || n_stride % kNT != 0;
+    auto kern = instr ? (mask ? el_decode_tc_kernel<UNITS, true, true> : el_decode_tc_kernel<UNITS, true, false>)
+                      : (mask ? el_decode_tc_kernel<UNITS, false, true> : el_decode_tc_kernel<UNITS, false, false>);
     constexpr uint32_t smem = DecLayout<UNITS>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // persistent: one cluster per pair of SMs
