@@ -153,7 +153,7 @@ __device__ __forceinline__ int tiles_of(const int* npi, int b, int n_stride, int
 // c+ncl, ...
 struct SplitArgs {
     int T;           // tiles per input (uniform mode), 0 = ragged / strided whole inputs
-    int W;           // tiles per cluster chunk (uniform mode)
+    int W;           // tiles per cluster chunk (uniform stream-K); -P: TAIL-SPLIT (see Sched)
     float* part;     // partial records [2 * ncl slots][2 ranks][kPartFloats]
     int vchunks;     // virtual inputs per real input (query rows / 64 when rows > 64)
 };
@@ -175,6 +175,26 @@ struct Sched {
     // next segment: input bb, tiles [j0, j1) of its Tb; kind -1 = whole input, 0 = first
     // segment of this cluster's chunk, 1 = last segment (partial-record slot 2*cl + kind)
     __device__ bool next(int& bb, int& j0, int& j1, int& Tb, int& kind) {
+        if (T > 0 && W < 0) {
+            // TAIL-SPLIT: the full rounds as whole inputs (b = cl, cl + ncl, ... < Bw), then
+            // part c % P of leftover input Bw + c / P, c = cl = b - Bw (no extra state: the
+            // decode is sensitive to register pressure)
+            const int Bw = B - B % ncl;
+            if (b < Bw) {
+                bb = b, j0 = 0, j1 = T, Tb = T, kind = -1;
+                b += ncl;
+                return true;
+            }
+            if (!first) return false;
+            first = false;
+            const int P = -W, c = b - Bw;
+            if (c >= (B - Bw) * P) return false;
+            bb = Bw + c / P;
+            j0 = (T * (c % P)) / P;
+            j1 = (T * (c % P + 1)) / P;
+            Tb = T, kind = 0;
+            return j1 > j0;
+        }
         if (T > 0) {
             if (g >= g_end) return false;
             bb = g / T;
@@ -911,14 +931,22 @@ template <int UNITS>
 __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __restrict__ part, int T, int W, int ncl,
                                                               int rows, int d_m, float scale_log2,
                                                               __nv_bfloat16* __restrict__ ctx,
-                                                              float2* __restrict__ stats) {
+                                                              float2* __restrict__ stats, int Bw) {
     constexpr int kPF = kPartFloatsHdr + UNITS * kPartFloatsUnit;
-    const int k = int(blockIdx.x) + 1, rank = int(blockIdx.y), m = int(blockIdx.z);
-    const int64_t gk = int64_t(k) * W;
-    const int b = int(gk / T);
-    if (gk % T == 0 || int64_t(k - 1) * W > int64_t(b) * T) return;  // not a split, or not b's first boundary
-    const int c_first = int((int64_t(b) * T) / W);
-    const int nseg = min(kMaxSegs, int((int64_t(b) * T + T - 1) / W) - c_first + 1);
+    const int rank = int(blockIdx.y), m = int(blockIdx.z);
+    int b, c_first, nseg;
+    if (W < 0) {  // tail-split: input Bw + x in P = -W parts on clusters P x .. P x + P - 1 (slot 0)
+        b = Bw + int(blockIdx.x);
+        c_first = int(blockIdx.x) * -W;
+        nseg = -W;
+    } else {
+        const int k = int(blockIdx.x) + 1;
+        const int64_t gk = int64_t(k) * W;
+        b = int(gk / T);
+        if (gk % T == 0 || int64_t(k - 1) * W > int64_t(b) * T) return;  // not a split, or not b's first boundary
+        c_first = int((int64_t(b) * T) / W);
+        nseg = min(kMaxSegs, int((int64_t(b) * T + T - 1) / W) - c_first + 1);
+    }
     __shared__ const float* s_rec[kMaxSegs];
     __shared__ float s_w[kMaxSegs][64];
     __shared__ float s_inv[64];
@@ -926,7 +954,7 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
     const int tid = int(threadIdx.x);
     if (tid < nseg) {
         const int c2 = c_first + tid;
-        const int kd = (int64_t(c2) * W >= int64_t(b) * T) ? 0 : 1;  // b's segment is c2's first?
+        const int kd = (W < 0 || int64_t(c2) * W >= int64_t(b) * T) ? 0 : 1;  // b's segment is c2's first?
         s_rec[tid] = part + (int64_t(2 * c2 + kd) * 2 + rank) * kPF;
     }
     __syncthreads();
@@ -1043,16 +1071,30 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     // of the clusters: then stream-K (every input-segment transition costs a pipeline drain,
     // so splitting only pays when the tail is short; measured on B200 for B = 64..320).
     const int last_round = B % max_cl;
-    // ELATTN_DECODE_SCHED = auto (default) | streamk | whole: tuning override
+    // ELATTN_DECODE_SCHED = auto (default) | streamk | tail | whole: tuning override
     static const int sched_mode = [] {
         const char* e = getenv("ELATTN_DECODE_SCHED");
         if (!e) return 0;
         const std::string v(e);
-        return v == "streamk" ? 1 : v == "whole" ? 2 : 0;
+        return v == "streamk" ? 1 : v == "whole" ? 2 : v == "tail" ? 3 : 0;
     }();
     const bool stream_k = npi == nullptr && last_round != 0 &&
-                          (sched_mode == 1 || (sched_mode == 0 && 5 * last_round < 3 * max_cl));
-    if (stream_k) {
+                          (sched_mode == 1 || sched_mode == 3 || (sched_mode == 0 && 5 * last_round < 3 * max_cl));
+    // TAIL-SPLIT instead of stream-K when there is at least one full round and the leftover
+    // inputs, cut into P <= kMaxSegs equal parts, keep >= 3/4 of the clusters busy: the
+    // full rounds stay whole inputs (no records, no extra transitions)
+    const int T_all = (n_stride + kNT - 1) / kNT;
+    const int P_tail = last_round > 0 ? std::min(kMaxSegs, std::min(max_cl / last_round, T_all)) : 0;
+    const bool tail_split = stream_k && B >= max_cl && sched_mode != 1 && P_tail >= 2 &&
+                            (sched_mode == 3 || 4 * last_round * P_tail >= 3 * max_cl);
+    if (tail_split) {
+        sa.T = T_all;
+        sa.W = -P_tail;
+        sa.vchunks = vchunks;
+        clusters = max_cl;
+        constexpr size_t kPF = kPartFloatsHdr + size_t(UNITS) * kPartFloatsUnit;
+        sa.part = split_scratch(st, size_t(2 * clusters) * 2 * kPF * sizeof(float));
+    } else if (stream_k) {
         // stream-K over B*T tiles: chunks of W tiles (>= kMinChunkTiles), one per cluster
         const int T = (n_stride + kNT - 1) / kNT;
         const int64_t TT = int64_t(B) * T;
@@ -1079,8 +1121,10 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
                                                      g_decode_trace, g_tuning, sa, stats);
     ELA_CHECK_LAUNCH();
     if (sa.part != nullptr && clusters > 1) {
-        el_decode_merge_kernel<UNITS><<<dim3(clusters - 1, 2, UNITS), 256, 0, st>>>(
-            sa.part, sa.T, sa.W, clusters, rows, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx), stats);
+        const int Bw = B - last_round;
+        const int gx = sa.W < 0 ? last_round : clusters - 1;
+        el_decode_merge_kernel<UNITS><<<dim3(gx, 2, UNITS), 256, 0, st>>>(
+            sa.part, sa.T, sa.W, clusters, rows, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx), stats, Bw);
         ELA_CHECK_LAUNCH();
     }
 }
