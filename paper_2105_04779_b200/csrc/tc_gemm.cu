@@ -40,7 +40,7 @@ struct GemmSmem {
     static constexpr int kBoxCols = BN / 2 < 64 ? BN / 2 : 64;  // 64 (SW128) or 32 (SW64)
     static constexpr uint32_t kWarpBox = 32 * kBoxCols * 2;
     static constexpr uint32_t kWarpStage = (BN / 2) / kBoxCols * kWarpBox;
-    static constexpr int kOutStages = 2;
+    static constexpr int kOutStages = 3;
     static constexpr uint32_t kOutBytes = kEpiWarps * kOutStages * kWarpStage;
     static constexpr uint32_t kFixed = kOutBytes + 256 + 1024;
     static constexpr int kStagesFit = int((232448u - kFixed) / kStageBytes);
