@@ -244,3 +244,29 @@ def test_decode_schedules_agree_over_random_batches():
         want = decode_ref(qp.view(B, rows, d_m)[sel].reshape(-1, d_m), H[sel], rows, 0.125)
         got = outs[0].view(B, rows, d_m)[sel].reshape(-1, d_m)
         assert (got - want).abs().max().item() / want.abs().max().item() < 2e-2, (B, n)
+
+
+def test_decode_instrumented_instantiation_matches():
+    """The instrumented decode instantiation (selected while the clock64 trace hook is set)
+    computes bit-identical outputs to the production one, and records stamps."""
+    import torch
+
+    L, capi = _testing_lib()
+    L.elattn_gpu_testing_set_decode_trace.argtypes = [ctypes.c_void_p]
+    B, rows, n, d_m = 80, 64, 300, 1024  # stream-K / split schedule, masked last tile
+    g = torch.Generator(device="cuda").manual_seed(21)
+    qp = (torch.randn(B * rows, d_m, generator=g, device="cuda") * 0.3).to(torch.bfloat16)
+    H = (torch.rand(B, n, d_m, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    st = torch.cuda.current_stream().cuda_stream
+    tr = torch.zeros(2 * 32 * 64, dtype=torch.int64, device="cuda")
+    outs = []
+    for trace in (None, tr):
+        L.elattn_gpu_testing_set_decode_trace(trace.data_ptr() if trace is not None else None)
+        ctx = torch.full((B * rows, d_m), float("nan"), device="cuda", dtype=torch.bfloat16)
+        capi.check(L.elattn_gpu_testing_decode_bf16(qp.data_ptr(), H.data_ptr(), None, B, rows, n, d_m, 0.125,
+                                                    ctx.data_ptr(), 1, st))
+        torch.cuda.synchronize()
+        outs.append(ctx)
+    L.elattn_gpu_testing_set_decode_trace(None)
+    assert torch.equal(outs[0], outs[1])
+    assert int((tr != 0).sum()) > 0
