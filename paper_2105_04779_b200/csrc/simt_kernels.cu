@@ -118,9 +118,11 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
                                                              int d_m, float scale_log2,
                                                              T* __restrict__ ctx, float2* __restrict__ stats) {
     extern __shared__ float smem[];
-    const int ldq = d_m, ldh = d_m + 1;  // +1: conflict-free column walks of the H tile
-    float* sq = smem;                                // [16][d_m]
-    float* sh = sq + kSimtRows * ldq;                // [16][d_m + 1]
+    // padded rows: q rows 16 banks apart (+16), H rows 4 apart land 16 banks apart (+4), so
+    // the two half-warps of the score phase never collide
+    const int ldq = d_m + 16, ldh = d_m + 4;
+    float* sq = smem;                                // [16][d_m + 16]
+    float* sh = sq + kSimtRows * ldq;                // [16][d_m + 4]
     float* sp = sh + kSimtTile * ldh;                // [16][16]
     float* s_alpha = sp + kSimtRows * kSimtTile;     // [16]
     float* s_l = s_alpha + kSimtRows;                // [16]
@@ -156,12 +158,47 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
             sh[r * ldh + c] = (t0 + r < n) ? to_f32(Hb[(int64_t)(t0 + r) * d_m + c]) : 0.f;
         }
         __syncthreads();
-        float s = 0.f;
+        // scores, register-blocked: half-warp = one 4 (q rows) x 4 (H rows) block, its 16 lanes
+        // split K (k = lane, lane + 16, ...): 8 shared loads per 16 FMAs; a butterfly
+        // reduce-scatter over the 16 lanes leaves lane s with score (4 rb + s/4, 4 tb + s%4)
         {
-            const float* a = sq + sr * ldq;
-            const float* h = sh + st_ * ldh;
-            for (int k = 0; k < d_m; ++k) s = fmaf(a[k], h[k], s);
+            const int ks = tid & 15, pair = tid >> 4, rb = pair >> 2, tb = pair & 3;
+            float acc_s[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc_s[i] = 0.f;
+            const float* a = sq + (rb * 4) * ldq;
+            const float* hh = sh + (tb * 4) * ldh;
+#pragma unroll 4
+            for (int k = ks; k < d_m; k += 16) {
+                float qa[4], hb[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) qa[i] = a[i * ldq + k];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) hb[j] = hh[j * ldh + k];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc_s[i * 4 + j] = fmaf(qa[i], hb[j], acc_s[i * 4 + j]);
+            }
+            // reduce-scatter: at step w (8, 4, 2, 1) keep the half of the values whose index
+            // bit matches this lane's bit, add the partner's copy of it
+#pragma unroll
+            for (int w = 8; w >= 1; w >>= 1) {
+                const bool upper = (ks & w) != 0;
+#pragma unroll
+                for (int i = 0; i < w; ++i) {
+                    const float send = upper ? acc_s[i] : acc_s[i + w];
+                    const float keep = upper ? acc_s[i + w] : acc_s[i];
+                    acc_s[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+                }
+            }
+            // lane ks now holds the block element whose index bits equal ks (bit-reversed
+            // accumulation order keeps index == ks): score (4 rb + ks / 4, 4 tb + ks % 4)
+            sp[(rb * 4 + (ks >> 2)) * kSimtTile + tb * 4 + (ks & 3)] = acc_s[0];
         }
+        __syncthreads();
+        float s = sp[sr * kSimtTile + st_];
+        __syncthreads();  // sp is rewritten with P below
         s = (t0 + st_ < n) ? s * scale_log2 : -INFINITY;
         float mx = s;
 #pragma unroll
@@ -221,7 +258,7 @@ static void launch_decode_cpt(const void* qp, const void* H, const int* npi, int
                               int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st,
                               float2* stats) {
     const size_t smem =
-        sizeof(float) * (size_t(kSimtRows) * d_m + size_t(kSimtTile) * (d_m + 1) +
+        sizeof(float) * (size_t(kSimtRows) * (d_m + 16) + size_t(kSimtTile) * (d_m + 4) +
                          kSimtRows * kSimtTile + 2 * kSimtRows);
     auto kern = el_decode_simt_kernel<T, CPT>;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
