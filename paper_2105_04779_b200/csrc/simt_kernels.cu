@@ -5,6 +5,8 @@
 // cannot meet that bound, so fp32 runs on CUDA cores.  They also serve bf16
 // shapes outside the tcgen05 kernels' envelope (e.g. the reference tests'
 // d_m = 8..128, d_k = 3).  All accumulation is fp32.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -116,7 +118,9 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
                                                              const int* __restrict__ n_per_input,
                                                              int rows_per_input, int n_stride,
                                                              int d_m, float scale_log2,
-                                                             T* __restrict__ ctx, float2* __restrict__ stats) {
+                                                             T* __restrict__ ctx, float2* __restrict__ stats,
+                                                             int splits, float* __restrict__ part_o,
+                                                             float2* __restrict__ part_ml) {
     extern __shared__ float smem[];
     // padded rows: q rows 16 banks apart (+16), H rows 4 apart land 16 banks apart (+4), so
     // the two half-warps of the score phase never collide
@@ -126,6 +130,7 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
     float* sp = sh + kSimtTile * ldh;                // [16][16]
     float* s_alpha = sp + kSimtRows * kSimtTile;     // [16]
     float* s_l = s_alpha + kSimtRows;                // [16]
+    float* s_m = s_l + kSimtRows;                    // [16]
     const int b = blockIdx.y, r0 = blockIdx.x * kSimtRows, tid = threadIdx.x;
     const int n = n_per_input ? n_per_input[b] : n_stride;
     const T* Hb = H + (int64_t)b * n_stride * d_m;
@@ -151,7 +156,13 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
     const int sr = tid / kSimtTile, st_ = tid % kSimtTile;
     float m_run = -INFINITY, l_run = 0.f;  // valid in threads with st_ == 0 (replicated)
 
-    for (int t0 = 0; t0 < n; t0 += kSimtTile) {
+    // split z of `splits` takes tiles [z T / S, (z + 1) T / S) of the context (flash-decoding
+    // style; the partial rows are combined by simt_merge_kernel)
+    const int T_all = (n + kSimtTile - 1) / kSimtTile;
+    const int t_beg = int((int64_t(blockIdx.z) * T_all) / splits) * kSimtTile;
+    const int t_end = min(n, int((int64_t(blockIdx.z + 1) * T_all) / splits) * kSimtTile);
+    if (tid < kSimtRows) s_m[tid] = -INFINITY, s_l[tid] = 0.f;
+    for (int t0 = t_beg; t0 < t_end; t0 += kSimtTile) {
         __syncthreads();  // previous tile fully consumed
         for (int e = tid; e < kSimtTile * d_m; e += 256) {
             const int r = e / d_m, c = e % d_m;
@@ -215,7 +226,8 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
         if (st_ == 0) {
             s_alpha[sr] = alpha;
             s_l[sr] = l_run;
-            if (stats != nullptr && sr < nrows) stats[row_base + sr] = make_float2(m_run, l_run);
+            s_m[sr] = m_run;
+            if (splits == 1 && stats != nullptr && sr < nrows) stats[row_base + sr] = make_float2(m_run, l_run);
         }
         __syncthreads();
 #pragma unroll
@@ -241,6 +253,20 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
         }
     }
     __syncthreads();
+    if (splits > 1) {  // unnormalised partial rows + {m, l} for the merge
+        const int64_t prow = int64_t(blockIdx.z) * gridDim.y * rows_per_input + row_base;
+        if (tid < nrows) part_ml[prow + tid] = make_float2(s_m[tid], s_l[tid]);
+#pragma unroll
+        for (int r = 0; r < kSimtRows; ++r) {
+            if (r >= nrows) break;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const int col = tid + c * 256;
+                if (col < d_m) part_o[(prow + r) * d_m + col] = acc[r][c];
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int r = 0; r < kSimtRows; ++r) {
         if (r >= nrows) break;
@@ -253,19 +279,74 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
     }
 }
 
+// Combines the `splits` partial rows of the split SIMT decode: M = max m_s,
+// w_s = 2^(m_s - M), L = sum l_s w_s, C = sum w_s O_s / L (stats {M, L}).  One CTA per row.
+template <typename T>
+__global__ void __launch_bounds__(256) simt_merge_kernel(const float* __restrict__ part_o,
+                                                         const float2* __restrict__ part_ml, int splits,
+                                                         int64_t total_rows, int rows_per_input,
+                                                         const int* __restrict__ n_per_input, int n_stride,
+                                                         int d_m, T* __restrict__ ctx, float2* __restrict__ stats) {
+    const int64_t row = blockIdx.x;
+    if (n_per_input != nullptr) {
+        const int n = n_per_input[row / rows_per_input];
+        if (n < 1 || n > n_stride) return;  // the decode wrote loud NaN rows
+    }
+    float M = -INFINITY;
+    for (int s = 0; s < splits; ++s) M = fmaxf(M, part_ml[s * total_rows + row].x);
+    float L = 0.f;
+    for (int s = 0; s < splits; ++s) {
+        const float2 ml = part_ml[s * total_rows + row];
+        L += ml.y * exp2f(ml.x - M);
+    }
+    const float inv = 1.f / L;
+    for (int col = threadIdx.x; col < d_m; col += 256) {
+        float acc = 0.f;
+        for (int s = 0; s < splits; ++s) {
+            const float2 ml = part_ml[s * total_rows + row];
+            acc += part_o[(s * total_rows + row) * d_m + col] * exp2f(ml.x - M);
+        }
+        ctx[row * d_m + col] = from_f32<T>(acc * inv);
+    }
+    if (stats != nullptr && threadIdx.x == 0) stats[row] = make_float2(M, L);
+}
+
 template <typename T, int CPT>
 static void launch_decode_cpt(const void* qp, const void* H, const int* npi, int B, int rows,
                               int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st,
                               float2* stats) {
     const size_t smem =
         sizeof(float) * (size_t(kSimtRows) * (d_m + 16) + size_t(kSimtTile) * (d_m + 4) +
-                         kSimtRows * kSimtTile + 2 * kSimtRows);
+                         kSimtRows * kSimtTile + 3 * kSimtRows);
     auto kern = el_decode_simt_kernel<T, CPT>;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    dim3 grid(unsigned(ceil_div(rows, kSimtRows)), unsigned(B));
+    // split the context over CTAs when (row blocks x inputs) leave more than a quarter of the
+    // SMs idle (measured: B = 8 BART 0.96 -> 0.48 ms per layer; at B = 32, 128 blocks on 148
+    // SMs, the partial rows cost more than the idle SMs)
+    const int blocks = int(ceil_div(rows, kSimtRows)) * B;
+    const int T_all = int(ceil_div(n_stride, kSimtTile));
+    int splits = 4 * blocks >= 3 * 148 ? 1 : int(ceil_div(296, blocks));
+    splits = std::max(1, std::min({splits, 8, T_all}));
+    float* part_o = nullptr;
+    float2* part_ml = nullptr;
+    const int64_t total_rows = int64_t(B) * rows;
+    if (splits > 1) {
+        ELA_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part_o),
+                                       sizeof(float) * size_t(splits) * size_t(total_rows) * d_m, st));
+        ELA_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part_ml),
+                                       sizeof(float2) * size_t(splits) * size_t(total_rows), st));
+    }
+    dim3 grid(unsigned(ceil_div(rows, kSimtRows)), unsigned(B), unsigned(splits));
     kern<<<grid, 256, smem, st>>>(static_cast<const T*>(qp), static_cast<const T*>(H), npi, rows,
-                                  n_stride, d_m, scale_log2, static_cast<T*>(ctx), stats);
+                                  n_stride, d_m, scale_log2, static_cast<T*>(ctx), stats, splits, part_o, part_ml);
     ELA_CHECK_LAUNCH();
+    if (splits > 1) {
+        simt_merge_kernel<T><<<unsigned(total_rows), 256, 0, st>>>(part_o, part_ml, splits, total_rows, rows, npi,
+                                                                   n_stride, d_m, static_cast<T*>(ctx), stats);
+        ELA_CHECK_LAUNCH();
+        cudaFreeAsync(part_o, st);
+        cudaFreeAsync(part_ml, st);
+    }
 }
 
 template <typename T>
