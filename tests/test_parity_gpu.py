@@ -495,3 +495,25 @@ def test_beam_candidates_errors_and_edges(gpu):
     lp1 = np.round(rng.uniform(-4, 0, (512, 1)) * 8) / 8
     live1 = np.round(rng.uniform(-4, 0, 512) * 8) / 8
     _beam_check(E, lp1, live1, 256, 16, 256)
+
+
+def test_fp32_decoder_step_graph_with_split_simt_decode(gpu):
+    """fp32 layers in the CUDA-graph decoder step: at the oracle config the SIMT decode splits
+    the context over CTAs (stream-ordered scratch inside the capture) — the graph equals
+    the eager layer chain."""
+    import torch
+
+    E = gpu
+    h, d_m, d_k, x, n, B, L = 8, 512, 64, 4, 128, 2, 3
+    layers = [E.ElAttentionLayer(E.AttentionParams.random(h, d_m, d_k, E.Rng(10 + l)), E.DTYPE_F32) for l in range(L)]
+    g = torch.Generator(device="cuda").manual_seed(1)
+    H = torch.rand((B, n, d_m), generator=g, device="cuda") * 2 - 1
+    Y = torch.rand((B * x, d_m), generator=g, device="cuda") * 2 - 1
+    dec = E.DecoderStep(layers, H, B, x)
+    got = dec.run(Y).clone()
+    torch.cuda.synchronize()
+    y = Y
+    for ly in layers:
+        y = ly.step(y, H)
+    torch.cuda.synchronize()
+    assert (got - y).abs().max().item() / y.abs().max().item() < 1e-6
