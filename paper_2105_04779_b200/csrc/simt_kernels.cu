@@ -109,7 +109,7 @@ void launch_key_bias_scalars(int dtype, const void* Q, const float* bk, int R, i
 //   S = q'.Hᵀ  -> online softmax (exp2, running max / sum) -> O += P.H.
 // No per-head K/V and no beam-expanded H is ever formed.
 // --------------------------------------------------------------------------
-constexpr int kSimtRows = 16;  // query rows per CTA
+constexpr int kSimtRows = 8;   // query rows per CTA (two CTAs per SM at d_m 1024 fp32)
 constexpr int kSimtTile = 16;  // H rows per tile
 
 template <typename T, int CPT>
@@ -169,18 +169,19 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
             sh[r * ldh + c] = (t0 + r < n) ? to_f32(Hb[(int64_t)(t0 + r) * d_m + c]) : 0.f;
         }
         __syncthreads();
-        // scores, register-blocked: half-warp = one 4 (q rows) x 4 (H rows) block, its 16 lanes
-        // split K (k = lane, lane + 16, ...): 8 shared loads per 16 FMAs; a butterfly
-        // reduce-scatter over the 16 lanes leaves lane s with score (4 rb + s/4, 4 tb + s%4)
+        // scores, register-blocked: warp w = one 4 (q rows) x 4 (H rows) block (2 x 4 blocks
+        // cover 8 x 16), its 32 lanes split K (k = lane, lane + 32, ...): 8 shared loads per 16
+        // FMAs; an xor-16 sum then a butterfly reduce-scatter over 16 lanes leaves lane s
+        // (mod 16) with score (4 rb + s/4, 4 tb + s%4)
         {
-            const int ks = tid & 15, pair = tid >> 4, rb = pair >> 2, tb = pair & 3;
+            const int ks = tid & 31, pair = tid >> 5, rb = pair >> 2, tb = pair & 3;
             float acc_s[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) acc_s[i] = 0.f;
             const float* a = sq + (rb * 4) * ldq;
             const float* hh = sh + (tb * 4) * ldh;
 #pragma unroll 4
-            for (int k = ks; k < d_m; k += 16) {
+            for (int k = ks; k < d_m; k += 32) {
                 float qa[4], hb[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) qa[i] = a[i * ldq + k];
@@ -191,8 +192,8 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
 #pragma unroll
                     for (int j = 0; j < 4; ++j) acc_s[i * 4 + j] = fmaf(qa[i], hb[j], acc_s[i * 4 + j]);
             }
-            // reduce-scatter: at step w (8, 4, 2, 1) keep the half of the values whose index
-            // bit matches this lane's bit, add the partner's copy of it
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc_s[i] += __shfl_xor_sync(0xffffffffu, acc_s[i], 16);
 #pragma unroll
             for (int w = 8; w >= 1; w >>= 1) {
                 const bool upper = (ks & w) != 0;
@@ -203,12 +204,12 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
                     acc_s[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
                 }
             }
-            // lane ks now holds the block element whose index bits equal ks (bit-reversed
-            // accumulation order keeps index == ks): score (4 rb + ks / 4, 4 tb + ks % 4)
-            sp[(rb * 4 + (ks >> 2)) * kSimtTile + tb * 4 + (ks & 3)] = acc_s[0];
+            if (ks < 16) sp[(rb * 4 + (ks >> 2)) * kSimtTile + tb * 4 + (ks & 3)] = acc_s[0];
         }
         __syncthreads();
-        float s = sp[sr * kSimtTile + st_];
+        // softmax threads: 16 per query row (threads past kSimtRows rows idle along)
+        const bool srow = sr < kSimtRows;
+        float s = srow ? sp[sr * kSimtTile + st_] : 0.f;
         __syncthreads();  // sp is rewritten with P below
         s = (t0 + st_ < n) ? s * scale_log2 : -INFINITY;
         float mx = s;
@@ -222,8 +223,8 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
         const float alpha = exp2f(m_run - m_new);  // 0 on the first tile
         l_run = l_run * alpha + sum;
         m_run = m_new;
-        sp[sr * kSimtTile + st_] = p;
-        if (st_ == 0) {
+        if (srow) sp[sr * kSimtTile + st_] = p;
+        if (srow && st_ == 0) {
             s_alpha[sr] = alpha;
             s_l[sr] = l_run;
             s_m[sr] = m_run;
