@@ -22,6 +22,21 @@ int elattn_gpu_testing_gemm_bf16(const void* A, int64_t lda, int64_t sAz, const 
                                  int64_t sbz, int M, int N, int K, int Z, float alpha, int kernel,
                                  elattn_stream_t stream);
 
+/* Force the block shape of the tcgen05 GEMM family for every following bf16 projection
+ * (tests sweep every instantiation; 0 = the automatic per-shape choice): bn in
+ * {64, 128, 256} columns per tile, mt in {1, 2} 128-row m-subtiles per CTA sharing the
+ * B slice, kbp in {1, 2} k-blocks of 64 per TMA box.  Combinations without an
+ * instantiation make the next GEMM fail with ELATTN_ERR_UNSUPPORTED. */
+int elattn_gpu_testing_gemm_config(int bn, int mt, int kbp);
+
+/* Programmatic dependent launch of the step's kernels on (1, default) or off (0). */
+int elattn_gpu_testing_set_pdl(int on);
+
+/* Device buffer (>= 64 u64) receiving %globaltimer stamps of CTA 0 of every following
+ * tcgen05 GEMM launch (setup, each k-step's operands landing, accumulator ready, epilogue
+ * done); NULL disables tracing. */
+int elattn_gpu_testing_set_gemm_trace(unsigned long long* trace);
+
 /* Stage (2) with an explicit kernel choice: 0 = SIMT, 1 = tcgen05. */
 int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H, const int* n_per_input, int B,
                                    int rows, int n, int d_m, float scale, void* ctx, int kernel,

@@ -28,9 +28,6 @@ struct elattn_gpu_params_s {
     float* bk = nullptr;  // [h*d_k]
     float* bv = nullptr;  // [h*d_k] (zero when include_value_bias == 0)
     float* bo = nullptr;  // [d_m]
-    void* bq16 = nullptr;  // bf16 copies of bq / bv / bo for the cuBLASLt bias epilogue (bf16 path only)
-    void* bv16 = nullptr;
-    void* bo16 = nullptr;
 };
 
 namespace elattn_gpu {
@@ -41,6 +38,15 @@ thread_local int64_t g_launches = 0;
 }  // namespace
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+int g_pdl = -1;
+bool pdl_enabled() {
+    if (g_pdl < 0) {
+        const char* e = getenv("ELATTN_PDL");
+        g_pdl = (e && std::string(e) == "0") ? 0 : 1;
+    }
+    return g_pdl != 0;
+}
 void count_launch(int n) { g_launches += n; }
 
 namespace {
@@ -96,7 +102,7 @@ float* upload_f32(const std::vector<double>& v) {
 void free_params(elattn_gpu_params_s* p) {
     if (!p) return;
     for (void* ptr : {p->WqT, p->WkT, p->Wk, p->WvT, p->WoT, (void*)p->bq, (void*)p->bk, (void*)p->bv,
-                      (void*)p->bo, p->bq16, p->bv16, p->bo16})
+                      (void*)p->bo})
         if (ptr) cudaFree(ptr);
     delete p;
 }
@@ -140,32 +146,10 @@ size_t step_workspace(const elattn_gpu_params_s* p, int64_t R) {
     return align256(R * hk * e) * 2 + align256(R * hm * e) * 2;
 }
 
-// Dense projections (Z == 1) go to cuBLASLt; the head-batched EL GEMMs to our tcgen05
-// kernel.  ELATTN_DENSE_GEMM=tc forces the tcgen05 kernel for the dense ones too.
-bool dense_via_lt() {
-    static const bool v = [] {
-        const char* e = getenv("ELATTN_DENSE_GEMM");
-        return !(e && std::string(e) == "tc");
-    }();
-    return v;
-}
-
-// The per-head V projection (K = d_m, N = d_k: 160 tiles of 128 x 64 at B = 320, 1.1 waves
-// on 148 SMs for our persistent kernel) goes to cuBLASLt's strided-batched GEMM, which
-// writes V_i straight into the head-concatenated rows; ELATTN_VPROJ_GEMM=tc keeps it on the
-// tcgen05 kernel.
-bool vproj_via_lt() {
-    static const bool v = [] {
-        const char* e = getenv("ELATTN_VPROJ_GEMM");
-        return !(e && std::string(e) == "tc");
-    }();
-    return v;
-}
-
+// Every bf16 projection runs on the tcgen05 GEMM family (tc_gemm.cu); shapes outside its
+// envelope (K not a multiple of 64, unaligned rows) and the fp32 path use the SIMT kernel.
 void gemm(const elattn_gpu_params_s* p, const GemmArgs& g, cudaStream_t st) {
-    if (p->dtype == ELATTN_DTYPE_BF16 && g.Z == 1 && dense_via_lt() && lt_gemm_supported(g))
-        launch_lt_gemm(g, st);
-    else if (p->dtype == ELATTN_DTYPE_BF16 && tc_gemm_supported(g))
+    if (p->dtype == ELATTN_DTYPE_BF16 && tc_gemm_supported(g))
         launch_tc_gemm(g, st);
     else
         launch_simt_gemm(p->dtype, g, st);
@@ -176,7 +160,7 @@ void query_expansion(const elattn_gpu_params_s* p, const void* Y, int64_t R, voi
                      cudaStream_t st) {
     const int h = p->h, d_m = p->d_m, d_k = p->d_k, hk = h * d_k;
     GemmArgs a{};
-    a.A = Y, a.lda = d_m, a.B = p->WqT, a.ldb = d_m, a.C = Q, a.ldc = hk, a.bias = p->bq, a.bias16 = p->bq16;
+    a.A = Y, a.lda = d_m, a.B = p->WqT, a.ldb = d_m, a.C = Q, a.ldc = hk, a.bias = p->bq;
     a.M = int(R), a.N = hk, a.K = d_m, a.Z = 1, a.alpha = 1.f;
     gemm(p, a, st);
     const size_t e = dtype_bytes(p->dtype);
@@ -186,14 +170,7 @@ void query_expansion(const elattn_gpu_params_s* p, const void* Y, int64_t R, voi
     b.C = qp, b.ldc = int64_t(h) * d_m, b.sCz = d_m;          // row r*h + i
     b.M = int(R), b.N = d_m, b.K = d_k, b.Z = h, b.alpha = 1.f;
     (void)e;
-    static const bool qexp_lt = [] {
-        const char* v = getenv("ELATTN_QEXP_GEMM");
-        return v && std::string(v) == "lt";
-    }();
-    if (qexp_lt && p->dtype == ELATTN_DTYPE_BF16 && lt_gemm_supported(b))
-        launch_lt_gemm(b, st);
-    else
-        gemm(p, b, st);
+    gemm(p, b, st);
 }
 
 // (3a) V_{r,i} = C_{r*h+i}.W_V,i + b_V,i ; (3b) out = V.W_O + b_O   (attention.hpp:283-288)
@@ -203,18 +180,15 @@ void v_projection(const elattn_gpu_params_s* p, const void* C, int64_t R, void* 
     a.A = C, a.lda = int64_t(h) * d_m, a.sAz = d_m;
     a.B = p->WvT, a.ldb = d_m, a.sBz = int64_t(d_k) * d_m;
     a.C = V, a.ldc = hk, a.sCz = d_k;
-    a.bias = p->bv, a.sbz = d_k, a.bias16 = p->bv16;
+    a.bias = p->bv, a.sbz = d_k;
     a.M = int(R), a.N = d_k, a.K = d_m, a.Z = h, a.alpha = 1.f;
-    if (p->dtype == ELATTN_DTYPE_BF16 && vproj_via_lt() && lt_gemm_supported(a))
-        launch_lt_gemm(a, st);
-    else
-        gemm(p, a, st);
+    gemm(p, a, st);
 }
 
 void o_projection(const elattn_gpu_params_s* p, const void* V, int64_t R, void* out, cudaStream_t st) {
     const int d_m = p->d_m, hk = p->h * p->d_k;
     GemmArgs b{};
-    b.A = V, b.lda = hk, b.B = p->WoT, b.ldb = hk, b.C = out, b.ldc = d_m, b.bias = p->bo, b.bias16 = p->bo16;
+    b.A = V, b.lda = hk, b.B = p->WoT, b.ldb = hk, b.C = out, b.ldc = d_m, b.bias = p->bo;
     b.M = int(R), b.N = d_m, b.K = hk, b.Z = 1, b.alpha = 1.f;
     gemm(p, b, st);
 }
@@ -305,11 +279,6 @@ int elattn_gpu_params_create(int h, int d_m, int d_k, int dtype, int include_key
         p->bk = upload_f32(vbk);
         p->bv = upload_f32(vbv);
         p->bo = upload_f32(vbo);
-        if (dtype == ELATTN_DTYPE_BF16) {
-            p->bq16 = upload(vbq, ELATTN_DTYPE_BF16);
-            p->bv16 = upload(vbv, ELATTN_DTYPE_BF16);
-            p->bo16 = upload(vbo, ELATTN_DTYPE_BF16);
-        }
         *out = p.release();
     });
 }
@@ -438,6 +407,24 @@ extern "C" int elattn_gpu_testing_gemm_bf16(const void* A, int64_t lda, int64_t 
     });
 }
 
+extern "C" int elattn_gpu_testing_gemm_config(int bn, int mt, int kbp) {
+    return guarded([&] {
+        ELA_REQUIRE((bn == 0 || bn == 64 || bn == 128 || bn == 256) && mt >= 0 && mt <= 2 && kbp >= 0 && kbp <= 2,
+                    ELATTN_ERR_PARAM, "gemm_config: bn in {0, 64, 128, 256}, mt and kbp in {0, 1, 2}");
+        g_gemm_force_bn = bn, g_gemm_force_mt = mt, g_gemm_force_kbp = kbp;
+    });
+}
+
+extern "C" int elattn_gpu_testing_set_pdl(int on) {
+    g_pdl = on ? 1 : 0;
+    return ELATTN_OK;
+}
+
+extern "C" int elattn_gpu_testing_set_gemm_trace(unsigned long long* trace) {
+    g_gemm_trace = trace;
+    return ELATTN_OK;
+}
+
 extern "C" int elattn_gpu_testing_set_decode_trace(unsigned long long* trace) {
     g_decode_trace = trace;
     return ELATTN_OK;
@@ -473,7 +460,6 @@ struct elattn_gpu_decoder_s {
 
 namespace elattn_gpu {
 void release_stream_scratch(cudaStream_t st);  // el_decode_tc.cu
-void release_lt_stream(cudaStream_t st);       // blas_lt.cu
 }  // namespace elattn_gpu
 
 namespace {
@@ -486,7 +472,6 @@ void decoder_free(elattn_gpu_decoder_s* d) {
     if (d->st) {
         cudaStreamSynchronize(d->st);
         elattn_gpu::release_stream_scratch(d->st);
-        elattn_gpu::release_lt_stream(d->st);
         cudaStreamDestroy(d->st);
     }
     delete d;
@@ -544,8 +529,8 @@ extern "C" int elattn_gpu_decoder_create(const elattn_gpu_params_t* layers, int 
         ELA_CHECK_CUDA(cudaMalloc(&d->ybuf[1], rows_bytes));
         d->ws_bytes = step_workspace(p0, R);
         ELA_CHECK_CUDA(cudaMalloc(&d->ws, d->ws_bytes));
-        // eager run first: allocates this stream's scratch (split records, cuBLASLt
-        // workspace) outside the capture, and surfaces launch errors directly
+        // eager run first: allocates this stream's scratch (split records) outside the
+        // capture, and surfaces launch errors directly
         decoder_enqueue(d.get(), H, n_per_input, Y_in, out);
         ELA_CHECK_CUDA(cudaStreamSynchronize(d->st));
         const int64_t before = g_launches;

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "elattn_gpu.h"
 
@@ -60,5 +61,41 @@ void count_launch(int n = 1);
     } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Programmatic dependent launch (PDL) for the kernels of a layer step: each kernel is
+// launched with programmatic stream serialisation, signals launch_dependents once its
+// prologue (barriers, TMEM allocation) is done and waits (griddepcontrol.wait) before
+// touching data of its predecessors, so launch latency and prologue overlap the previous
+// kernel's tail.  On by default; ELATTN_PDL=0 or elattn_gpu_testing_set_pdl(0) turns it off.
+extern int g_pdl;  // -1 = not yet read from the environment
+bool pdl_enabled();
+
+// cudaLaunchKernelEx with optional cluster dims and the PDL attribute.
+template <typename... KArgs, typename... Args>
+void launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster_x,
+               Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (cluster_x > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = cluster_x;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    if (pdl_enabled()) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    ELA_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 }  // namespace elattn_gpu

@@ -227,7 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const __nv_bfloat16* __restrict__ qp_rows, const int* __restrict__ n_per_input, int B,
                         int rows, int n_stride, int d_m, float scale_log2, __nv_bfloat16* __restrict__ ctx,
                         unsigned long long* __restrict__ trace, DecodeTuning tune, SplitArgs sa,
-                        float2* __restrict__ stats) {
+                        float2* __restrict__ stats, int pdl) {
     using L = DecLayout<UNITS>;
     constexpr int kRing = L::kRing;
     // optional per-tile clock64 trace of the first cluster (testing hook); G = cluster tile index.
@@ -315,6 +315,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::cluster_sync();  // peer barriers initialised before any st.async / remote arrive targets them
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (pdl) {
+        // prologue done (TMEM held): the next kernel may launch; wait for the previous one
+        ptx::griddep_launch_dependents();
+        ptx::griddep_wait();
+    }
 
     if (warp == 0) {
         // ================= TMA producer =================
@@ -933,6 +938,7 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
                                                               __nv_bfloat16* __restrict__ ctx,
                                                               float2* __restrict__ stats, int Bw) {
     constexpr int kPF = kPartFloatsHdr + UNITS * kPartFloatsUnit;
+    ptx::griddep_wait();  // launched with PDL after the decode: its records must be complete
     const int rank = int(blockIdx.y), m = int(blockIdx.z);
     int b, c_first, nseg;
     if (W < 0) {  // tail-split: input Bw + x in P = -W parts on clusters P x .. P x + P - 1 (slot 0)
@@ -1116,15 +1122,16 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
         sa.vchunks = vchunks;
         clusters = B < max_cl ? B : max_cl;
     }
-    kern<<<dim3(2 * clusters), kThreads, smem, st>>>(tq, th, tc, static_cast<const __nv_bfloat16*>(qp), npi, B, rows,
-                                                     n_stride, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx),
-                                                     g_decode_trace, g_tuning, sa, stats);
+    // the kernel is declared with __cluster_dims__(2, 1, 1)
+    launch_ex(kern, dim3(2 * clusters), dim3(kThreads), smem, st, 1, tq, th, tc,
+              static_cast<const __nv_bfloat16*>(qp), npi, B, rows, n_stride, d_m, scale_log2,
+              static_cast<__nv_bfloat16*>(ctx), g_decode_trace, g_tuning, sa, stats, pdl_enabled() ? 1 : 0);
     ELA_CHECK_LAUNCH();
     if (sa.part != nullptr && clusters > 1) {
         const int Bw = B - last_round;
         const int gx = sa.W < 0 ? last_round : clusters - 1;
-        el_decode_merge_kernel<UNITS><<<dim3(gx, 2, UNITS), 256, 0, st>>>(
-            sa.part, sa.T, sa.W, clusters, rows, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx), stats, Bw);
+        launch_ex(el_decode_merge_kernel<UNITS>, dim3(gx, 2, UNITS), dim3(256), 0, st, 1, static_cast<const float*>(sa.part),
+                  sa.T, sa.W, clusters, rows, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx), stats, Bw);
         ELA_CHECK_LAUNCH();
     }
 }

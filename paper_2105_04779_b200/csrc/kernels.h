@@ -24,7 +24,6 @@ struct GemmArgs {
     int64_t sbz;
     int M, N, K, Z;
     float alpha;
-    const void* bias16;  // optional bf16 copy of bias (cuBLASLt's bias epilogue needs D's type)
 };
 void launch_simt_gemm(int dtype, const GemmArgs& g, cudaStream_t st);
 
@@ -40,17 +39,15 @@ void launch_el_decode_simt(int dtype, const void* qp, const void* H, const int* 
                            int B, int rows_per_input, int n_stride, int d_m, float scale,
                            void* ctx, cudaStream_t st, float2* stats = nullptr);
 
-// tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM, bf16 out), same contract as
-// launch_simt_gemm but requires K % 64 == 0, 16-byte aligned rows and
-// N % 16 == 0.  Returns false if the shape is outside its envelope.
+// tcgen05 GEMM family (tc_gemm.cu: bf16 in, fp32 accumulate in TMEM, bf16 out), same
+// contract as launch_simt_gemm but requires K % 64 == 0, 16-byte aligned rows and
+// N % 16 == 0.  tc_gemm_supported returns false outside that envelope.
 bool tc_gemm_supported(const GemmArgs& g);
 void launch_tc_gemm(const GemmArgs& g, cudaStream_t st);
 
-// Plain (Z == 1) bf16 GEMM + bias through cuBLASLt (blas_lt.cu): used for the two dense
-// projections Y.W_Q + b_Q and V.W_O + b_O.  cuBLASLt's bias epilogue takes the bias in
-// the output type, so the bf16 path stores b_Q and b_O in bf16 (GemmArgs::bias16).
-bool lt_gemm_supported(const GemmArgs& g);
-void launch_lt_gemm(const GemmArgs& g, cudaStream_t st);
+// Testing / tuning override of the tcgen05 GEMM block shape (0 = automatic choice).
+extern int g_gemm_force_bn, g_gemm_force_mt, g_gemm_force_kbp;
+extern unsigned long long* g_gemm_trace;
 
 // Mixed self-attention merge (mixed.cu): see the file header.
 void launch_mixed_combine(int dtype, const void* Q, const float2* stats, void* V, const void* Kc, const void* Vc,

@@ -1,22 +1,28 @@
-// tc_gemm.cu — persistent tcgen05 GEMM for the projection stages of the bf16 path.
+// tc_gemm.cu — tcgen05 GEMM family for the projection stages of the bf16 path.
 //
 //   C[z][m][n] = alpha * sum_k A[z][m][k] * B[z][n][k] + bias[z][n]     (bf16 in/out)
 //
 // Replaces the reference's CPU matmuls of query expansion (attention.hpp:205-206:
-// q.Wq_i + bq_i, Q_i.Wk_i^T) and of the output projection (:286, :221-231:
-// ctx.Wv_i + bv_i, then .Wo + bo).
+// q.Wq_i + bq_i, then Q_i.Wk_i^T) and of the output projection (:283-288 with
+// el_bias_terms :221-231: ctx.Wv_i + bv_i, then .Wo + bo).  Every projection of a layer
+// step runs here (no vendor BLAS on the path).
 //
-// Persistent, warp-specialised: one CTA per SM walks 128 x BN output tiles
-// (n fastest, so consecutive tiles reuse the A block from L2).
-//   warp 0      TMA producer: 128x64 / BNx64 bf16 K-slices (SWIZZLE_128B) through an
-//               mbarrier ring;
-//   warp 1      MMA issuer (tcgen05.mma M=128 N=BN K=16, fp32 accumulator in TMEM,
-//               double-buffered so the epilogue of tile t overlaps the MMAs of t+1);
-//   warps 2..9  epilogue, two warps per TMEM lane quadrant (column halves):
-//               tcgen05.ld -> alpha/bias -> bf16 -> SWIZZLE_128B smem stage (double
-//               buffered) -> TMA tensor store (3-D maps, so head-strided outputs such
-//               as q' rows r*h + i are written directly).  The write-bound shapes
-//               (q' = Q_i.Wk_i^T: K = 64, 42 MB out at B = 320) live in this epilogue.
+// Persistent, warp-specialised.  A CTA owns MT m-subtiles of 128 rows x BN columns that
+// share each staged B slice (MT = 2 halves the weight traffic of the per-head V
+// projection, whose N = d_k = 64).  Measured on B200 (tools/probes/l2_ingress_probe.cu,
+// gemm_ingress_probe.cu): a CTA's TMA ingress is bounded by the number of boxes in flight,
+// not by L2 bandwidth — one 16 KB box per ~800 cycles — so every stage moves KBP k-blocks
+// per operand in ONE 4-D box (64 x rows x KBP k-blocks, the k-block dimension strided by
+// 128 B inside the row-major operand), and the epilogue stores 128-row boxes written by
+// four warps together instead of 32-row boxes per warp.
+//   warp 0      TMA producer (KBP k-blocks of MT A subtiles + the B slice per stage);
+//   warp 1      MMA issuer: tcgen05.mma M=128 N=BN K=16, fp32 accumulators in TMEM,
+//               double-buffered so the epilogue of tile t overlaps the MMAs of t+1;
+//   warps 2..9  epilogue: two groups of four warps (one per TMEM lane quadrant), group g
+//               owns column half g; per 64-column block: tcgen05.ld -> alpha/bias -> bf16
+//               -> SWIZZLE_128B stage (128 rows) -> one TMA tensor store (3-D maps, so
+//               head-strided outputs such as q' rows r*h + i and V_i columns i*d_k are
+//               written in place).
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx_sm100.cuh"
@@ -24,54 +30,73 @@
 
 namespace elattn_gpu {
 
+int g_gemm_force_bn = 0, g_gemm_force_mt = 0, g_gemm_force_kbp = 0;  // testing / tuning override (0 = auto)
+unsigned long long* g_gemm_trace = nullptr;                            // testing: timeline of CTA 0
+
 namespace {
 
 constexpr int kBM = 128, kBK = 64;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
-template <int BN>
+template <int BN, int MT, int KBP>
 struct GemmSmem {
-    static constexpr uint32_t kABytes = kBM * kBK * 2;
-    static constexpr uint32_t kBBytes = BN * kBK * 2;
-    static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    // epilogue: every warp stages its own 32 rows x BN/2 columns as 32-row x 64-column
-    // SWIZZLE_128B boxes (4 KB each) and stores them itself, double buffered
-    static constexpr int kBoxCols = BN / 2 < 64 ? BN / 2 : 64;  // 64 (SW128) or 32 (SW64)
-    static constexpr uint32_t kWarpBox = 32 * kBoxCols * 2;
-    static constexpr uint32_t kWarpStage = (BN / 2) / kBoxCols * kWarpBox;
-    static constexpr int kOutStages = 3;
-    static constexpr uint32_t kOutBytes = kEpiWarps * kOutStages * kWarpStage;
-    static constexpr uint32_t kFixed = kOutBytes + 256 + 1024;
-    static constexpr int kStagesFit = int((232448u - kFixed) / kStageBytes);
+    static constexpr uint32_t kABytes = kBM * kBK * 2;  // one m-subtile, one k-block
+    static constexpr uint32_t kBBytes = BN * kBK * 2;   // the B slice, one k-block
+    static constexpr uint32_t kStageBytes = KBP * (MT * kABytes + kBBytes);
+    // epilogue: per group (column half) blocks of 128 rows x kPiece columns
+    // (64 -> SWIZZLE_128B, 32 -> SWIZZLE_64B)
+    static constexpr int kHalf = BN / 2;
+    static constexpr int kPiece = kHalf < 64 ? kHalf : 64;
+    static constexpr uint32_t kPieceBytes = kBM * kPiece * 2;
+    static constexpr uint32_t kFixedNoOut = 256 + 1024;
+    // two stage buffers per group unless that leaves fewer than three operand stages
+    static constexpr int kStages2 = int((232448u - kFixedNoOut - 2 * 2 * kPieceBytes) / kStageBytes);
+    static constexpr int kOutBufs = kStages2 >= 3 ? 2 : 1;
+    static constexpr uint32_t kOutBytes = 2 * kOutBufs * kPieceBytes;
+    static constexpr int kStagesFit = int((232448u - kFixedNoOut - kOutBytes) / kStageBytes);
     static constexpr int kStages = kStagesFit < 8 ? kStagesFit : 8;
     static constexpr uint32_t kOutOff = kStages * kStageBytes;
     static constexpr uint32_t kBarOff = kOutOff + kOutBytes;
     static constexpr uint32_t kTotal = kBarOff + 256 + 1024;  // + barriers + alignment slack
+    static constexpr uint32_t kAccCols = MT * BN;              // one accumulator set
+    static constexpr uint32_t kTmemCols =
+        2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : (2 * kAccCols <= 256 ? 256 : 512));
+    static_assert(2 * kAccCols <= 512, "TMEM: two accumulator sets");
+    static_assert(kStages >= 2, "smem ring");
     static_assert(kTotal <= 232448, "smem");
 };
 
 struct GemmParams {
     int M, N, K, Z;
-    int tiles_m, tiles_n;
+    int tiles_m, tiles_n;  // tiles_m counts MT-subtile groups of 128 rows
     float alpha;
     const float* bias;
     int64_t sbz;
-    int a_zm, b_zm, c_zm;  // 1: tensor map coordinate order is (k, z, m) instead of (k, m, z)
-    int a_bcast;  // A shared by every z (sAz == 0): load it with z = 0
+    int a_zm, b_zm, c_zm;  // 1: tensor map coordinate order is (k, z, m, ..) instead of (k, m, z, ..)
+    int a_bcast;           // A shared by every z (sAz == 0): load it with z = 0
+    int pdl;               // wait for the preceding kernel (programmatic dependent launch)
+    unsigned long long* trace;  // testing: %globaltimer stamps of CTA 0 (null = off)
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN, bool BIAS, bool SCALE>
+__device__ __forceinline__ void group_bar(uint32_t id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
+
+template <int BN, int MT, int KBP, bool BIAS, bool SCALE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmParams p) {
-    using S = GemmSmem<BN>;
+    using S = GemmSmem<BN, MT, KBP>;
     constexpr int kStages = S::kStages;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B, by offsetting the __shared__ array itself so
@@ -83,18 +108,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* acc_full = empty + kStages;  // [2] MMA -> epilogue
     uint64_t* acc_empty = acc_full + 2;    // [2] epilogue -> MMA
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-    constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-    const int num_k = p.K / kBK;
+    const bool tr = p.trace != nullptr && blockIdx.x == 0;
+    if (tr && threadIdx.x == 0) p.trace[0] = gtimer();
+    const int num_kb = p.K / kBK;
+    const int num_ks = (num_kb + KBP - 1) / KBP;  // stages per tile (the last may run past K: zero-filled)
     const int num_tiles = p.Z * p.tiles_m * p.tiles_n;
     // z (head) fastest: the CTAs running concurrently touch the SAME rows r of the
-    // head-interleaved layouts (q' / C rows r*h + i), so their 128-byte row pieces land
-    // in the same DRAM pages instead of 32 KB apart
+    // head-interleaved layouts (q' / C rows r*h + i), so their row pieces land in the same
+    // DRAM pages; then n, so neighbouring CTAs share the A rows in L2
     auto tile_coords = [&](int t, int& z, int& m0, int& n0) {
         z = t % p.Z;
         const int r = t / p.Z;
-        m0 = (r / p.tiles_n) * kBM;
+        m0 = (r / p.tiles_n) * (MT * kBM);
         n0 = (r % p.tiles_n) * BN;
     };
 
@@ -115,35 +142,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
     } else if (warp == 1) {
-        ptx::tmem_alloc<kTmemCols>(tmem_slot);
+        ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
     }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (p.pdl) {
+        // prologue done (TMEM held): the next kernel may launch; wait for the previous one
+        ptx::griddep_launch_dependents();
+        ptx::griddep_wait();
+    }
+    if (tr && threadIdx.x == 0) p.trace[1] = gtimer();
 
     if (warp == 0) {
-        // ---- TMA producer
+        // ---- TMA producer: per stage one 4-D box per A subtile and one for B
         if (ptx::elect_one()) {
             int it = 0;
             for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
                 int z, m0, n0;
                 tile_coords(t, z, m0, n0);
-                for (int kb = 0; kb < num_k; ++kb, ++it) {
+                const int za = p.a_bcast ? 0 : z;
+                for (int ks = 0; ks < num_ks; ++ks, ++it) {
                     const int s = it % kStages;
                     ptx::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
                     uint8_t* a = smem + s * S::kStageBytes;
-                    uint8_t* b = a + S::kABytes;
+                    uint8_t* b = a + KBP * MT * S::kABytes;
                     ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
-                    const int za = p.a_bcast ? 0 : z;
-                    if (p.a_zm)
-                        ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, za, m0, ptx::kEvictNormal);
-                    else
-                        ptx::tma_load_3d(a, &tmA, &full[s], kb * kBK, m0, za, ptx::kEvictNormal);
+                    const int kb = ks * KBP;
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        uint8_t* dst = a + mt * KBP * S::kABytes;  // [kb][128 rows][64]
+                        if (p.a_zm)
+                            ptx::tma_load_4d(dst, &tmA, &full[s], 0, za, m0 + mt * kBM, kb, ptx::kEvictNormal);
+                        else
+                            ptx::tma_load_4d(dst, &tmA, &full[s], 0, m0 + mt * kBM, za, kb, ptx::kEvictNormal);
+                    }
                     if (p.b_zm)
-                        ptx::tma_load_3d(b, &tmB, &full[s], kb * kBK, z, n0, ptx::kEvictLast);
+                        ptx::tma_load_4d(b, &tmB, &full[s], 0, z, n0, kb, ptx::kEvictLast);
                     else
-                        ptx::tma_load_3d(b, &tmB, &full[s], kb * kBK, n0, z, ptx::kEvictLast);
+                        ptx::tma_load_4d(b, &tmB, &full[s], 0, n0, z, kb, ptx::kEvictLast);
                 }
             }
         }
@@ -157,17 +195,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int ab = local & 1;
             ptx::mbar_wait(&acc_empty[ab], ((local >> 1) & 1) ^ 1);
             ptx::tc_fence_after();
-            const uint32_t d = tmem + ab * BN;
-            for (int kb = 0; kb < num_k; ++kb, ++it) {
+            const uint32_t d = tmem + ab * S::kAccCols;
+            for (int ks = 0; ks < num_ks; ++ks, ++it) {
                 const int s = it % kStages;
                 ptx::mbar_wait(&full[s], (it / kStages) & 1);
                 ptx::tc_fence_after();
+                if (tr && lane == 0 && it < 32) p.trace[2 + it] = gtimer();
                 if (lane == 0) {
                     const uint64_t a = d0 + uint64_t((s * S::kStageBytes) >> 4);
-                    const uint64_t b = a + uint64_t(S::kABytes >> 4);
+                    const uint64_t b = a + uint64_t((KBP * MT * S::kABytes) >> 4);
+                    const int nk = min(KBP, num_kb - ks * KBP);
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k)
-                        ptx::mma_bf16(d, a + uint64_t(2 * k), b + uint64_t(2 * k), idesc, (kb | k) != 0);
+                    for (int j = 0; j < KBP; ++j) {
+                        if (j >= nk) break;
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                            for (int k = 0; k < kBK / 16; ++k)
+                                ptx::mma_bf16(d + mt * BN,
+                                              a + uint64_t(((mt * KBP + j) * S::kABytes) >> 4) + uint64_t(2 * k),
+                                              b + uint64_t((j * S::kBBytes) >> 4) + uint64_t(2 * k), idesc,
+                                              (ks | j | k) != 0);
+                    }
                     ptx::mma_commit(&empty[s]);
                 }
                 __syncwarp();
@@ -176,115 +225,149 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
         }
     } else {
-        // ---- epilogue warps 2..9: quadrant qd = warp % 4 (TMEM lanes / tile rows
-        // 32 qd..), column half ch = (warp - 2) / 4 (tile columns ch*BN/2 ..).  Each warp
-        // is independent: TMEM -> registers -> its own SWIZZLE_128B stage -> its own TMA
-        // store (boxes of 32 rows x 64 columns); no CTA-wide barrier in the tile loop.
-        const uint32_t qd = warp & 3, ch = (warp - 2) >> 2;
-        constexpr int kHalf = BN / 2;
-        uint8_t* my_stage = out_stage + (warp - 2) * S::kOutStages * S::kWarpStage;
-        int local = 0;
+        // ---- epilogue: group g = column half (warps 2..5 -> 0, 6..9 -> 1); within a group
+        // warp w reads TMEM lane quadrant qd = w % 4 (rows 32 qd ..).  Per block of kPiece
+        // columns the four warps fill one 128-row stage and warp (w - 2) % 4 == 0 stores it.
+        const uint32_t qd = warp & 3, grp = (warp - 2) >> 2;
+        const bool leader = ((warp - 2) & 3) == 0 && lane == 0;
+        constexpr int kHalf = S::kHalf, kPiece = S::kPiece;
+        uint8_t* grp_stage = out_stage + grp * S::kOutBufs * S::kPieceBytes;
+        const uint32_t bar_id = 1 + grp;
+        int local = 0, piece = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
             int z, m0, n0;
             tile_coords(t, z, m0, n0);
             const int ab = local & 1;
-            uint8_t* stage = my_stage + (local % S::kOutStages) * S::kWarpStage;
-            ptx::mbar_wait(&acc_full[ab], (local >> 1) & 1);
-            ptx::tc_fence_after();
-            const uint32_t t_row = tmem + ((qd * 32) << 16) + ab * BN + ch * kHalf;
-            uint32_t rr[kHalf];  // this warp's 32 rows x kHalf columns, one TMEM round trip
-#pragma unroll
-            for (int c0 = 0; c0 < kHalf; c0 += 32) ptx::tmem_ld32(t_row + c0, *reinterpret_cast<uint32_t(*)[32]>(&rr[c0]));
-            ptx::tmem_ld_wait();
-            // this warp's part of the accumulator is read: the MMA warp may reuse it
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                ptx::mbar_arrive(&acc_empty[ab]);
-                ptx::bulk_wait_group_read<S::kOutStages - 1>();  // this stage's previous store has read it
-            }
-            __syncwarp();
-            // bias of this warp's columns: lane l holds column c0 + l of each 32-column
-            // chunk, broadcast with shuffles (no per-element loads)
+            // bias of this warp's columns (lane l: column 32 c + l of the half), loaded
+            // before the accumulator is ready
             float bcol[kHalf / 32];
             if constexpr (BIAS) {
 #pragma unroll
                 for (int c = 0; c < kHalf / 32; ++c) {
-                    const int n = n0 + int(ch) * kHalf + 32 * c + int(lane);
+                    const int n = n0 + int(grp) * kHalf + 32 * c + int(lane);
                     bcol[c] = n < p.N ? __ldg(p.bias + z * p.sbz + n) : 0.f;
                 }
             }
+            ptx::mbar_wait(&acc_full[ab], (local >> 1) & 1);
+            ptx::tc_fence_after();
+            if (tr && warp == 2 && lane == 0 && local < 8) p.trace[34 + 2 * local] = gtimer();
+#pragma unroll 1
+            for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll 1
+                for (int c0 = 0; c0 < kHalf; c0 += kPiece, ++piece) {
+                    const uint32_t t_row =
+                        tmem + ((qd * 32) << 16) + ab * S::kAccCols + mt * BN + grp * kHalf + c0;
+                    uint32_t rr[kPiece];
 #pragma unroll
-            for (int c0 = 0; c0 < kHalf; c0 += 32) {
-                const uint32_t* r = rr + c0;
-                uint32_t packed[16];
-#pragma unroll
-                for (int j = 0; j < 32; j += 2) {
-                    float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
-                    if constexpr (SCALE) v0 *= p.alpha, v1 *= p.alpha;
-                    if constexpr (BIAS) {
-                        v0 += __shfl_sync(0xffffffffu, bcol[c0 / 32], j);
-                        v1 += __shfl_sync(0xffffffffu, bcol[c0 / 32], j + 1);
+                    for (int c = 0; c < kPiece; c += 32)
+                        ptx::tmem_ld32(t_row + c, *reinterpret_cast<uint32_t(*)[32]>(&rr[c]));
+                    ptx::tmem_ld_wait();
+                    if (mt == MT - 1 && c0 + kPiece >= kHalf) {
+                        // this warp's part of the accumulator is read: the MMA warp may reuse it
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
                     }
-                    packed[j / 2] = pack2(v0, v1);
-                }
-                // 32-row box of kBoxCols columns: SWIZZLE_128B (16-byte chunk c of row l at
-                // c ^ (l & 7)) for 64 columns, SWIZZLE_64B (c ^ ((l >> 1) & 3)) for 32
-                constexpr int kBoxCols = S::kBoxCols;
-                uint8_t* box = stage + (c0 / kBoxCols) * S::kWarpBox + lane * (kBoxCols * 2);
-                const int cbase = (c0 % kBoxCols) >> 3;
-                const int sw = kBoxCols == 64 ? int(lane & 7) : int((lane >> 1) & 3);
+                    uint8_t* stage = grp_stage + (piece % S::kOutBufs) * S::kPieceBytes;
+                    // the store that last used this buffer has read it
+                    if (leader) ptx::bulk_wait_group_read<S::kOutBufs - 1>();
+                    group_bar(bar_id);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    *reinterpret_cast<uint4*>(box + (((cbase + q) ^ sw) << 4)) =
-                        make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-            }
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
+                    for (int cc = 0; cc < kPiece; cc += 32) {
+                        uint32_t packed[16];
 #pragma unroll
-                for (int bx = 0; bx < kHalf / S::kBoxCols; ++bx) {
-                    const int c0 = n0 + int(ch) * kHalf + S::kBoxCols * bx;
-                    if (c0 >= p.N) break;
-                    const int r0 = m0 + int(qd) * 32;
-                    if (p.c_zm)
-                        ptx::tma_store_3d(&tmC, stage + bx * S::kWarpBox, c0, z, r0);
-                    else
-                        ptx::tma_store_3d(&tmC, stage + bx * S::kWarpBox, c0, r0, z);
+                        for (int j = 0; j < 32; j += 2) {
+                            float v0 = __uint_as_float(rr[cc + j]), v1 = __uint_as_float(rr[cc + j + 1]);
+                            if constexpr (SCALE) v0 *= p.alpha, v1 *= p.alpha;
+                            if constexpr (BIAS) {
+                                const float bc = bcol[(c0 + cc) / 32];
+                                v0 += __shfl_sync(0xffffffffu, bc, j);
+                                v1 += __shfl_sync(0xffffffffu, bc, j + 1);
+                            }
+                            packed[j / 2] = pack2(v0, v1);
+                        }
+                        // row 32 qd + lane: SWIZZLE_128B (16-byte chunk c of row l at c ^ (l & 7))
+                        // for 64-column blocks, SWIZZLE_64B (c ^ ((l >> 1) & 3)) for 32
+                        uint8_t* row = stage + (qd * 32 + lane) * (kPiece * 2);
+                        const int cbase = cc >> 3;
+                        const int sw = kPiece == 64 ? int(lane & 7) : int((lane >> 1) & 3);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            *reinterpret_cast<uint4*>(row + (((cbase + q) ^ sw) << 4)) =
+                                make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                    }
+                    ptx::fence_proxy_async_smem();
+                    group_bar(bar_id);
+                    if (leader) {
+                        const int nbase = n0 + int(grp) * kHalf + c0, r0 = m0 + mt * kBM;
+                        if (nbase < p.N && r0 < p.M) {
+                            if (p.c_zm)
+                                ptx::tma_store_3d(&tmC, stage, nbase, z, r0);
+                            else
+                                ptx::tma_store_3d(&tmC, stage, nbase, r0, z);
+                        }
+                        ptx::bulk_commit_group();
+                    }
                 }
-                ptx::bulk_commit_group();
             }
         }
-        if (lane == 0) ptx::bulk_wait_group<0>();
+        // the smem stages must stay valid until the stores have read them (global
+        // visibility of TMA stores is guaranteed at grid completion)
+        if (leader) ptx::bulk_wait_group_read<0>();
         __syncwarp();
+        if (tr && warp == 2 && lane == 0) p.trace[50] = gtimer();
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<kTmemCols>(tmem);
+        ptx::tmem_dealloc<S::kTmemCols>(tmem);
     }
 }
 
-// 3-D map over an operand X[z][r][k] (r = M or N rows, k contiguous):
-// returns the map and whether coordinates are ordered (k, z, r).
-CUtensorMap operand_map(const void* base, int64_t ld, int64_t sz, int rows, int K, int Z, uint32_t box_rows,
-                        int* zr_order, int box_k = kBK) {
-    const int swz = box_k * 2;  // 128-byte rows -> SWIZZLE_128B, 64-byte -> SWIZZLE_64B
-    const uint64_t ld_b = uint64_t(ld) * 2;
-    uint64_t sz_b = uint64_t(sz) * 2;
+// Maps over an operand X[z][r][k] (r = M or N rows, k contiguous).  Loads use 4-D maps
+// (64 k, r | z, z | r, k-block) whose k-block dimension has stride 128 B, so one box
+// carries `kbp` k-blocks of `box_rows` rows as [kb][row][64] — KBP SWIZZLE_128B K-major
+// slabs back to back.  Stores (and loads of C-shaped operands) use 3-D maps (k, r, z).
+// zr_order: 1 if the coordinates are ordered (k, z, r) (keeps the r/z strides monotonic).
+void dims_rz(int64_t ld, int64_t sz, int rows, int Z, uint64_t& ld_b, uint64_t& sz_b, int* zr_order) {
+    ld_b = uint64_t(ld) * 2;
+    sz_b = uint64_t(sz) * 2;
     if (Z == 1 || sz == 0) sz_b = ld_b * uint64_t(rows);
-    if (sz_b < ld_b && Z > 1) {  // keep strides monotonic: dims (k, z, r)
-        const uint64_t dims[3] = {uint64_t(K), uint64_t(Z), uint64_t(rows)};
+    *zr_order = (sz_b < ld_b && Z > 1) ? 1 : 0;
+}
+
+CUtensorMap load_map(const void* base, int64_t ld, int64_t sz, int rows, int K, int Z, uint32_t box_rows, int kbp,
+                     int* zr_order) {
+    uint64_t ld_b, sz_b;
+    dims_rz(ld, sz, rows, Z, ld_b, sz_b, zr_order);
+    const uint64_t nkb = uint64_t(K / kBK);
+    if (*zr_order) {
+        const uint64_t dims[4] = {uint64_t(kBK), uint64_t(Z), uint64_t(rows), nkb};
+        const uint64_t strides[3] = {sz_b, ld_b, uint64_t(kBK) * 2};
+        const uint32_t box[4] = {uint32_t(kBK), 1, box_rows, uint32_t(kbp)};
+        return make_tmap_bf16(base, 4, dims, strides, box, 128);
+    }
+    const uint64_t dims[4] = {uint64_t(kBK), uint64_t(rows), uint64_t(Z), nkb};
+    const uint64_t strides[3] = {ld_b, sz_b, uint64_t(kBK) * 2};
+    const uint32_t box[4] = {uint32_t(kBK), box_rows, 1, uint32_t(kbp)};
+    return make_tmap_bf16(base, 4, dims, strides, box, 128);
+}
+
+CUtensorMap store_map(const void* base, int64_t ld, int64_t sz, int rows, int N, int Z, uint32_t box_rows,
+                      int box_cols, int* zr_order) {
+    uint64_t ld_b, sz_b;
+    dims_rz(ld, sz, rows, Z, ld_b, sz_b, zr_order);
+    const int swz = box_cols * 2;  // 128-byte rows -> SWIZZLE_128B, 64-byte -> SWIZZLE_64B
+    if (*zr_order) {
+        const uint64_t dims[3] = {uint64_t(N), uint64_t(Z), uint64_t(rows)};
         const uint64_t strides[2] = {sz_b, ld_b};
-        const uint32_t box[3] = {uint32_t(box_k), 1, box_rows};
-        *zr_order = 1;
+        const uint32_t box[3] = {uint32_t(box_cols), 1, box_rows};
         return make_tmap_bf16(base, 3, dims, strides, box, swz);
     }
-    const uint64_t dims[3] = {uint64_t(K), uint64_t(rows), uint64_t(Z)};
+    const uint64_t dims[3] = {uint64_t(N), uint64_t(rows), uint64_t(Z)};
     const uint64_t strides[2] = {ld_b, sz_b};
-    const uint32_t box[3] = {uint32_t(box_k), box_rows, 1};
-    *zr_order = 0;
+    const uint32_t box[3] = {uint32_t(box_cols), box_rows, 1};
     return make_tmap_bf16(base, 3, dims, strides, box, swz);
 }
 
@@ -297,28 +380,67 @@ int num_sms() {
     return n;
 }
 
-template <int BN, bool BIAS, bool SCALE>
-void launch_bn(const GemmArgs& g, cudaStream_t st) {
+template <int BN, int MT, int KBP, bool BIAS, bool SCALE>
+void launch_cfg(const GemmArgs& g, cudaStream_t st) {
+    using S = GemmSmem<BN, MT, KBP>;
     GemmParams p{};
     p.M = g.M, p.N = g.N, p.K = g.K, p.Z = g.Z, p.alpha = g.alpha, p.bias = g.bias, p.sbz = g.sbz;
-    p.tiles_m = int(ceil_div(g.M, kBM));
+    p.tiles_m = int(ceil_div(g.M, int64_t(kBM) * MT));
     p.tiles_n = int(ceil_div(g.N, BN));
     p.a_bcast = (g.Z > 1 && g.sAz == 0) ? 1 : 0;
-    CUtensorMap ta = operand_map(g.A, g.lda, g.sAz, g.M, g.K, p.a_bcast ? 1 : g.Z, kBM, &p.a_zm);
-    CUtensorMap tb = operand_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, BN, &p.b_zm);
-    // output C[z][m][n]: boxes of 32 rows x kBoxCols columns (one epilogue warp's piece),
-    // clipped at M / N
-    CUtensorMap tc = operand_map(g.C, g.ldc, g.sCz, g.M, g.N, g.Z, 32, &p.c_zm, GemmSmem<BN>::kBoxCols);
-    auto kern = tc_gemm_kernel<BN, BIAS, SCALE>;
-    constexpr uint32_t smem = GemmSmem<BN>::kTotal;
+    p.pdl = pdl_enabled() ? 1 : 0;
+    p.trace = g_gemm_trace;
+    CUtensorMap ta = load_map(g.A, g.lda, g.sAz, g.M, g.K, p.a_bcast ? 1 : g.Z, kBM, KBP, &p.a_zm);
+    CUtensorMap tb = load_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, BN, KBP, &p.b_zm);
+    CUtensorMap tc = store_map(g.C, g.ldc, g.sCz, g.M, g.N, g.Z, kBM, S::kPiece, &p.c_zm);
+    auto kern = tc_gemm_kernel<BN, MT, KBP, BIAS, SCALE>;
+    constexpr uint32_t smem = S::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const int tiles = p.Z * p.tiles_m * p.tiles_n;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, kThreads, smem, st>>>(ta, tb, tc, p);
+    // a stage always expects KBP full k-blocks: a short last stage (K / 64 not a multiple
+    // of KBP) is completed by the zero-filled out-of-range part of the box
+    launch_ex(kern, dim3(grid), dim3(kThreads), smem, st, 1, ta, tb, tc, p);
     ELA_CHECK_LAUNCH();
 }
 
+template <int BN, int MT, int KBP>
+void launch_variant(const GemmArgs& g, cudaStream_t st) {
+    const bool bias = g.bias != nullptr, scale = g.alpha != 1.f;
+    if (bias && scale) return launch_cfg<BN, MT, KBP, true, true>(g, st);
+    if (bias) return launch_cfg<BN, MT, KBP, true, false>(g, st);
+    if (scale) return launch_cfg<BN, MT, KBP, false, true>(g, st);
+    return launch_cfg<BN, MT, KBP, false, false>(g, st);
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+struct Cfg {
+    int bn, mt, kbp;
+};
+
+// Block shape per GEMM (B200, 148 SMs):
+//   * N <= 64 (per-head V projection, N = d_k): 128 x 64 tiles, two m-subtiles per CTA
+//     sharing the weight slice when that still leaves one wave;
+//   * K <= 128 (q' expansion, write-bound): 128 x 256 tiles, one k-step;
+//   * otherwise (Y.W_Q, V.W_O): 128 x 128 tiles;
+// with two k-blocks per TMA box whenever K allows.
+Cfg choose(const GemmArgs& g) {
+    Cfg c{128, 1, 2};
+    if (g.N <= 64) {
+        c = {64, 1, 2};
+        const int64_t tiles = ceil_div(g.M, kBM) * g.Z;
+        if (g.K >= 256 && tiles > num_sms()) c.mt = 2;
+    } else if (g.K <= 128) {
+        c = {g.N >= 256 ? 256 : 128, 1, 1};
+    }
+    if (g.K / kBK < 2) c.kbp = 1;
+    if (g_gemm_force_bn) c.bn = g_gemm_force_bn;
+    if (g_gemm_force_mt) c.mt = g_gemm_force_mt;
+    if (g_gemm_force_kbp) c.kbp = g_gemm_force_kbp;
+    if (c.bn > 64 && g.N <= 64) c.bn = 64;
+    return c;
+}
 
 }  // namespace
 
@@ -328,20 +450,24 @@ bool tc_gemm_supported(const GemmArgs& g) {
            aligned16(g.B) && aligned16(g.C);
 }
 
-template <int BN>
-void launch_variant(const GemmArgs& g, cudaStream_t st) {
-    const bool bias = g.bias != nullptr, scale = g.alpha != 1.f;
-    if (bias && scale) return launch_bn<BN, true, true>(g, st);
-    if (bias) return launch_bn<BN, true, false>(g, st);
-    if (scale) return launch_bn<BN, false, true>(g, st);
-    return launch_bn<BN, false, false>(g, st);
-}
-
 void launch_tc_gemm(const GemmArgs& g, cudaStream_t st) {
-    if (g.N <= 64)
-        launch_variant<64>(g, st);
-    else
-        launch_variant<128>(g, st);
+    const Cfg c = choose(g);
+    const int key = c.bn * 100 + c.mt * 10 + c.kbp;
+    switch (key) {
+        case 6411: return launch_variant<64, 1, 1>(g, st);
+        case 6412: return launch_variant<64, 1, 2>(g, st);
+        case 6421: return launch_variant<64, 2, 1>(g, st);
+        case 6422: return launch_variant<64, 2, 2>(g, st);
+        case 12811: return launch_variant<128, 1, 1>(g, st);
+        case 12812: return launch_variant<128, 1, 2>(g, st);
+        case 12821: return launch_variant<128, 2, 1>(g, st);
+        case 12822: return launch_variant<128, 2, 2>(g, st);
+        case 25611: return launch_variant<256, 1, 1>(g, st);
+        case 25612: return launch_variant<256, 1, 2>(g, st);
+        default:
+            throw Status{ELATTN_ERR_UNSUPPORTED, "tc_gemm: no instantiation for BN " + std::to_string(c.bn) +
+                                                     " MT " + std::to_string(c.mt) + " KBP " + std::to_string(c.kbp)};
+    }
 }
 
 }  // namespace elattn_gpu

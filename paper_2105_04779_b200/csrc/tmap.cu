@@ -28,9 +28,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                            const uint32_t* box, int swizzle_bytes) {
     CUtensorMap m;
-    cuuint32_t elem_strides[3] = {1, 1, 1};
-    cuuint64_t gdims[3], gstrides[2];
-    cuuint32_t boxd[3];
+    ELA_REQUIRE(rank >= 1 && rank <= 5, ELATTN_ERR_PARAM, "tensor map rank must be 1..5");
+    cuuint32_t elem_strides[5] = {1, 1, 1, 1, 1};
+    cuuint64_t gdims[5], gstrides[4];
+    cuuint32_t boxd[5];
     for (int i = 0; i < rank; ++i) {
         gdims[i] = dims[i];
         boxd[i] = box[i];

@@ -9,7 +9,8 @@
 
 namespace elattn_gpu {
 
-// bf16 tensor map with up to 3 dims (dim 0 innermost, contiguous).
+// bf16 tensor map with up to 5 dims (dim 0 innermost, contiguous; the other strides need
+// not be monotonic, e.g. a k-block dimension of stride 128 B inside [rows][K]).
 // dims/box in elements, strides (for dims 1..rank-1) in bytes; swizzle_bytes in
 // {0, 32, 64, 128} (default SWIZZLE_128B); out-of-bounds elements are filled with zeros
 // on loads and clipped on stores.

@@ -69,6 +69,32 @@ def test_gemm_vs_torch(kernel, M, N, K, Z, layout):
     assert err < 1e-2, err
 
 
+@pytest.mark.parametrize("bn,mt,kbp", [
+    (64, 1, 1), (64, 2, 1), (64, 1, 2), (64, 2, 2),
+    (128, 1, 1), (128, 2, 1), (128, 1, 2), (128, 2, 2),
+    (256, 1, 1), (256, 1, 2),
+])
+@pytest.mark.parametrize("M,N,K,Z,layout", [
+    (1280, 1024, 1024, 1, "plain"),     # Q = Y.W_Q / out = V.W_O (BART, B = 320)
+    (300, 64, 1024, 16, "heads"),       # V_i = C_i.W_V,i shape class, M tail
+    (1280, 1024, 64, 16, "heads"),      # q' expansion (BART, B = 320)
+    (77, 192, 128, 3, "plain"),         # M and N tails
+    (140, 128, 192, 2, "heads"),        # K / 64 odd: the last 2-k-block box runs past K
+])
+def test_gemm_block_shapes(bn, mt, kbp, M, N, K, Z, layout):
+    """Every instantiation of the tcgen05 GEMM family (tile width, m-subtiles sharing the B
+    slice, k-blocks per TMA box) against torch fp32, including M / N / K tails."""
+    L, capi = _testing_lib()
+    L.elattn_gpu_testing_gemm_config.argtypes = [ctypes.c_int] * 3
+    capi.check(L.elattn_gpu_testing_gemm_config(bn, mt, kbp))
+    try:
+        got, want = gemm_case(1, M, N, K, Z, layout, seed=M + N + K + bn + mt + kbp, alpha=0.5)
+    finally:
+        capi.check(L.elattn_gpu_testing_gemm_config(0, 0, 0))
+    err = (got - want).abs().max().item() / want.abs().max().item()
+    assert err < 1e-2, err
+
+
 def decode_ref(qp, H, rows, scale, npi=None):
     """torch fp32: C[b*rows+q] = softmax(q' H_b^T * scale) H_b."""
     import torch

@@ -16,6 +16,7 @@ ap.add_argument("--B", type=int, default=320)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--only", default=None, help="substring of the GEMM name to run")
 ap.add_argument("--no-cublas", action="store_true")
+ap.add_argument("--sweep", action="store_true", help="time every block-shape instantiation")
 a = ap.parse_args()
 L = capi.lib()
 vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
@@ -65,9 +66,18 @@ def graph_time(fn, reps):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
-for name, (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z) in shapes.items():
+L.elattn_gpu_testing_gemm_config.argtypes = [i32, i32, i32]
+CFGS = [(0, 0, 0)]
+if a.sweep:
+    CFGS += [(bn, mt, kbp) for bn in (64, 128, 256) for mt in (1, 2) for kbp in (1, 2)
+             if not (bn == 256 and mt == 2)]
+for (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z), name, cfg in [
+        (v, k, c) for k, v in shapes.items() for c in CFGS]:
     if a.only and a.only not in name:
         continue
+    if cfg[0] > 64 and N <= 64:
+        continue
+    capi.check(L.elattn_gpu_testing_gemm_config(*cfg))
     def run():
         capi.check(L.elattn_gpu_testing_gemm_bf16(A.data_ptr(), lda, sAz, Bm.data_ptr(), ldb, sBz, C.data_ptr(), ldc,
                                                   sCz, bs.data_ptr() if bs is not None else None, sbz, M, N, K, Z,
@@ -76,9 +86,10 @@ for name, (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z) in shape
     torch.cuda.synchronize()
     us = graph_time(run, a.reps)
     byt = (M * K * Z + N * K * Z + M * N * Z) * 2
-    print(json.dumps({"gemm": name, "us": round(us, 2), "GBps": round(byt / us / 1e3, 1),
+    print(json.dumps({"gemm": name, "cfg": cfg, "us": round(us, 2), "GBps": round(byt / us / 1e3, 1),
                       "TFLOPs": round(2 * M * N * K * Z / us / 1e6, 1)}))
 
+capi.check(L.elattn_gpu_testing_gemm_config(0, 0, 0))
 # cuBLAS (torch.matmul) on the two plain shapes, for reference
 if a.no_cublas:
     raise SystemExit(0)
