@@ -29,6 +29,10 @@ int elattn_gpu_testing_gemm_bf16(const void* A, int64_t lda, int64_t sAz, const 
  * instantiation make the next GEMM fail with ELATTN_ERR_UNSUPPORTED. */
 int elattn_gpu_testing_gemm_config(int bn, int mt, int kbp);
 
+/* GEMM epilogue: 0 = coalesced st.global through a per-warp smem transpose, 1 = 128-row
+ * TMA tensor stores, -1 = per shape (default: TMA stores for the write-bound q' expansion). */
+int elattn_gpu_testing_gemm_epilogue(int tma);
+
 /* Programmatic dependent launch of the step's kernels on (1, default) or off (0). */
 int elattn_gpu_testing_set_pdl(int on);
 

@@ -415,6 +415,11 @@ extern "C" int elattn_gpu_testing_gemm_config(int bn, int mt, int kbp) {
     });
 }
 
+extern "C" int elattn_gpu_testing_gemm_epilogue(int tma) {
+    g_gemm_epilogue_tma = tma < 0 ? -1 : (tma ? 1 : 0);
+    return ELATTN_OK;
+}
+
 extern "C" int elattn_gpu_testing_set_pdl(int on) {
     g_pdl = on ? 1 : 0;
     return ELATTN_OK;

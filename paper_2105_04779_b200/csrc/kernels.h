@@ -48,6 +48,7 @@ void launch_tc_gemm(const GemmArgs& g, cudaStream_t st);
 // Testing / tuning override of the tcgen05 GEMM block shape (0 = automatic choice).
 extern int g_gemm_force_bn, g_gemm_force_mt, g_gemm_force_kbp;
 extern unsigned long long* g_gemm_trace;
+extern int g_gemm_epilogue_tma;
 
 // Mixed self-attention merge (mixed.cu): see the file header.
 void launch_mixed_combine(int dtype, const void* Q, const float2* stats, void* V, const void* Kc, const void* Vc,

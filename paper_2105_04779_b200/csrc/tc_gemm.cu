@@ -32,6 +32,7 @@ namespace elattn_gpu {
 
 int g_gemm_force_bn = 0, g_gemm_force_mt = 0, g_gemm_force_kbp = 0;  // testing / tuning override (0 = auto)
 unsigned long long* g_gemm_trace = nullptr;                            // testing: timeline of CTA 0
+int g_gemm_epilogue_tma = -1;                                          // testing / tuning: 1 TMA stores, 0 st.global, -1 auto
 
 namespace {
 
@@ -50,9 +51,12 @@ struct GemmSmem {
     static constexpr int kPiece = kHalf < 64 ? kHalf : 64;
     static constexpr uint32_t kPieceBytes = kBM * kPiece * 2;
     static constexpr uint32_t kFixedNoOut = 256 + 1024;
-    // two stage buffers per group unless that leaves fewer than three operand stages
+    // store buffers per group: a TMA store holds its buffer for ~600 ns (until it has read
+    // it), so the write-bound shape (BN = 256, one k-step per tile: q' expansion) keeps four
+    // in flight per group and two operand stages; the others two, or one if that would
+    // leave fewer than three operand stages
     static constexpr int kStages2 = int((232448u - kFixedNoOut - 2 * 2 * kPieceBytes) / kStageBytes);
-    static constexpr int kOutBufs = kStages2 >= 3 ? 2 : 1;
+    static constexpr int kOutBufs = (BN == 256 && KBP == 1) ? 4 : (kStages2 >= 3 ? 2 : 1);
     static constexpr uint32_t kOutBytes = 2 * kOutBufs * kPieceBytes;
     static constexpr int kStagesFit = int((232448u - kFixedNoOut - kOutBytes) / kStageBytes);
     static constexpr int kStages = kStagesFit < 8 ? kStagesFit : 8;
@@ -76,6 +80,9 @@ struct GemmParams {
     int a_zm, b_zm, c_zm;  // 1: tensor map coordinate order is (k, z, m, ..) instead of (k, m, z, ..)
     int a_bcast;           // A shared by every z (sAz == 0): load it with z = 0
     int pdl;               // wait for the preceding kernel (programmatic dependent launch)
+    int direct;            // epilogue: coalesced st.global through a per-warp smem transpose (1) or TMA stores (0)
+    __nv_bfloat16* C;      // output for the direct epilogue: C + z * sCz + m * ldc + n
+    int64_t ldc, sCz;
     unsigned long long* trace;  // testing: %globaltimer stamps of CTA 0 (null = off)
 };
 
@@ -170,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* b = a + KBP * MT * S::kABytes;
                     ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
                     const int kb = ks * KBP;
+                    if (tr && it < 4) p.trace[52 + it] = gtimer();
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
                         uint8_t* dst = a + mt * KBP * S::kABytes;  // [kb][128 rows][64]
@@ -262,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int c = 0; c < kPiece; c += 32)
                         ptx::tmem_ld32(t_row + c, *reinterpret_cast<uint32_t(*)[32]>(&rr[c]));
                     ptx::tmem_ld_wait();
+                    if (tr && warp == 2 && lane == 0 && piece < 2) p.trace[60 + 3 * piece] = gtimer();
                     if (mt == MT - 1 && c0 + kPiece >= kHalf) {
                         // this warp's part of the accumulator is read: the MMA warp may reuse it
                         ptx::tc_fence_before();
@@ -269,9 +278,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
                     }
                     uint8_t* stage = grp_stage + (piece % S::kOutBufs) * S::kPieceBytes;
-                    // the store that last used this buffer has read it
-                    if (leader) ptx::bulk_wait_group_read<S::kOutBufs - 1>();
-                    group_bar(bar_id);
+                    if (!p.direct) {
+                        // the store that last used this buffer has read it
+                        if (leader) ptx::bulk_wait_group_read<S::kOutBufs - 1>();
+                        group_bar(bar_id);
+                    }
 #pragma unroll
                     for (int cc = 0; cc < kPiece; cc += 32) {
                         uint32_t packed[16];
@@ -296,8 +307,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                             *reinterpret_cast<uint4*>(row + (((cbase + q) ^ sw) << 4)) =
                                 make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
                     }
+                    if (p.direct) {
+                        // this warp's 32 rows leave through its own slice of the stage,
+                        // read back row-contiguous: each st.global.v4 instruction writes
+                        // 32 / kChunks whole 128-byte (64-byte) row pieces
+                        constexpr int kChunks = kPiece / 8, kRowsPerInst = 32 / kChunks;
+                        __syncwarp();
+                        if (tr && warp == 2 && lane == 0 && piece < 2) p.trace[61 + 3 * piece] = gtimer();
+                        const uint8_t* slice = stage + qd * 32 * (kPiece * 2);
+                        const int rbase = m0 + mt * kBM + int(qd) * 32, cbase = n0 + int(grp) * kHalf + c0;
+#pragma unroll
+                        for (int s = 0; s < 32 / kRowsPerInst; ++s) {
+                            const int rr = s * kRowsPerInst + int(lane) / kChunks, ch = int(lane) % kChunks;
+                            const int sw = kPiece == 64 ? (rr & 7) : ((rr >> 1) & 3);
+                            const uint4 v = *reinterpret_cast<const uint4*>(slice + rr * (kPiece * 2) + ((ch ^ sw) << 4));
+                            const int row = rbase + rr, col = cbase + ch * 8;
+                            if (row < p.M && col < p.N)
+                                *reinterpret_cast<uint4*>(p.C + z * p.sCz + int64_t(row) * p.ldc + col) = v;
+                        }
+                        __syncwarp();
+                        if (tr && warp == 2 && lane == 0 && piece < 2) p.trace[62 + 3 * piece] = gtimer();
+                        continue;
+                    }
                     ptx::fence_proxy_async_smem();
                     group_bar(bar_id);
+                    if (tr && leader && warp == 2 && piece < 4) p.trace[56 + piece] = gtimer();
                     if (leader) {
                         const int nbase = n0 + int(grp) * kHalf + c0, r0 = m0 + mt * kBM;
                         if (nbase < p.N && r0 < p.M) {
@@ -389,6 +423,9 @@ void launch_cfg(const GemmArgs& g, cudaStream_t st) {
     p.tiles_n = int(ceil_div(g.N, BN));
     p.a_bcast = (g.Z > 1 && g.sAz == 0) ? 1 : 0;
     p.pdl = pdl_enabled() ? 1 : 0;
+    // write-bound q' expansion (BN = 256): TMA stores; the others: coalesced st.global
+    p.direct = g_gemm_epilogue_tma < 0 ? (BN == 256 ? 0 : 1) : (g_gemm_epilogue_tma ? 0 : 1);
+    p.C = static_cast<__nv_bfloat16*>(g.C), p.ldc = g.ldc, p.sCz = g.sCz;
     p.trace = g_gemm_trace;
     CUtensorMap ta = load_map(g.A, g.lda, g.sAz, g.M, g.K, p.a_bcast ? 1 : g.Z, kBM, KBP, &p.a_zm);
     CUtensorMap tb = load_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, BN, KBP, &p.b_zm);

@@ -88,11 +88,14 @@ def test_gemm_block_shapes(bn, mt, kbp, M, N, K, Z, layout):
     L.elattn_gpu_testing_gemm_config.argtypes = [ctypes.c_int] * 3
     capi.check(L.elattn_gpu_testing_gemm_config(bn, mt, kbp))
     try:
-        got, want = gemm_case(1, M, N, K, Z, layout, seed=M + N + K + bn + mt + kbp, alpha=0.5)
+        for tma in (0, 1):  # both epilogues: coalesced st.global / 128-row TMA stores
+            capi.check(L.elattn_gpu_testing_gemm_epilogue(tma))
+            got, want = gemm_case(1, M, N, K, Z, layout, seed=M + N + K + bn + mt + kbp, alpha=0.5)
+            err = (got - want).abs().max().item() / want.abs().max().item()
+            assert err < 1e-2, (tma, err)
     finally:
         capi.check(L.elattn_gpu_testing_gemm_config(0, 0, 0))
-    err = (got - want).abs().max().item() / want.abs().max().item()
-    assert err < 1e-2, err
+        capi.check(L.elattn_gpu_testing_gemm_epilogue(-1))
 
 
 def decode_ref(qp, H, rows, scale, npi=None):

@@ -75,4 +75,5 @@ for name, (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z) in shape
     rel = lambda v: (v - t0) if v else None
     ks = [rel(v) for v in t[2:34] if v]
     print(name, "event us %.2f" % e0.elapsed_time(e1) * 1, "setup", rel(t[1]), "kstep ns", ks[:20],
-          "acc", [rel(v) for v in t[34:50:2] if v], "epi_done", rel(t[50]))
+          "acc", [rel(v) for v in t[34:50:2] if v], "epi_done", rel(t[50]),
+          "prod_issue", [rel(v) for v in t[52:56] if v], "store_issue", [rel(v) for v in t[56:60] if v], "epi(ld,cvt,st)", [rel(v) for v in t[60:66] if v])

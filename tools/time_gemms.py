@@ -17,6 +17,7 @@ ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--only", default=None, help="substring of the GEMM name to run")
 ap.add_argument("--no-cublas", action="store_true")
 ap.add_argument("--sweep", action="store_true", help="time every block-shape instantiation")
+ap.add_argument("--tma-epilogue", action="store_true")
 a = ap.parse_args()
 L = capi.lib()
 vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
@@ -67,6 +68,7 @@ def graph_time(fn, reps):
 
 
 L.elattn_gpu_testing_gemm_config.argtypes = [i32, i32, i32]
+L.elattn_gpu_testing_gemm_epilogue(1 if a.tma_epilogue else -1)
 CFGS = [(0, 0, 0)]
 if a.sweep:
     CFGS += [(bn, mt, kbp) for bn in (64, 128, 256) for mt in (1, 2) for kbp in (1, 2)
