@@ -9,7 +9,10 @@ output projection; layer l+1 consumes layer l's output rows as its queries.
 
 metric: decoder-step attention tokens/s = (B*x) / t_step, summed over ranks.
 Weak scaling: every rank owns B inputs (its own H shard); no collective in the
-timed region; one NCCL all_gather of the output rows afterwards (sharding.py).
+timed region; one NCCL all_gather of the output rows afterwards (sharding.py),
+and rank 0 recomputes other ranks' shards from their seeds and checks the
+gathered rows bit for bit.  `--gpus N` outside torchrun starts the N ranks itself
+(torch.distributed.run on this node, one rank per GPU).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -42,7 +45,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=320, help="inputs per GPU (B)")
     ap.add_argument("--layers", type=int, default=CFG["layers"])
-    ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    ap.add_argument("--cpu-sample-s", type=float, default=8.0, help="seconds per CPU-baseline mode (fp64, f32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -123,127 +126,247 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU baseline
-def cpu_reference_rate(seconds_target: float, layers: int):
-    """The reference's own CPU path (oracle/_ref: build_el_query x 4 -> fold ->
-    el_attention_folded per input, attention.hpp:197,293,262), all host cores,
-    one std::thread per core over independent inputs.  Falls back to the C port
-    of the oracle if the reference was not compiled."""
-    import numpy as np
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    import oracle as O
 
-    c = CFG
-    threads = os.cpu_count() or 1
-    kind = "reference" if O.ref_available() else "port"
-    p = O.params_random(c["h"], c["d_m"], c["d_k"], O.OracleRng(1))
-    # calibrate on one input per thread, then size the sample to ~seconds_target
-    per_round = threads
-    rng = O.OracleRng(2)
-    H = rng.uniform((per_round, c["n"], c["d_m"]))
-    Y = rng.uniform((per_round * c["x"], c["d_m"]))
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
-    def run(rounds):
-        t0 = time.perf_counter()
-        for _ in range(rounds):
-            if kind == "reference":
-                O.el_layer_step(p, Y, H, c["x"], impl="reference", nthreads=threads)
+
+class RefStep:
+    """One bounded sample of the decoder step on the host: `Bs` inputs x all layers through
+    the reference's own functions (oracle/_ref: build_el_query x beams -> fold_el_queries ->
+    el_attention_folded per input, attention.hpp:197,293,262), one std::thread per host core
+    over independent inputs, with the layers' parameters built once (RefLayer).  f32 selects
+    the reference's PrecisionGuard(f32) mode (tensor.hpp:25-29).  Falls back to the C port
+    of the oracle when the reference was not compiled.  Used by BOTH the GPU arm's
+    cpu_baseline and the --impl reference arm, so the two report the same thing."""
+
+    def __init__(self, n_layers: int, threads: int, f32: bool = False):
+        import numpy as np
+
+        import oracle as O
+
+        c = CFG
+        self.O, self.np, self.f32 = O, np, f32
+        self.threads = threads
+        self.kind = "reference" if O.ref_available() else "port"
+        self.params = [O.params_random(c["h"], c["d_m"], c["d_k"], O.OracleRng(1 + l)) for l in range(n_layers)]
+        self.ref = [O.RefLayer(p) for p in self.params] if self.kind == "reference" else None
+        self.Bs = threads
+        rng = O.OracleRng(2)
+        self.H = rng.uniform((self.Bs, c["n"], c["d_m"]))
+        self.Y0 = rng.uniform((self.Bs * c["x"], c["d_m"]))
+        self.out = np.zeros_like(self.Y0)
+
+    def __call__(self):
+        x = CFG["x"]
+        y = self.Y0
+        for l in range(len(self.params)):
+            if self.kind == "reference":
+                self.ref[l].step(y, self.H, x, None, 0, self.Bs, self.out, self.threads, self.f32)
+                y = self.out.copy()
             else:
-                O.el_layer_step(p, Y, H, c["x"])
-        return time.perf_counter() - t0
+                y = self.O.el_layer_step(self.params[l], y, self.H, x, f32=self.f32)
+        return y
 
-    t1 = run(1)
-    rounds = max(1, min(50, int(seconds_target / max(t1, 1e-3))))
-    t = run(rounds)
-    inputs = rounds * per_round
-    layer_rate = inputs * c["x"] / t  # beam-token-layers / s
-    return {"value": layer_rate / layers, "unit": UNIT, "cores": threads if kind == "reference" else 1,
-            "kind": kind,
-            "sample": f"{inputs} inputs x 1 layer (BART-large, beam 4, n 1024, fp64), {t:.1f} s; "
-                      f"value = beam-token-layers/s / {layers} layers",
-            "beam_token_layers_per_s": layer_rate}
+    def tokens(self) -> int:
+        return self.Bs * CFG["x"]
+
+    def cores(self) -> int:
+        return self.threads if self.kind == "reference" else 1
+
+
+def cpu_reference_rate(seconds_target: float, layers: int):
+    """The reference's CPU path on this box's host cores, fp64 and f32 mode, each sized to
+    about `seconds_target` seconds (whole decoder steps of RefStep)."""
+    threads = host_threads()
+    res = {}
+    for mode in ("f64", "f32"):
+        rs = RefStep(layers, threads, f32=(mode == "f32"))
+        t0 = time.perf_counter()
+        rs()
+        t1 = time.perf_counter() - t0
+        steps = max(1, min(20, int(seconds_target / max(t1, 1e-3))))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            rs()
+        dt = (time.perf_counter() - t0) / steps
+        res[mode] = (rs, steps, dt)
+    rs, steps, dt = res["f64"]
+    value = rs.tokens() / dt
+    return {"value": value, "unit": UNIT, "cores": rs.cores(), "kind": rs.kind,
+            "sample": f"{steps} decoder steps x {rs.Bs} inputs x {layers} layers (BART-large, beam 4, n 1024, "
+                      f"fp64, one thread per core), {steps * dt:.1f} s; same RefStep as --impl reference",
+            "f32_mode_value": res["f32"][0].tokens() / res["f32"][2],
+            "cpu_model": cpu_model(), "nproc": threads}
 
 
 def reference_arm(args):
     """--impl reference: the reference's CPU implementation, same metric/config,
-    each step a bounded sample (threads inputs x all layers)."""
-    import numpy as np
-
-    import oracle as O
-
+    each step a bounded sample (one input per host thread x all layers)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    c = CFG
-    threads = os.cpu_count() or 1
-    kind = "reference" if O.ref_available() else "port"
-    layers = [O.params_random(c["h"], c["d_m"], c["d_k"], O.OracleRng(1 + l)) for l in range(args.layers)]
-    rng = O.OracleRng(2)
-    Bs = threads
-    H = rng.uniform((Bs, c["n"], c["d_m"]))
-    Y0 = rng.uniform((Bs * c["x"], c["d_m"]))
-    ref_layers = [O.RefLayer(p) for p in layers] if kind == "reference" else None
-    out = np.zeros_like(Y0)
-
-    def step():
-        y = Y0
-        for l in range(args.layers):
-            if kind == "reference":
-                ref_layers[l].step(y, H, c["x"], None, 0, Bs, out, threads)
-                y = out.copy()
-            else:
-                y = O.el_layer_step(layers[l], y, H, c["x"])
-        return y
-
+    threads = host_threads()
+    rs = RefStep(args.layers, threads)
     for _ in range(args.warmup):
-        step()
+        rs()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        step()
+        rs()
     dt = (time.perf_counter() - t0) / args.steps
-    value = Bs * c["x"] / dt
+    value = rs.tokens() / dt
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"BART-large EL cross-attention decode step, {args.layers} layers, "
-                                   f"beam 4, n 1024, d_m 1024, 16 heads; bounded sample of {Bs} inputs per step",
-                       "inputs_per_step": Bs, "layers": args.layers},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads if kind == "reference" else 1,
-                             "kind": kind, "sample": f"{Bs} inputs x {args.layers} layers per step"},
+                                   f"beam 4, n 1024, d_m 1024, 16 heads; bounded sample of {rs.Bs} inputs per step",
+                       "inputs_per_step": rs.Bs, "layers": args.layers},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": rs.cores(), "kind": rs.kind,
+                             "sample": f"{rs.Bs} inputs x {args.layers} layers per step",
+                             "cpu_model": cpu_model(), "nproc": threads},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ multi-rank plumbing
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N outside torchrun: start N ranks (one per GPU) under torch.distributed.run on
+    this node and relay their output (rank 0 prints the JSON line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(ROOT / "bench.py"), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def shard_inputs(rank, B, x, n, d_m, device, dtype):
+    """Rank `rank`'s shard of the global batch (inputs [rank*B, (rank+1)*B)): H [B, n, d_m]
+    and the first layer's query rows Y [B*x, d_m], U(-1, 1) from a per-rank seeded generator,
+    so any rank can regenerate another rank's shard bit for bit."""
+    import torch
+
+    gen = torch.Generator(device=device).manual_seed(1000 + rank)
+    H = (torch.rand((B, n, d_m), generator=gen, device=device) * 2 - 1).to(dtype)
+    Y0 = (torch.rand((B * x, d_m), generator=gen, device=device) * 2 - 1).to(dtype)
+    return H, Y0
+
+
+def shard_check(full, recompute, world, B, x):
+    """Rank 0: recompute whole shards of other ranks locally (same B, so the same decode
+    schedule) and compare them with the gathered rows bit for bit."""
+    import torch
+
+    ranks = sorted({r for r in (1, world - 1) if r > 0})
+    ok = True
+    for r in ranks:
+        want = recompute(r)
+        got = full[r * B * x:(r + 1) * B * x]
+        ok = ok and bool(torch.equal(got.cpu(), want.cpu()))
+    return {"ranks_recomputed_on_rank0": ranks, "bit_exact": ok, "rows_per_rank": B * x}
+
+
+def init_dist(backend, local):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return world, int(os.environ.get("RANK", "0"))
+
+
+def cpu_standin_arm(args):
+    """ELATTN_BENCH_STANDIN=cpu (tests only, no GPU): the same rank spawn, input sharding,
+    max-over-ranks timing, output all_gather and rank-0 shard check as the GPU arm, with a
+    deterministic CPU stand-in (torch ops) in place of the decoder-step kernels."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2105_04779_b200.sharding import gather_outputs
+
+    world, rank = init_dist("gloo", 0)
+    c = CFG
+    B, x, n, d_m, L = args.batch, c["x"], 16, 32, args.layers
+
+    def step(H, Y0):
+        y = Y0
+        ctx = H.mean(dim=1).repeat_interleave(x, dim=0)
+        for l in range(L):
+            y = torch.tanh(y * (0.5 + 0.01 * l) + ctx)
+        return y
+
+    H, Y0 = shard_inputs(rank, B, x, n, d_m, "cpu", torch.float32)
+    for _ in range(args.warmup):
+        step(H, Y0)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = step(H, Y0)
+    t = torch.tensor([(time.perf_counter() - t0) / args.steps * 1e3], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    full = gather_outputs(out, world * B, x) if world > 1 else out
+    chk = shard_check(full, lambda r: step(*shard_inputs(r, B, x, n, d_m, "cpu", torch.float32)), world, B, x) \
+        if rank == 0 and world > 1 else None
+    if rank == 0:
+        ms = float(t.item())
+        print(json.dumps({"metric": METRIC, "value": world * B * x / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                          "config": {"workload": "CPU stand-in (plumbing test only)", "global_batch": world * B},
+                          "shard_check": chk}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ GPU arm
 def gpu_arm(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2105_04779_b200 as E
     from paper_2105_04779_b200 import capi
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank = init_dist("nccl", local)
     c = CFG
     B, x, n, d_m, h, d_k, L = args.batch, c["x"], c["n"], c["d_m"], c["h"], c["d_k"], args.layers
     dev = torch.device("cuda", local)
 
-    # weights: L independent random layers (AttentionParams::random, seeds 1..L)
+    # weights: L independent random layers (AttentionParams::random, seeds 1..L), replicated
     layers = []
     for l in range(L):
         p = E.AttentionParams.random(h, d_m, d_k, E.Rng(1 + l))
         layers.append(E.ElAttentionLayer(p, E.DTYPE_BF16))
     kind = layers[0].dev.decode_kernel_kind(x)
     # this rank's shard of inputs: H [B, n, d_m] resident in HBM (671 MB at B = 320)
-    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
-    H = (torch.rand((B, n, d_m), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
-    Y0 = (torch.rand((B * x, d_m), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
+    H, Y0 = shard_inputs(rank, B, x, n, d_m, dev, torch.bfloat16)
     # the public batched decoder-step API: L layers over the shared H, captured once into
     # a CUDA graph by the library (elattn_gpu_decoder_create), replayed per step
     dec = E.DecoderStep(layers, H, B, x)
@@ -364,14 +487,27 @@ def gpu_arm(args):
     e2e_value = world * B * x / (float(te.item()) / 1e3)
 
     # ---- gather every rank's output rows over NCCL, outside the timed region
-    # (input sharding: rank r owns inputs [r*B, (r+1)*B) of the global batch)
+    # (input sharding: rank r owns inputs [r*B, (r+1)*B) of the global batch), and on rank 0
+    # recompute other ranks' shards from their seeds: the gathered rows must match bit for bit
     from paper_2105_04779_b200.sharding import gather_outputs, shard_range
 
     dec.Y.copy_(Y0)
     out = step()
+    torch.cuda.synchronize()
     assert shard_range(world * B, rank, world) == (rank * B, (rank + 1) * B)
     full = gather_outputs(out, world * B, x) if world > 1 else out
     finite = bool(torch.isfinite(full.float()).all())
+    chk = None
+    if rank == 0 and world > 1:
+        def recompute(r):
+            Hr, Yr = shard_inputs(r, B, x, n, d_m, dev, torch.bfloat16)
+            dr = E.DecoderStep(layers, Hr, B, x)
+            dr.Y.copy_(Yr)
+            o = dr.run(stream=stream).clone()
+            torch.cuda.synchronize()
+            del dr, Hr
+            return o
+        chk = shard_check(full, recompute, world, B, x)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -410,6 +546,8 @@ def gpu_arm(args):
             "cpu_baseline": cpu,
             "outputs_finite": finite,
         }
+        if chk is not None:
+            line["shard_check"] = chk
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -419,6 +557,11 @@ def main():
     args = parse()
     if args.impl == "reference":
         reference_arm(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if os.environ.get("ELATTN_BENCH_STANDIN") == "cpu":
+        cpu_standin_arm(args)
     else:
         gpu_arm(args)
 

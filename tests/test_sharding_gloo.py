@@ -65,3 +65,27 @@ def test_two_rank_gloo_gather_matches_single_process(tmp_path, B):
     p, Y, H = make_case(2, 16, 8, 9, B, x, 5, 6)
     want = O.el_layer_step(p, Y, H, x)
     assert np.array_equal(np.load(out_path), want)
+
+
+def test_bench_spawns_ranks_and_checks_shards():
+    """`bench.py --gpus 2` outside torchrun starts its 2 ranks itself (torch.distributed.run),
+    shards the inputs, takes the max over ranks, all_gathers the outputs and has rank 0
+    recompute rank 1's shard bit for bit — here over gloo with the CPU stand-in for the
+    kernels (ELATTN_BENCH_STANDIN=cpu), the same plumbing the GPU arm runs over NCCL."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, ELATTN_BENCH_STANDIN="cpu")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "1",
+                        "--batch", "3", "--layers", "2"], capture_output=True, text=True, timeout=600, cwd=root,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["global_batch"] == 6 and line["value"] > 0
+    assert line["shard_check"] == {"ranks_recomputed_on_rank0": [1], "bit_exact": True, "rows_per_rank": 12}
