@@ -159,6 +159,8 @@ int elattn_gpu_decode_kernel_kind(elattn_gpu_params_t params, int g);
  *   H            [B][n][d_m] device, n_per_input device int[B] or NULL (as in _step)
  *   Y_in, out    [B*x][d_m] device buffers bound at creation: write Y_in, run, read out
  *                (out may alias Y_in)
+ * create waits for all prior device work (cudaDeviceSynchronize) and runs one eager
+ * warm-up step into internal scratch before capturing; run is stream-ordered on `stream`.
  * Errors: PARAM (null / mismatched layers), SHAPE, STATE (n < 1), OOM, CUDA.
  */
 typedef struct elattn_gpu_decoder_s* elattn_gpu_decoder_t;
@@ -166,7 +168,7 @@ int elattn_gpu_decoder_create(const elattn_gpu_params_t* layers, int L, const vo
                               int B, int x, int n, const void* Y_in, void* out, elattn_gpu_decoder_t* dec);
 int elattn_gpu_decoder_run(elattn_gpu_decoder_t dec, elattn_stream_t stream);
 int elattn_gpu_decoder_destroy(elattn_gpu_decoder_t dec);
-/* our own kernels launched by one run (the graph's kernel nodes outside cuBLASLt) */
+/* our own kernels launched by one run (the graph's kernel nodes) */
 int64_t elattn_gpu_decoder_kernels_per_run(elattn_gpu_decoder_t dec);
 
 /*
@@ -222,7 +224,9 @@ size_t elattn_gpu_mixed_workspace_size(elattn_gpu_params_t params, int B, int x)
  * reference's candidate_better order (decoding.hpp:163-167: higher lp_sum, then smaller
  * token, then smaller parent) -> parent/token/lp_sum [B][k] (parent -1 when fewer than k).
  * roots = 1 on the first step (all lanes identical), = lanes afterwards.  penalty (may be
- * NULL): device float[B][V] >= 0 subtracted from every finite log-prob before the sum —
+ * NULL): device float[B][V] >= 0 subtracted from every finite log-prob before the sum (the
+ * raw-log-prob pre-filter is exact only for non-negative penalties: negative values are
+ * outside the contract; the Python wrapper rejects them) —
  * diverse_beam_search's `v -= strength * step_token_counts[tok]` (decoding.hpp:312-316),
  * called once per group with that group's contiguous lanes.
  */

@@ -182,6 +182,17 @@ def _stream_ptr(stream) -> int:
     return int(s.cuda_stream)
 
 
+def _record(tensors, stream) -> None:
+    """Tie allocator lifetimes to `stream`: buffers allocated on the current stream but used
+    by library kernels on another stream must not be recycled while those kernels run."""
+    torch = _torch()
+    if stream is None or stream == torch.cuda.current_stream():
+        return
+    for t in tensors:
+        if t is not None:
+            t.record_stream(stream)
+
+
 class DeviceParams:
     """Opaque device weights (``elattn_gpu_params_t``): packed once, K-major, in `dtype`."""
 
@@ -230,11 +241,14 @@ class ElAttentionLayer:
         self.dtype = self.dev.dtype
         self._ws = None
 
-    def workspace(self, B: int, x: int, n: int):
+    def workspace(self, B: int, x: int, n: int, stream=None):
         torch = _torch()
         need = self.dev.workspace_size(B, x, n)
         if self._ws is None or self._ws.numel() < need:
+            # the old buffer may still be in use by launches on other streams: its
+            # record_stream marks (from earlier calls) keep the allocator from reusing it early
             self._ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+        _record([self._ws], stream)
         return self._ws
 
     def _check(self, t, shape, what):
@@ -266,7 +280,8 @@ class ElAttentionLayer:
             if n_per_input.dtype != torch.int32 or not n_per_input.is_cuda or n_per_input.numel() != B:
                 raise ParamError("n_per_input must be a CUDA int32 tensor of length B")
             npi = n_per_input.data_ptr()
-        ws = self.workspace(B, x, n)
+        ws = self.workspace(B, x, n, stream)
+        _record([out], stream)
         capi.check(capi.lib().elattn_gpu_el_attention_step(
             self.dev.handle, Y.data_ptr(), H.data_ptr(), npi or None, B, x, n, out.data_ptr(),
             ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
@@ -278,7 +293,8 @@ class ElAttentionLayer:
         self._check(Y, (R, self.dev.d_m), "Y")
         if qprime is None:
             qprime = torch.empty(R * self.dev.h, self.dev.d_m, dtype=Y.dtype, device=Y.device)
-        ws = self.workspace(R, 1, 1)
+        ws = self.workspace(R, 1, 1, stream)
+        _record([qprime], stream)
         capi.check(capi.lib().elattn_gpu_build_el_query(
             self.dev.handle, Y.data_ptr(), R, qprime.data_ptr(), s.data_ptr() if s is not None else None,
             ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
@@ -291,7 +307,8 @@ class ElAttentionLayer:
         self._check(H, None, "H")
         if out is None:
             out = torch.empty(B * g, d_m, dtype=H.dtype, device=H.device)
-        ws = self.workspace(B, g, n)
+        ws = self.workspace(B, g, n, stream)
+        _record([out], stream)
         npi = n_per_input.data_ptr() if n_per_input is not None else None
         capi.check(capi.lib().elattn_gpu_el_attention_folded(
             self.dev.handle, qprime.data_ptr(), None, H.data_ptr(), npi, B, g, n, out.data_ptr(),
@@ -512,6 +529,7 @@ def mixed_self_attention_batched(layer: "ElAttentionLayer", Y, P, cache: KvCache
         out = torch.empty_like(Y)
     need = capi.lib().elattn_gpu_mixed_workspace_size(layer.dev.handle, B, x)
     ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+    _record([ws, out], stream)  # released on return while the kernels may still run on `stream`
     npi = n_per_input.data_ptr() if n_per_input is not None else None
     capi.check(capi.lib().elattn_gpu_mixed_self_attention(
         layer.dev.handle, Y.data_ptr(), P.data_ptr(), npi, B, x, n, cache.K.data_ptr(), cache.V.data_ptr(),
@@ -634,6 +652,10 @@ def beam_candidates(lprobs, live_lp, lanes: int, k: int, roots: Optional[int] = 
         penalty = penalty.contiguous().float()
         if penalty.numel() != B * V:
             raise ShapeError("beam_candidates: penalty must be [B, V]")
+        # the kernel's pre-filter compares raw log-probs with the running k-th score, which
+        # is exact only for penalties >= 0 (diversity strength x counts, decoding.hpp:312-316)
+        if bool((penalty < 0).any()):
+            raise ParamError("beam_candidates: penalty must be >= 0")
     parent = torch.empty(B, k, dtype=torch.int32, device=lprobs.device)
     token = torch.empty_like(parent)
     lp_sum = torch.empty(B, k, dtype=torch.float32, device=lprobs.device)

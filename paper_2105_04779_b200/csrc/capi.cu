@@ -139,11 +139,17 @@ class Scratch {
 
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
-// Scratch layout of a full step: Q [R][h*d_k], q' [R*h][d_m], C [R*h][d_m], V [R][h*d_k].
+// Partial records of inputs the tcgen05 decode splits across clusters (bf16 path).
+size_t decode_scratch(const elattn_gpu_params_s* p) {
+    return p->dtype == ELATTN_DTYPE_BF16 ? align256(el_decode_tc_scratch_bytes(p->d_m)) : 0;
+}
+
+// Scratch layout of a full step: Q [R][h*d_k], q' [R*h][d_m], C [R*h][d_m], V [R][h*d_k],
+// decode records.
 size_t step_workspace(const elattn_gpu_params_s* p, int64_t R) {
     const size_t e = dtype_bytes(p->dtype);
     const size_t hk = size_t(p->h) * p->d_k, hm = size_t(p->h) * p->d_m;
-    return align256(R * hk * e) * 2 + align256(R * hm * e) * 2;
+    return align256(R * hk * e) * 2 + align256(R * hm * e) * 2 + decode_scratch(p);
 }
 
 // Every bf16 projection runs on the tcgen05 GEMM family (tc_gemm.cu); shapes outside its
@@ -205,10 +211,10 @@ bool use_tc_decode(const elattn_gpu_params_s* p, int rows_per_input) {
 
 // (2) fused decode: C = softmax(q'.H^T / sqrt(d_k)) . H   (attention.hpp:272-280)
 void decode(const elattn_gpu_params_s* p, const void* qp, const void* H, const int* npi, int B,
-            int rows_per_input, int n, void* C, cudaStream_t st, float2* stats = nullptr) {
+            int rows_per_input, int n, void* C, float* part, cudaStream_t st, float2* stats = nullptr) {
     const float scale = float(1.0 / std::sqrt(double(p->d_k)));
     if (use_tc_decode(p, rows_per_input))
-        launch_el_decode_tc(qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats);
+        launch_el_decode_tc(qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats, part);
     else
         launch_el_decode_simt(p->dtype, qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats);
 }
@@ -342,10 +348,11 @@ int elattn_gpu_el_attention_folded(elattn_gpu_params_t p, const void* qprime, co
         const int64_t R = int64_t(B) * g;
         const size_t e = dtype_bytes(p->dtype);
         const size_t cbytes = size_t(R) * p->h * p->d_m * e, vbytes = size_t(R) * p->h * p->d_k * e;
-        Scratch scratch(ws, ws_bytes, align256(cbytes) + align256(vbytes), st);
+        Scratch scratch(ws, ws_bytes, align256(cbytes) + align256(vbytes) + decode_scratch(p), st);
         void* C = scratch.take(cbytes);
         void* V = scratch.take(vbytes);
-        decode(p, qprime, H, n_per_input, B, g * p->h, n, C, st);
+        float* part = static_cast<float*>(scratch.take(decode_scratch(p)));
+        decode(p, qprime, H, n_per_input, B, g * p->h, n, C, part, st);
         output_projection(p, C, R, V, out, st);
     });
 }
@@ -358,7 +365,9 @@ int elattn_gpu_el_attention_decode(elattn_gpu_params_t p, const void* qprime, co
         ELA_REQUIRE(B >= 1 && rows >= 1, ELATTN_ERR_SHAPE, "el_attention_decode: B, rows must be >= 1");
         ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "el_attention_decode: empty context");
         ELA_REQUIRE(qprime && H && ctx, ELATTN_ERR_PARAM, "el_attention_decode: null buffer");
-        decode(p, qprime, H, n_per_input, B, rows, n, ctx, reinterpret_cast<cudaStream_t>(stream));
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        Scratch scratch(nullptr, 0, decode_scratch(p), st);
+        decode(p, qprime, H, n_per_input, B, rows, n, ctx, static_cast<float*>(scratch.take(decode_scratch(p))), st);
     });
 }
 
@@ -379,8 +388,9 @@ int elattn_gpu_el_attention_step(elattn_gpu_params_t p, const void* Y, const voi
         void* qp = scratch.take(qpb);
         void* C = scratch.take(qpb);
         void* V = scratch.take(qb);
+        float* part = static_cast<float*>(scratch.take(decode_scratch(p)));
         query_expansion(p, Y, R, Q, qp, st);
-        decode(p, qp, H, n_per_input, B, x * p->h, n, C, st);
+        decode(p, qp, H, n_per_input, B, x * p->h, n, C, part, st);
         output_projection(p, C, R, V, out, st);
     });
 }
@@ -443,7 +453,9 @@ extern "C" int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H,
         if (kernel == 1) {
             ELA_REQUIRE(el_decode_tc_supported(rows, d_m), ELATTN_ERR_UNSUPPORTED,
                         "shape outside the tcgen05 decode envelope");
-            launch_el_decode_tc(qprime, H, n_per_input, B, rows, n, d_m, scale, ctx, st);
+            Scratch scratch(nullptr, 0, align256(el_decode_tc_scratch_bytes(d_m)), st);
+            launch_el_decode_tc(qprime, H, n_per_input, B, rows, n, d_m, scale, ctx, st, nullptr,
+                                static_cast<float*>(scratch.take(el_decode_tc_scratch_bytes(d_m))));
         } else {
             launch_el_decode_simt(ELATTN_DTYPE_BF16, qprime, H, n_per_input, B, rows, n, d_m, scale, ctx, st);
         }
@@ -464,7 +476,6 @@ struct elattn_gpu_decoder_s {
 };
 
 namespace elattn_gpu {
-void release_stream_scratch(cudaStream_t st);  // el_decode_tc.cu
 }  // namespace elattn_gpu
 
 namespace {
@@ -476,7 +487,6 @@ void decoder_free(elattn_gpu_decoder_s* d) {
         if (p) cudaFree(p);
     if (d->st) {
         cudaStreamSynchronize(d->st);
-        elattn_gpu::release_stream_scratch(d->st);
         cudaStreamDestroy(d->st);
     }
     delete d;
@@ -493,13 +503,14 @@ void decoder_enqueue(elattn_gpu_decoder_s* d, const void* H, const int* npi, con
     void* qp = base + align256(qb);
     void* C = base + align256(qb) + align256(qpb);
     void* V = base + align256(qb) + 2 * align256(qpb);
+    float* part = reinterpret_cast<float*>(base + 2 * align256(qb) + 2 * align256(qpb));
     const void* y = Y_in;
     const int L = int(d->layers.size());
     for (int l = 0; l < L; ++l) {
         void* dst = (l == L - 1) ? out : d->ybuf[l & 1];
         const elattn_gpu_params_s* p = d->layers[l];
         query_expansion(p, y, R, Q, qp, d->st);
-        decode(p, qp, H, npi, d->B, d->x * p->h, d->n, C, d->st);
+        decode(p, qp, H, npi, d->B, d->x * p->h, d->n, C, part, d->st);
         output_projection(p, C, R, V, dst, d->st);
         y = dst;
     }
@@ -534,10 +545,23 @@ extern "C" int elattn_gpu_decoder_create(const elattn_gpu_params_t* layers, int 
         ELA_CHECK_CUDA(cudaMalloc(&d->ybuf[1], rows_bytes));
         d->ws_bytes = step_workspace(p0, R);
         ELA_CHECK_CUDA(cudaMalloc(&d->ws, d->ws_bytes));
-        // eager run first: allocates this stream's scratch (split records) outside the
-        // capture, and surfaces launch errors directly
-        decoder_enqueue(d.get(), H, n_per_input, Y_in, out);
-        ELA_CHECK_CUDA(cudaStreamSynchronize(d->st));
+        // eager run first (surfaces launch errors directly).  The private stream does not
+        // order after the caller's streams: wait for all prior device work (the caller may
+        // still be writing Y_in / H / n_per_input) and write the warm-up result into scratch,
+        // not into `out`, which the caller may still be reading.
+        ELA_CHECK_CUDA(cudaDeviceSynchronize());
+        void* warm_out = nullptr;
+        ELA_CHECK_CUDA(cudaMalloc(&warm_out, rows_bytes));
+        try {
+            decoder_enqueue(d.get(), H, n_per_input, Y_in, warm_out);
+        } catch (...) {
+            cudaStreamSynchronize(d->st);
+            cudaFree(warm_out);
+            throw;
+        }
+        const cudaError_t warm_err = cudaStreamSynchronize(d->st);
+        cudaFree(warm_out);
+        ELA_CHECK_CUDA(warm_err);
         const int64_t before = g_launches;
         ELA_CHECK_CUDA(cudaStreamBeginCapture(d->st, cudaStreamCaptureModeThreadLocal));
         try {
@@ -642,9 +666,10 @@ extern "C" int elattn_gpu_mixed_self_attention(elattn_gpu_params_t p, const void
         void* qp = scratch.take(qpb);
         void* C = scratch.take(qpb);
         void* V = scratch.take(qb);
+        float* part = static_cast<float*>(scratch.take(decode_scratch(p)));
         float2* stats = static_cast<float2*>(scratch.take(sb));
         query_expansion(p, Y, R, Q, qp, st);
-        decode(p, qp, P, n_per_input, B, x * p->h, n, C, st, stats);
+        decode(p, qp, P, n_per_input, B, x * p->h, n, C, part, st, stats);
         v_projection(p, C, R, V, st);
         if (t_out > 0)
             launch_mixed_combine(p->dtype, Q, stats, V, Kc, Vc, int(R), p->h, p->d_k, t_max, t_out,

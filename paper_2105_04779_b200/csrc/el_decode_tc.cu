@@ -47,8 +47,6 @@
 
 #include <algorithm>
 #include <cstdlib>
-#include <mutex>
-#include <unordered_map>
 
 namespace elattn_gpu {
 
@@ -900,28 +898,6 @@ int num_sms_decode() {
     return n;
 }
 
-// Per-stream scratch for split-input partial records, grown on demand.
-struct DecodeScratch {
-    float* part = nullptr;
-    size_t part_bytes = 0;
-};
-std::mutex g_scratch_mu;
-std::unordered_map<cudaStream_t, DecodeScratch> g_scratch;
-
-float* split_scratch(cudaStream_t st, size_t part_bytes) {
-    std::lock_guard<std::mutex> lock(g_scratch_mu);
-    DecodeScratch& s = g_scratch[st];
-    if (s.part_bytes < part_bytes) {
-        ELA_CHECK_CUDA(cudaStreamSynchronize(st));  // previous launches may still use the old buffer
-        if (s.part) cudaFree(s.part);
-        s.part = nullptr;
-        s.part_bytes = 0;
-        ELA_CHECK_CUDA(cudaMalloc(reinterpret_cast<void**>(&s.part), part_bytes));
-        s.part_bytes = part_bytes;
-    }
-    return s.part;
-}
-
 // Combines the partial records of every split input (stream-K) into C rows.
 // CTA (chunk boundary k, rank r, unit m), 256 threads; only the CTA of the first boundary
 // inside an input works.  Phase 1 (one thread per query row q): M = max_s m_s, per-segment
@@ -1026,12 +1002,12 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
 
 }  // namespace
 
-void release_stream_scratch(cudaStream_t st) {
-    std::lock_guard<std::mutex> lock(g_scratch_mu);
-    auto it = g_scratch.find(st);
-    if (it == g_scratch.end()) return;
-    if (it->second.part) cudaFree(it->second.part);
-    g_scratch.erase(it);
+size_t el_decode_tc_scratch_bytes(int d_m) {
+    // partial records of split inputs: 2 slots per cluster x 2 CTA ranks, at most one
+    // cluster per pair of SMs (the schedule never uses more clusters than that)
+    const size_t units = size_t(d_m / 256 < 1 ? 1 : d_m / 256);
+    const size_t kPF = kPartFloatsHdr + units * kPartFloatsUnit;
+    return size_t(2 * (num_sms_decode() / 2)) * 2 * kPF * sizeof(float);
 }
 
 namespace {
@@ -1040,7 +1016,7 @@ constexpr int kMinChunkTiles = 8;  // bounds the segments per input (merge cost)
 
 template <int UNITS>
 void launch_units(const void* qp, const void* H, const int* npi, int B, int rows, int n_stride, int d_m,
-                  float scale_log2, void* ctx, cudaStream_t st, float2* stats) {
+                  float scale_log2, void* ctx, cudaStream_t st, float2* stats, float* part) {
     // > 64 query rows per input: rows/64 virtual inputs of 64 rows each (q' and C rows are
     // contiguous per input, so virtual input v owns rows [64 v, 64 v + 64)); H_b is shared
     const int vchunks = rows > kRowsQ ? rows / kRowsQ : 1;
@@ -1099,7 +1075,8 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
         sa.vchunks = vchunks;
         clusters = max_cl;
         constexpr size_t kPF = kPartFloatsHdr + size_t(UNITS) * kPartFloatsUnit;
-        sa.part = split_scratch(st, size_t(2 * clusters) * 2 * kPF * sizeof(float));
+        (void)kPF;
+        sa.part = part;
     } else if (stream_k) {
         // stream-K over B*T tiles: chunks of W tiles (>= kMinChunkTiles), one per cluster
         const int T = (n_stride + kNT - 1) / kNT;
@@ -1111,7 +1088,8 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
         ELA_REQUIRE(TT < (int64_t(1) << 30), ELATTN_ERR_UNSUPPORTED, "tcgen05 decode: too many tiles");
         if (W % T != 0) {  // some inputs are split across clusters: partial records
             constexpr size_t kPF = kPartFloatsHdr + size_t(UNITS) * kPartFloatsUnit;
-            sa.part = split_scratch(st, size_t(2 * ncl) * 2 * kPF * sizeof(float));
+            (void)kPF;
+            sa.part = part;
         }
         sa.T = T;
         sa.W = int(W);
@@ -1127,7 +1105,8 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
               static_cast<const __nv_bfloat16*>(qp), npi, B, rows, n_stride, d_m, scale_log2,
               static_cast<__nv_bfloat16*>(ctx), g_decode_trace, g_tuning, sa, stats, pdl_enabled() ? 1 : 0);
     ELA_CHECK_LAUNCH();
-    if (sa.part != nullptr && clusters > 1) {
+    if ((sa.T > 0 && (sa.W < 0 || sa.W % sa.T != 0)) && clusters > 1) {
+        ELA_REQUIRE(part != nullptr, ELATTN_ERR_PARAM, "tcgen05 decode: split schedule needs the partial-record scratch");
         const int Bw = B - last_round;
         const int gx = sa.W < 0 ? last_round : clusters - 1;
         launch_ex(el_decode_merge_kernel<UNITS>, dim3(gx, 2, UNITS), dim3(256), 0, st, 1, static_cast<const float*>(sa.part),
@@ -1147,7 +1126,8 @@ bool el_decode_tc_supported(int rows_per_input, int d_m) {
 }
 
 void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B, int rows_per_input,
-                         int n_stride, int d_m, float scale, void* ctx, cudaStream_t st, float2* stats) {
+                         int n_stride, int d_m, float scale, void* ctx, cudaStream_t st, float2* stats,
+                         float* part) {
     ELA_REQUIRE(el_decode_tc_supported(rows_per_input, d_m), ELATTN_ERR_UNSUPPORTED,
                 "tcgen05 decode: rows <= 64 or a multiple of 64 (<= 512), d_m in {256, 512, 768, 1024}");
     ELA_REQUIRE((reinterpret_cast<uintptr_t>(qp) & 15) == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0 &&
@@ -1161,10 +1141,10 @@ void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, 
     }();
     (void)env_read;
     switch (d_m / 256) {
-        case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats);
-        case 2: return launch_units<2>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats);
-        case 3: return launch_units<3>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats);
-        default: return launch_units<4>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats);
+        case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part);
+        case 2: return launch_units<2>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part);
+        case 3: return launch_units<3>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part);
+        default: return launch_units<4>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part);
     }
 }
 

@@ -76,8 +76,11 @@ extern unsigned long long* g_decode_trace;
 
 // tcgen05/TMA fused EL decode for bf16 (cluster of 2 CTAs per input, split d_m).
 bool el_decode_tc_supported(int rows_per_input, int d_m);
+// `part`: scratch of el_decode_tc_scratch_bytes(d_m) bytes for the partial records of
+// inputs split across clusters (stream-ordered, owned by the caller's workspace).
+size_t el_decode_tc_scratch_bytes(int d_m);
 void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B,
                          int rows_per_input, int n_stride, int d_m, float scale, void* ctx,
-                         cudaStream_t st, float2* stats = nullptr);
+                         cudaStream_t st, float2* stats, float* part);
 
 }  // namespace elattn_gpu

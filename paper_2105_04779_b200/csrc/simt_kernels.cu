@@ -104,7 +104,7 @@ void launch_key_bias_scalars(int dtype, const void* Q, const float* bk, int R, i
 
 // --------------------------------------------------------------------------
 // SIMT fused EL decode (the core of el_attention_folded, attention.hpp:272-280):
-// one CTA owns 16 EL-Q rows of one input and streams H_b in 16-row tiles
+// one CTA owns kSimtRows (8) EL-Q rows of one input and streams H_b in kSimtTile-row tiles
 // through shared memory once, using each tile as both key and value:
 //   S = q'.Hᵀ  -> online softmax (exp2, running max / sum) -> O += P.H.
 // No per-head K/V and no beam-expanded H is ever formed.
@@ -125,12 +125,12 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
     // padded rows: q rows 16 banks apart (+16), H rows 4 apart land 16 banks apart (+4), so
     // the two half-warps of the score phase never collide
     const int ldq = d_m + 16, ldh = d_m + 4;
-    float* sq = smem;                                // [16][d_m + 16]
-    float* sh = sq + kSimtRows * ldq;                // [16][d_m + 4]
-    float* sp = sh + kSimtTile * ldh;                // [16][16]
-    float* s_alpha = sp + kSimtRows * kSimtTile;     // [16]
-    float* s_l = s_alpha + kSimtRows;                // [16]
-    float* s_m = s_l + kSimtRows;                    // [16]
+    float* sq = smem;                                // [kSimtRows][d_m + 16]
+    float* sh = sq + kSimtRows * ldq;                // [kSimtTile][d_m + 4]
+    float* sp = sh + kSimtTile * ldh;                // [kSimtRows][kSimtTile]
+    float* s_alpha = sp + kSimtRows * kSimtTile;     // [kSimtRows]
+    float* s_l = s_alpha + kSimtRows;                // [kSimtRows]
+    float* s_m = s_l + kSimtRows;                    // [kSimtRows]
     const int b = blockIdx.y, r0 = blockIdx.x * kSimtRows, tid = threadIdx.x;
     const int n = n_per_input ? n_per_input[b] : n_stride;
     const T* Hb = H + (int64_t)b * n_stride * d_m;
@@ -326,27 +326,39 @@ static void launch_decode_cpt(const void* qp, const void* H, const int* npi, int
     // SMs, the partial rows cost more than the idle SMs)
     const int blocks = int(ceil_div(rows, kSimtRows)) * B;
     const int T_all = int(ceil_div(n_stride, kSimtTile));
-    int splits = 4 * blocks >= 3 * 148 ? 1 : int(ceil_div(296, blocks));
+    static const int sms = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    // two 8-row CTAs fit per SM
+    int splits = 4 * blocks >= 3 * sms ? 1 : int(ceil_div(2 * sms, blocks));
     splits = std::max(1, std::min({splits, 8, T_all}));
-    float* part_o = nullptr;
-    float2* part_ml = nullptr;
+    // partial rows of the split context: stream-ordered scratch, released on every path
+    struct Parts {
+        float* o = nullptr;
+        float2* ml = nullptr;
+        cudaStream_t st;
+        ~Parts() {
+            if (o) cudaFreeAsync(o, st);
+            if (ml) cudaFreeAsync(ml, st);
+        }
+    } parts{nullptr, nullptr, st};
     const int64_t total_rows = int64_t(B) * rows;
     if (splits > 1) {
-        ELA_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part_o),
+        ELA_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&parts.o),
                                        sizeof(float) * size_t(splits) * size_t(total_rows) * d_m, st));
-        ELA_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part_ml),
+        ELA_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&parts.ml),
                                        sizeof(float2) * size_t(splits) * size_t(total_rows), st));
     }
     dim3 grid(unsigned(ceil_div(rows, kSimtRows)), unsigned(B), unsigned(splits));
     kern<<<grid, 256, smem, st>>>(static_cast<const T*>(qp), static_cast<const T*>(H), npi, rows,
-                                  n_stride, d_m, scale_log2, static_cast<T*>(ctx), stats, splits, part_o, part_ml);
+                                  n_stride, d_m, scale_log2, static_cast<T*>(ctx), stats, splits, parts.o, parts.ml);
     ELA_CHECK_LAUNCH();
     if (splits > 1) {
-        simt_merge_kernel<T><<<unsigned(total_rows), 256, 0, st>>>(part_o, part_ml, splits, total_rows, rows, npi,
+        simt_merge_kernel<T><<<unsigned(total_rows), 256, 0, st>>>(parts.o, parts.ml, splits, total_rows, rows, npi,
                                                                    n_stride, d_m, static_cast<T*>(ctx), stats);
         ELA_CHECK_LAUNCH();
-        cudaFreeAsync(part_o, st);
-        cudaFreeAsync(part_ml, st);
     }
 }
 
