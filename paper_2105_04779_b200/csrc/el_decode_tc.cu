@@ -75,6 +75,7 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max
 struct DecodeTuning {
     int s_ahead = 4;
     int l2_ahead = 0;
+    int skip_c_store = 0;  // TRACE builds only: drop the epilogue's global stores (timing experiments)
 };
 DecodeTuning g_tuning;
 
@@ -753,10 +754,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // scaled by sc[] (per query column of this thread) -> bf16 -> stage -> TMA store
             auto emit_unit = [&](int m, const uint32_t(&lo)[32], const uint32_t(&hi)[32], const float(&sc)[16]) {
                 if (warp == 2 && lane == 0) ELA_TRACE(24, li * 4 + m);
-                if (m > 0) {  // the previous unit's TMA store must have read the stage
-                    if (lane == 0) ptx::bulk_wait_group_read<0>();
-                    __syncwarp();
-                }
+                __syncwarp();  // every lane has read the previous unit out of the stage
                 if (warp == 2 && lane == 0) ELA_TRACE(25, li * 4 + m);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {  // query columns 8k..8k+7
@@ -774,13 +772,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::stmatrix_x4_trans(stm_base + k * 512 + ((stm_j ^ ((q >> 1) & 3u)) << 4), f[0], f[1], f[2],
                                            f[3]);
                 }
-                ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (warp == 2 && lane == 0) ELA_TRACE(26, li * 4 + m);
-                if (lane == 0) {
-                    ptx::tma_store_2d(&tm_c, my_stage, dm_off + m * 128 + int(qd) * 32, b * rows);
-                    ptx::bulk_commit_group();
+                // read the [64 q][32 d] stage back row-contiguous and store with st.global.v4:
+                // each instruction writes 8 query rows x 64 bytes (no TMA-store round trip,
+                // so the next unit can be staged at once and the next input's softmax is
+                // not held up behind store-read latency)
+                __nv_bfloat16* dst = ctx + int64_t(b) * rows * d_m + dm_off + m * 128 + int(qd) * 32;
+#pragma unroll
+                for (int s8 = 0; s8 < 8; ++s8) {
+                    const int q = s8 * 8 + int(lane >> 2), j = int(lane & 3);
+                    const uint4 v = ptx::lds_u4(ptx::smem_u32(my_stage) + q * 64 + ((j ^ ((q >> 1) & 3)) << 4));
+                    if (q < rows && !(TRACE && tune.skip_c_store))
+                        *reinterpret_cast<uint4*>(dst + int64_t(q) * d_m + 8 * j) = v;
                 }
+                if (warp == 2 && lane == 0) ELA_TRACE(28, li * 4 + m);
             };
             if (kind < 0) {
                 // whole input: normalise by 1/l and write
@@ -802,27 +808,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(o_full, li & 1);  // all O MMAs done: P buffers are free as stages
                 ptx::tc_fence_after();
                 if (warp == 2 && lane == 0) ELA_TRACE(19, li);
-                // software-pipelined: unit m+1 streams out of TMEM while unit m is
-                // converted, staged and stored (two register sets, fully unrolled)
-                uint32_t fr[2][2][32];  // [set][lo/hi][32]
-                ptx::tmem_ld_16x256b_x8(t_lane, fr[0][0]);
-                ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16), fr[0][1]);
-                ptx::tmem_ld_wait();
-                if (warp == 2 && lane == 0) ELA_TRACE(21, li);
-#pragma unroll
+                // unit by unit: TMEM -> registers -> bf16 stage -> st.global (the stores do
+                // not block, so no software pipelining is needed to hide them)
+#pragma unroll 1
                 for (int m = 0; m < UNITS; ++m) {
-                    if (m + 1 < UNITS) {
-                        ptx::tmem_ld_16x256b_x8(t_lane + (m + 1) * 64, fr[(m + 1) & 1][0]);
-                        ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16) + (m + 1) * 64, fr[(m + 1) & 1][1]);
-                    }
+                    uint32_t lo[32], hi[32];
+                    ptx::tmem_ld_16x256b_x8(t_lane + m * 64, lo);
+                    ptx::tmem_ld_16x256b_x8(t_lane + (16u << 16) + m * 64, hi);
+                    ptx::tmem_ld_wait();
+                    if (m == 0 && warp == 2 && lane == 0) ELA_TRACE(21, li);
                     if (m == UNITS - 1) {  // O read out: the next segment may overwrite it
                         ptx::tc_fence_before();
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(o_free);
                     }
                     if (warp == 2 && lane == 0) ELA_TRACE(27, li * 4 + m);
-                    emit_unit(m, fr[m & 1][0], fr[m & 1][1], inv_l);
-                    if (m + 1 < UNITS) ptx::tmem_ld_wait();
+                    emit_unit(m, lo, hi, inv_l);
                 }
             } else {
                 // segment of a split input: write its partial record (running max m and
@@ -862,9 +863,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
             if (warp == 2 && lane == 0) ELA_TRACE(23, li);
-            // stages alias P: every warp's last store must have read its stage before
-            // any warp writes P of the next input
-            if (lane == 0) ptx::bulk_wait_group_read<0>();
+            // stages alias P: every warp has read its stage back before any warp writes P
+            // of the next input
             softmax_bar_sync();
             if (warp == 2 && lane == 0) ELA_TRACE(15, li);
             G += T;
@@ -1137,6 +1137,7 @@ void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, 
     static const bool env_read = [] {
         if (const char* e = getenv("ELATTN_DECODE_S_AHEAD")) g_tuning.s_ahead = atoi(e);
         if (const char* e = getenv("ELATTN_DECODE_L2_AHEAD")) g_tuning.l2_ahead = atoi(e);
+        if (const char* e = getenv("ELATTN_DECODE_SKIP_C_STORE")) g_tuning.skip_c_store = atoi(e);
         return true;
     }();
     (void)env_read;

@@ -84,8 +84,9 @@ for B in a.B:
         print(f"   li={li}: 0 | {r(3, li * T - 1)} {r(17, li)} {r(18, li)} {r(22, li)} {r(16, li)} "
               f"{r(13, li * T)} {r(19, li - 1)} {r(21, li - 1)} {r(23, li - 1)} {r(15, li - 1)} {r(20, li)}")
     # epilogue units of input li=1 (full inputs only): tmem-ld done / stage free / staged / (next)
-    print("  epilogue units li=1 (rel. to o_full): m: ld_done wait_start stage_free staged")
+    print("  epilogue units li=1 (rel. to o_full): m: ld_done wait_start stage_free staged stored")
     base = t[0, 19, 1]
     for m in range(4):
         i = 4 + m
-        print(f"   m={m}: {int(t[0, 27, i] - base)} {int(t[0, 24, i] - base)} {int(t[0, 25, i] - base)} {int(t[0, 26, i] - base)}")
+        st = int(t[0, 28, i] - base) if t[0, 28, i] else None
+        print(f"   m={m}: {int(t[0, 27, i] - base)} {int(t[0, 24, i] - base)} {int(t[0, 25, i] - base)} {int(t[0, 26, i] - base)} {st}")
