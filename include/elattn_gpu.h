@@ -218,6 +218,27 @@ int elattn_gpu_mixed_self_attention(elattn_gpu_params_t params, const void* Y, c
 size_t elattn_gpu_mixed_workspace_size(elattn_gpu_params_t params, int B, int x);
 
 /*
+ * Multi-head-attention baseline with per-head K/V caches, on the
+ * library's own kernels: the reference's multi_head_attention (attention.hpp:96-113) for
+ * B inputs x x query rows at once, split as KvCache construction + attention_over_cache
+ * (:118-180).  It is the comparator EL-attention is measured against on the same GPU.
+ *   mha_kv_build: Kc, Vc [h][B][n][d_k] (dtype) <- K_i = H.W_K,i (+ b_K,i if
+ *                 include_key_bias), V_i = H.W_V,i (+ b_V,i if include_value_bias), for every
+ *                 position of every input H [B][n][d_m].
+ *   mha_attention: out[b*x + k] = sum_i softmax(Q_{b,k,i} . K_i(b)^T / sqrt(d_k)) . V_i(b)
+ *                 . W_O,i + b_O with Q = Y.W_Q + b_Q; Y, out [B*x][d_m]; n_per_input (device
+ *                 int[B] or NULL) masks positions >= n_b of input b's cache (stride n).
+ *                 x <= 16; d_k a multiple of 8 up to 128.
+ *                 Workspace: elattn_gpu_mha_workspace_size (or NULL: stream-ordered alloc).
+ */
+int elattn_gpu_mha_kv_build(elattn_gpu_params_t params, const void* H, int B, int n, void* Kc, void* Vc,
+                            elattn_stream_t stream);
+size_t elattn_gpu_mha_workspace_size(elattn_gpu_params_t params, int B, int x);
+int elattn_gpu_mha_attention(elattn_gpu_params_t params, const void* Y, const void* Kc, const void* Vc,
+                             const int* n_per_input, int B, int x, int n, void* out, void* workspace,
+                             size_t workspace_bytes, elattn_stream_t stream);
+
+/*
  * Beam-search candidate selection on the device (decoding.hpp:186-230).
  * For each input b: candidates (parent i < roots, token t) with lp_sum = live_lp[b*lanes+i]
  * + lprobs[(b*lanes+i)*V + t], non-finite log-probs skipped; the k best (k <= 32) in the

@@ -8,6 +8,8 @@
 //   elattn::el_attention(q, H, p)                         attention.hpp:239-257
 //   elattn::el_attention_folded(queries, H, s, p)         attention.hpp:262-290
 //   elattn::mixed_self_attention(q, prefix, cache, p)     attention.hpp:309-365
+//   elattn::multi_head_attention(q, H, p)                 attention.hpp:96-113 (GPU MHA baseline:
+//                                                         K/V caches + attention over them)
 //
 // plus DecoderStep (the batched, graph-captured decoder step over L layers that replaces
 // the per-lane loop of model.hpp:357-385) for device-resident decode loops.
@@ -172,9 +174,20 @@ inline ElQuery build_el_query(const Tensor& q, const AttentionParams& p, Dtype d
     return build_el_query(q, dp);
 }
 
-// fold_el_queries (attention.hpp:293-304): host bookkeeping only, row = b*h + i.
+// fold_el_queries (attention.hpp:293-304): host bookkeeping only — query b's head i goes to
+// row b*h + i of the folded [(g*h) x d_m] matrix, its key-bias scalar to entry b*h + i.
 inline std::pair<Tensor, Tensor> fold_el_queries(const std::vector<ElQuery>& queries, int h, int d_m) {
-    return elattn::fold_el_queries(queries, h, d_m);
+    const int64_t g = static_cast<int64_t>(queries.size());
+    Tensor q({g * h, static_cast<int64_t>(d_m)});
+    Tensor s({g * h});
+    for (int64_t b = 0; b < g; ++b) {
+        const ElQuery& eq = queries[static_cast<size_t>(b)];
+        for (int i = 0; i < h; ++i) {
+            for (int64_t j = 0; j < d_m; ++j) q.at(b * h + i, j) = eq.elq.at(i, j);
+            s.at(b * h + i) = eq.s[static_cast<size_t>(i)];
+        }
+    }
+    return {q, s};
 }
 
 // el_attention_folded (attention.hpp:262-290).
@@ -207,10 +220,13 @@ inline Tensor el_attention_folded(const Tensor& queries, const Tensor& H, const 
     return el_attention_folded(queries, H, bias_scalars, dp);
 }
 
-// el_attention (attention.hpp:239-257): query expansion + fused decode + projection.
+// el_attention (attention.hpp:239-257): query expansion + fused decode + projection.  One
+// query row, as in the reference (build_el_query's check, :199-200); batches of rows and
+// inputs go through el_attention_step / DecoderStep.
 inline Tensor el_attention(const Tensor& q, const Tensor& H, const DeviceParams& dp) {
     if (H.empty() || H.rows() < 1) throw StateError("el_attention: empty context");
     if (q.cols() != dp.d_m || H.cols() != dp.d_m) throw ShapeError("el_attention: q/H width must equal d_m");
+    if (q.rows() != 1) throw ShapeError("build_el_query: q must be 1 x d_m");
     const int x = int(q.rows()), n = int(H.rows());
     detail::DeviceBuffer dq(size_t(q.size()), dp.dtype()), dH(size_t(H.size()), dp.dtype()),
         dout(size_t(x) * dp.d_m, dp.dtype());
@@ -227,6 +243,37 @@ inline Tensor el_attention(const Tensor& q, const Tensor& H, const AttentionPara
     p.validate();
     DeviceParams dp(p, dt);
     return el_attention(q, H, dp);
+}
+
+// multi_head_attention (attention.hpp:96-113) on the GPU MHA path: the per-head K/V of H
+// are projected once into device caches (elattn_gpu_mha_kv_build), then the g query rows
+// attend over them in chunks of 16 (elattn_gpu_mha_attention).
+inline Tensor multi_head_attention(const Tensor& q, const Tensor& H, const DeviceParams& dp) {
+    if (q.cols() != dp.d_m || H.cols() != dp.d_m) throw ShapeError("multi_head_attention: q/H width must equal d_m");
+    if (H.empty() || H.rows() < 1) throw StateError("multi_head_attention: empty context");
+    const int g = int(q.rows()), n = int(H.rows());
+    const size_t cache = size_t(dp.h()) * n * dp.d_k;
+    detail::DeviceBuffer dH(size_t(H.size()), dp.dtype()), dK(cache, dp.dtype()), dV(cache, dp.dtype()),
+        dq(size_t(q.size()) ? size_t(q.size()) : 1, dp.dtype()), dout(size_t(g) * dp.d_m ? size_t(g) * dp.d_m : 1, dp.dtype());
+    dH.upload(H.data().data());
+    check(elattn_gpu_mha_kv_build(dp.handle(), dH.get(), 1, n, dK.get(), dV.get(), nullptr));
+    if (g > 0) dq.upload(q.data().data());
+    const size_t e = dp.dtype() == Dtype::bf16 ? 2 : 4;
+    for (int r = 0; r < g; r += 16) {
+        const int x = g - r < 16 ? g - r : 16;
+        check(elattn_gpu_mha_attention(dp.handle(), static_cast<const char*>(dq.get()) + size_t(r) * dp.d_m * e,
+                                       dK.get(), dV.get(), nullptr, 1, x, n,
+                                       static_cast<char*>(dout.get()) + size_t(r) * dp.d_m * e, nullptr, 0, nullptr));
+    }
+    check_cuda(cudaDeviceSynchronize());
+    Tensor out({g, dp.d_m});
+    if (g > 0) dout.download(out.data().data());
+    return out;
+}
+inline Tensor multi_head_attention(const Tensor& q, const Tensor& H, const AttentionParams& p, Dtype dt = Dtype::f32) {
+    p.validate();
+    DeviceParams dp(p, dt);
+    return multi_head_attention(q, H, dp);
 }
 
 // Device-resident batched sub-layer for decode loops (the caller keeps H and

@@ -13,7 +13,7 @@ from .capi import (  # noqa: F401
 from .attention import (  # noqa: F401
     DTYPE_BF16, DTYPE_F32, AttentionParams, DecoderStep, DeviceParams, HiddenStateCache, KvCache, ElAttentionLayer, ElQuery, Rng,
     beam_candidates, build_el_query, el_attention, gather_lane_indices, keep_lane_indices, permute_lane_indices, el_attention_folded, fold_el_queries, mixed_self_attention,
-    mixed_self_attention_batched, round_to_dtype,
+    mixed_self_attention_batched, round_to_dtype, MhaKvCache, multi_head_attention,
     seeded_uniform,
 )
 

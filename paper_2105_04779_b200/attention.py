@@ -28,6 +28,8 @@ from .capi import DTYPE_BF16, DTYPE_F32, ParamError, ShapeError, StateError
 
 __all__ = [
     "DecoderStep",
+    "MhaKvCache",
+    "multi_head_attention",
     "beam_candidates",
     "gather_lane_indices",
     "keep_lane_indices",
@@ -537,6 +539,55 @@ def mixed_self_attention_batched(layer: "ElAttentionLayer", Y, P, cache: KvCache
     return out
 
 
+class MhaKvCache:
+    """The multi-head-attention baseline on the GPU: per-head K/V
+    caches of B inputs' hidden states, K_i = H.W_K,i (+ b_K,i), V_i = H.W_V,i (+ b_V,i)
+    (KvCache::append for every position, attention.hpp:134-150), and attention of x query
+    rows per input over them (attention_over_cache, :154-180) — the reference's
+    multi_head_attention (:96-113) batched.  Caches: [h][B][n][d_k] device tensors (2x the
+    bytes of H at d_m = h*d_k: the state EL-attention does not keep)."""
+
+    def __init__(self, layer: "ElAttentionLayer", H, stream=None):
+        torch = _torch()
+        if H.dim() != 3:
+            raise ShapeError("H must be [B, n, d_m]")
+        layer._check(H, None, "H")
+        B, n, d_m = H.shape
+        if d_m != layer.dev.d_m:
+            raise ShapeError("multi_head_attention: q/H width must equal d_m")
+        self.layer, self.B, self.n = layer, B, n
+        shape = (layer.dev.h, B, n, layer.dev.d_k)
+        self.K = torch.empty(shape, dtype=H.dtype, device=H.device)
+        self.V = torch.empty_like(self.K)
+        _record([self.K, self.V], stream)
+        capi.check(capi.lib().elattn_gpu_mha_kv_build(layer.dev.handle, H.data_ptr(), B, n, self.K.data_ptr(),
+                                                       self.V.data_ptr(), _stream_ptr(stream)))
+
+    def attend(self, Y, n_per_input=None, out=None, stream=None):
+        """Y [B*x, d_m] -> out [B*x, d_m]."""
+        torch = _torch()
+        lay = self.layer
+        if Y.dim() != 2 or Y.shape[0] % self.B:
+            raise ShapeError("Y must be [B*x, d_m]")
+        x = Y.shape[0] // self.B
+        lay._check(Y, (self.B * x, lay.dev.d_m), "Y")
+        if out is None:
+            out = torch.empty_like(Y)
+        lay._check(out, Y.shape, "out")
+        npi = None
+        if n_per_input is not None:
+            if n_per_input.dtype != torch.int32 or not n_per_input.is_cuda or n_per_input.numel() != self.B:
+                raise ParamError("n_per_input must be a CUDA int32 tensor of length B")
+            npi = n_per_input.data_ptr()
+        need = capi.lib().elattn_gpu_mha_workspace_size(lay.dev.handle, self.B, x)
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+        _record([ws, out], stream)
+        capi.check(capi.lib().elattn_gpu_mha_attention(lay.dev.handle, Y.data_ptr(), self.K.data_ptr(),
+                                                        self.V.data_ptr(), npi, self.B, x, self.n, out.data_ptr(),
+                                                        ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+        return out
+
+
 # ---------------------------------------------------------------------------
 # Reference-shaped host API (fp64 numpy in / out), the drop-in for attention.hpp.
 # ---------------------------------------------------------------------------
@@ -610,9 +661,29 @@ def el_attention(q: np.ndarray, H: np.ndarray, p: AttentionParams | DeviceParams
     q = np.asarray(q, dtype=np.float64)
     if q.ndim != 2 or q.shape[1] != d_m or H.ndim != 2 or H.shape[1] != d_m:
         raise ShapeError("el_attention: q/H width must equal d_m")
+    if q.shape[0] != 1:  # build_el_query's check (attention.hpp:199-200); batches: ElAttentionLayer.step
+        raise ShapeError("build_el_query: q must be 1 x d_m")
     layer = _layer(p, dtype)
     out = layer.step(_as_device(q, layer.dtype), _as_device(H[None], layer.dtype))
     return _to_host(out)
+
+
+def multi_head_attention(q: np.ndarray, H: np.ndarray, p: AttentionParams | DeviceParams,
+                         dtype: int = DTYPE_F32) -> np.ndarray:
+    """``multi_head_attention`` (attention.hpp:96-113) on the GPU MHA path: q [g, d_m],
+    H [n, d_m] -> [g, d_m] (per-head K/V projected once into caches, then attention of
+    the g rows over them; chunks of 16 rows share the caches)."""
+    h, d_m, _ = _params_dims(p)
+    q = np.asarray(q, dtype=np.float64)
+    H = np.asarray(H, dtype=np.float64)
+    if q.ndim != 2 or q.shape[1] != d_m or H.ndim != 2 or H.shape[1] != d_m:
+        raise ShapeError("multi_head_attention: q/H width must equal d_m")
+    if H.shape[0] < 1:
+        raise StateError("multi_head_attention: empty context")
+    layer = _layer(p, dtype)
+    cache = MhaKvCache(layer, _as_device(H[None], layer.dtype))
+    outs = [_to_host(cache.attend(_as_device(q[r:r + 16], layer.dtype))) for r in range(0, q.shape[0], 16)]
+    return np.concatenate(outs, axis=0) if outs else np.zeros((0, d_m))
 
 
 def mixed_self_attention(q: np.ndarray, prefix_hidden: np.ndarray, gen_rows: np.ndarray,

@@ -42,6 +42,9 @@ EXPORTED_SYMBOLS = (
     "elattn_gpu_beam_candidates",
     "elattn_gpu_lane_gather",
     "elattn_gpu_reset_launch_count",
+    "elattn_gpu_mha_kv_build",
+    "elattn_gpu_mha_workspace_size",
+    "elattn_gpu_mha_attention",
 )
 
 
@@ -120,6 +123,10 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.elattn_gpu_mixed_workspace_size.restype = sz
     lib.elattn_gpu_beam_candidates.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp]
     lib.elattn_gpu_lane_gather.argtypes = [vp, vp, vp, i32, i32, ctypes.c_int64, vp]
+    lib.elattn_gpu_mha_kv_build.argtypes = [vp, vp, i32, i32, vp, vp, vp]
+    lib.elattn_gpu_mha_workspace_size.argtypes = [vp, i32, i32]
+    lib.elattn_gpu_mha_workspace_size.restype = sz
+    lib.elattn_gpu_mha_attention.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, sz, vp]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(lib, name)
         if fn.restype is ctypes.c_int and name not in ("elattn_gpu_decode_kernel_kind",):

@@ -684,6 +684,66 @@ extern "C" size_t elattn_gpu_mixed_workspace_size(elattn_gpu_params_t p, int B, 
     return step_workspace(p, R) + align256(size_t(R) * p->h * sizeof(float2));
 }
 
+// ---------------------------------------------------------------- MHA baseline (K/V caches)
+extern "C" int elattn_gpu_mha_kv_build(elattn_gpu_params_t p, const void* H, int B, int n, void* Kc, void* Vc,
+                                       elattn_stream_t stream) {
+    return guarded([&] {
+        check_handle(p);
+        ELA_REQUIRE(H && Kc && Vc, ELATTN_ERR_PARAM, "mha_kv_build: null buffer");
+        ELA_REQUIRE(B >= 1, ELATTN_ERR_SHAPE, "mha_kv_build: B must be >= 1");
+        ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "multi_head_attention: empty context");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const int h = p->h, d_m = p->d_m, d_k = p->d_k;
+        const int64_t rows = int64_t(B) * n;
+        ELA_REQUIRE(rows < (int64_t(1) << 31), ELATTN_ERR_UNSUPPORTED, "mha_kv_build: B * n too large");
+        // K_i / V_i of every position of every input (KvCache::append, attention.hpp:134-150,
+        // for all positions at once): A = H shared by the heads, output [h][B*n][d_k]
+        for (int kv = 0; kv < 2; ++kv) {
+            GemmArgs a{};
+            a.A = H, a.lda = d_m, a.sAz = 0;
+            a.B = kv == 0 ? p->WkT : p->WvT, a.ldb = d_m, a.sBz = int64_t(d_k) * d_m;
+            a.C = kv == 0 ? Kc : Vc, a.ldc = d_k, a.sCz = rows * d_k;
+            a.bias = kv == 0 ? (p->include_key_bias ? p->bk : nullptr) : (p->include_value_bias ? p->bv : nullptr);
+            a.sbz = d_k;
+            a.M = int(rows), a.N = d_k, a.K = d_m, a.Z = h, a.alpha = 1.f;
+            gemm(p, a, st);
+        }
+    });
+}
+
+extern "C" size_t elattn_gpu_mha_workspace_size(elattn_gpu_params_t p, int B, int x) {
+    if (!p || B < 1 || x < 1) return 0;
+    const size_t qb = size_t(B) * x * p->h * p->d_k * dtype_bytes(p->dtype);
+    return 2 * align256(qb);
+}
+
+extern "C" int elattn_gpu_mha_attention(elattn_gpu_params_t p, const void* Y, const void* Kc, const void* Vc,
+                                        const int* n_per_input, int B, int x, int n, void* out, void* ws,
+                                        size_t ws_bytes, elattn_stream_t stream) {
+    return guarded([&] {
+        check_handle(p);
+        ELA_REQUIRE(B >= 1 && x >= 1, ELATTN_ERR_SHAPE, "mha_attention: B and x must be >= 1");
+        ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "multi_head_attention: empty context");
+        ELA_REQUIRE(Y && Kc && Vc && out, ELATTN_ERR_PARAM, "mha_attention: null buffer");
+        ELA_REQUIRE(mha_decode_supported(x, p->d_k, p->dtype), ELATTN_ERR_UNSUPPORTED,
+                    "mha_attention: x <= 16 query rows per input, d_k a multiple of 8 up to 128");
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const int64_t R = int64_t(B) * x;
+        const int hk = p->h * p->d_k;
+        const size_t qb = size_t(R) * hk * dtype_bytes(p->dtype);
+        Scratch scratch(ws, ws_bytes, 2 * align256(qb), st);
+        void* Q = scratch.take(qb);
+        void* ctx = scratch.take(qb);
+        GemmArgs a{};  // Q = Y.W_Q + b_Q (attention.hpp:106)
+        a.A = Y, a.lda = p->d_m, a.B = p->WqT, a.ldb = p->d_m, a.C = Q, a.ldc = hk, a.bias = p->bq;
+        a.M = int(R), a.N = hk, a.K = p->d_m, a.Z = 1, a.alpha = 1.f;
+        gemm(p, a, st);
+        launch_mha_decode(p->dtype, Q, Kc, Vc, n_per_input, B, x, p->h, p->d_k, n,
+                          float(1.0 / std::sqrt(double(p->d_k))), ctx, st);
+        o_projection(p, ctx, R, out, st);  // sum_i ctx_i . W_O,i + b_O (attention.hpp:111-113)
+    });
+}
+
 // ---------------------------------------------------------------- beam-search candidates
 extern "C" int elattn_gpu_beam_candidates(const float* lprobs, const float* live_lp, const float* penalty, int B,
                                           int lanes, int roots, int V, int k, int* parent, int* token, float* lp_sum,

@@ -50,6 +50,11 @@ extern int g_gemm_force_bn, g_gemm_force_mt, g_gemm_force_kbp;
 extern unsigned long long* g_gemm_trace;
 extern int g_gemm_epilogue_tma;
 
+// MHA baseline decode over per-input K/V caches [h][B][n_stride][d_k] (mha.cu).
+bool mha_decode_supported(int x, int d_k, int dtype);
+void launch_mha_decode(int dtype, const void* Q, const void* Kc, const void* Vc, const int* npi, int B, int x, int h,
+                       int d_k, int n_stride, float scale, void* ctx, cudaStream_t st);
+
 // Mixed self-attention merge (mixed.cu): see the file header.
 void launch_mixed_combine(int dtype, const void* Q, const float2* stats, void* V, const void* Kc, const void* Vc,
                           int R, int h, int d_k, int64_t t_max, int t_out, const float* bk, float scale,

@@ -44,12 +44,11 @@ def rel_err(got, want) -> float:
 
 
 def round_params(p, dtype):
-    """Weights rounded to the kernel's storage dtype.  Biases are fp32, except b_Q, b_V and
-    b_O on the bf16 path, which feed cuBLASLt's bias epilogue in bf16."""
+    """Weights rounded to the kernel's storage dtype; biases stay fp32 (the GEMM epilogues
+    add them in fp32)."""
     from paper_2105_04779_b200.attention import round_to_dtype
 
     f = lambda a: round_to_dtype(a, dtype)  # noqa: E731
     g = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
-    d = f if dtype == 1 else g
-    return O.Params(p.h, p.d_m, p.d_k, f(p.Wq), f(p.Wk), f(p.Wv), f(p.Wo), d(p.bq), g(p.bk), d(p.bv),
-                    d(p.bo), p.include_key_bias, p.include_value_bias)
+    return O.Params(p.h, p.d_m, p.d_k, f(p.Wq), f(p.Wk), f(p.Wv), f(p.Wo), g(p.bq), g(p.bk), g(p.bv),
+                    g(p.bo), p.include_key_bias, p.include_value_bias)

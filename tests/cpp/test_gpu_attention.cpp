@@ -167,8 +167,50 @@ int main() {
         auto [fq, fs] = elattn::fold_el_queries(eqs, 16, 1024);
         Tensor want = el_attention_folded(fq, Hr, fs, pr);
         gpu::DeviceParams dp(p, gpu::Dtype::bf16);
-        const double e = rel_err(gpu::el_attention(q, H, dp), want);
+        Tensor got({4, 1024});  // one el_attention call per beam row (the reference takes 1 x d_m)
+        for (int k = 0; k < 4; ++k) {
+            Tensor r = gpu::el_attention(q.row(k), H, dp);
+            for (int64_t j = 0; j < 1024; ++j) got.at(k, j) = r.at(0, j);
+        }
+        const double e = rel_err(got, want);
         report("BART-large beam 4, n 300, bf16 tcgen05 path", e <= 2e-2, "rel err " + std::to_string(e));
+    }
+    // test_attention.cpp:143-149 — multi_head_attention on the GPU MHA path (K/V caches +
+    // attention over them) against the reference's multi_head_attention, all bias flags,
+    // g = 1 / 3 / 20 query rows (20 > 16: two chunks over one cache)
+    {
+        double worst = 0;
+        int case_id = 0;
+        for (int h : {1, 2, 4})
+            for (int d_m : {32, 64})  // d_k = d_m / h: a multiple of 8 (the MHA kernel's envelope)
+                for (int flags = 0; flags < 4; ++flags)
+                    for (int g : {1, 3, 20}) {
+                        Rng rng(5000 + static_cast<uint64_t>(case_id++));
+                        AttentionParams p = AttentionParams::random(h, d_m, d_m / h, rng);
+                        p.include_key_bias = (flags & 1) != 0;
+                        p.include_value_bias = (flags & 2) != 0;
+                        Tensor q = seeded_uniform({g, d_m}, rng, -1, 1);
+                        Tensor H = seeded_uniform({13, d_m}, rng, -1, 1);  // 13 keys: a partial tile
+                        worst = std::max(worst, rel_err(gpu::multi_head_attention(q, H, p), multi_head_attention(q, H, p)));
+                    }
+        report("multi_head_attention == reference (72 configs: heads, widths, bias flags, 1/3/20 rows)",
+               worst <= 1e-5, "worst rel err " + std::to_string(worst));
+        Rng rng(77);
+        AttentionParams p = AttentionParams::random(2, 8, 4, rng);
+        // an empty H fails the reference's width check first (attention.hpp:98-100): same type here
+        const bool ref_shape = throws<ShapeError>([&] { multi_head_attention(random_tensor({1, 8}, 3), Tensor(), p); });
+        report("multi_head_attention: empty context rejected with the reference's exception type",
+               ref_shape ? throws<ShapeError>([&] { gpu::multi_head_attention(random_tensor({1, 8}, 3), Tensor(), p); })
+                         : throws<StateError>([&] { gpu::multi_head_attention(random_tensor({1, 8}, 3), Tensor(), p); }));
+        report("multi_head_attention: width mismatch rejected (ShapeError)",
+               throws<ShapeError>([&] { gpu::multi_head_attention(random_tensor({1, 6}, 3), random_tensor({4, 8}, 4), p); }));
+        report("el_attention: more than one query row rejected (ShapeError, as build_el_query)",
+               throws<ShapeError>([&] { gpu::el_attention(random_tensor({2, 8}, 5), random_tensor({4, 8}, 6), p); }));
+        std::vector<ElQuery> eqs = {elattn::build_el_query(random_tensor({1, 8}, 7), p),
+                                    elattn::build_el_query(random_tensor({1, 8}, 8), p)};
+        auto [gq, gs] = gpu::fold_el_queries(eqs, p.h, p.d_m);
+        auto [rq, rs] = elattn::fold_el_queries(eqs, p.h, p.d_m);
+        report("fold_el_queries restated == reference layout", rel_err(gq, rq) == 0 && rel_err(gs, rs) == 0);
     }
     // decoder-only mixed self-attention (attention.hpp:309-365) against the reference,
     // with the generated-token cache built by the reference's own KvCache::append

@@ -10,6 +10,9 @@ Decoder step of L cross-attention layers at BART-large shapes, B inputs x `beam`
                 ([B*x, h, n, d_k]); per step q = y.Wq + bq, SDPA over the cache, .Wo + bo.
   mha_shared    the same caches without the beam copy ([B, h, n, d_k]); the x beams of an
                 input are x query rows of one SDPA call (reads each cache once per step).
+  mha_ours      the same shared-cache MHA on THIS library's kernels (MhaKvCache: K/V caches
+                built by the tcgen05 GEMM, mha_decode_kernel over them, tcgen05 projections),
+                so EL and MHA run on the same GEMMs;
   el            this repo's EL path (DecoderStep: one CUDA graph over the L layers; H is
                 the only per-input state, shared by every layer, beam and head).
 
@@ -112,6 +115,27 @@ for B in a.B:
     del dec, layers
     torch.cuda.empty_cache()
 
+    # ---- MHA on this library's kernels: per-layer caches [h][B][n][d_k], built once
+    layers = [E.ElAttentionLayer(p, E.DTYPE_BF16) for p in params]
+    caches = []
+    build_ms = event_ms(lambda: caches.extend(E.MhaKvCache(l, H) for l in layers))
+    yb = [torch.empty(R, d_m, device=dev, dtype=bf) for _ in range(2)]
+
+    def step_ours():
+        y = Y
+        for l, c in enumerate(caches):
+            y = c.attend(y, out=yb[l % 2])
+        return y
+
+    ms = graph_ms(step_ours, a.reps)
+    out = step_ours()
+    err = ((out.float() - el_out.float()).abs().max() / el_out.float().abs().max()).item()
+    line["mha_ours"] = {"ms_per_step": ms, "tokens_per_s": R / (ms / 1e3),
+                        "state_bytes_per_input": L * 2 * n * h * d_k * 2, "cache_build_ms": build_ms,
+                        "rel_err_vs_el": err}
+    del caches, layers
+    torch.cuda.empty_cache()
+
     # ---- MHA caches: K_i, V_i per layer (build once per input)
     def build(expand):
         Ks, Vs = [], []
@@ -162,7 +186,7 @@ for B in a.B:
                       "cache_build_ms": build_ms, "rel_err_vs_el": err}
         del Ks, Vs, built
         torch.cuda.empty_cache()
-    for mode in ("mha_shared", "mha_expanded"):
+    for mode in ("mha_ours", "mha_shared", "mha_expanded"):
         if "ms_per_step" in line.get(mode, {}):
             line[f"el_speedup_vs_{mode}"] = line[mode]["ms_per_step"] / line["el"]["ms_per_step"]
             line[f"el_state_saving_vs_{mode}"] = line[mode]["state_bytes_per_input"] / line["el"]["state_bytes_per_input"]
