@@ -41,6 +41,14 @@ int elattn_gpu_testing_set_pdl(int on);
  * done); NULL disables tracing. */
 int elattn_gpu_testing_set_gemm_trace(unsigned long long* trace);
 
+/* The fp32 path's 3xTF32 tensor-core GEMM on fp32 operands (split into hi/lo inside):
+ * C[z][m][n] = alpha * sum_k A[z][m][k] B[z][n][k] + bias[z][n]; with C_lo non-null the
+ * output is written as (C, C_lo) = (tf32(C), C - tf32(C)).  K % 32 == 0. */
+int elattn_gpu_testing_gemm_tf32x3(const float* A, int64_t lda, int64_t sAz, const float* B, int64_t ldb,
+                                   int64_t sBz, float* C, float* C_lo, int64_t ldc, int64_t sCz,
+                                   const float* bias, int64_t sbz, int M, int N, int K, int Z, float alpha,
+                                   elattn_stream_t stream);
+
 /* Stage (2) with an explicit kernel choice: 0 = SIMT, 1 = tcgen05. */
 int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H, const int* n_per_input, int B,
                                    int rows, int n, int d_m, float scale, void* ctx, int kernel,

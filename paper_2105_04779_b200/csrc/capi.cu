@@ -28,6 +28,12 @@ struct elattn_gpu_params_s {
     float* bk = nullptr;  // [h*d_k]
     float* bv = nullptr;  // [h*d_k] (zero when include_value_bias == 0)
     float* bo = nullptr;  // [d_m]
+    // fp32 path on the tensor cores (3xTF32, tf32_gemm.cu): tf32 hi / lo parts of the
+    // weights, split once here [0] = hi, [1] = lo; same layouts as above
+    float* WqT_s[2] = {nullptr, nullptr};
+    float* Wk_s[2] = {nullptr, nullptr};
+    float* WvT_s[2] = {nullptr, nullptr};
+    float* WoT_s[2] = {nullptr, nullptr};
 };
 
 namespace elattn_gpu {
@@ -104,13 +110,38 @@ void free_params(elattn_gpu_params_s* p) {
     for (void* ptr : {p->WqT, p->WkT, p->Wk, p->WvT, p->WoT, (void*)p->bq, (void*)p->bk, (void*)p->bv,
                       (void*)p->bo})
         if (ptr) cudaFree(ptr);
+    for (int s = 0; s < 2; ++s)
+        for (float* ptr : {p->WqT_s[s], p->Wk_s[s], p->WvT_s[s], p->WoT_s[s]})
+            if (ptr) cudaFree(ptr);
     delete p;
+}
+
+// tf32 rounding of the host side (cvt.rna.tf32.f32: nearest, ties away from zero)
+float tf32_rna_host(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+// fp32 weights as (hi, lo) device arrays
+void upload_split(const std::vector<double>& v, float* (&dst)[2]) {
+    std::vector<double> hi(v.size()), lo(v.size());
+    for (size_t i = 0; i < v.size(); ++i) {
+        const float f = float(v[i]), h = tf32_rna_host(f);
+        hi[i] = h;
+        lo[i] = f - h;
+    }
+    dst[0] = upload_f32(hi);
+    dst[1] = upload_f32(lo);
 }
 
 // Stream-ordered scratch: caller-provided or cudaMallocAsync'd for this call.
 class Scratch {
    public:
-    Scratch(void* ws, size_t ws_bytes, size_t need, cudaStream_t st) : st_(st) {
+    Scratch(void* ws, size_t ws_bytes, size_t need, cudaStream_t st) : st_(st), cap_(need) {
         if (need == 0) return;
         if (ws) {
             ELA_REQUIRE(ws_bytes >= need, ELATTN_ERR_PARAM,
@@ -125,16 +156,21 @@ class Scratch {
         if (owned_) cudaFreeAsync(base_, st_);
     }
     void* take(size_t bytes) {
+        ELA_REQUIRE(base_ != nullptr || bytes == 0, ELATTN_ERR_PARAM, "workspace: no scratch reserved");
         void* p = base_ + off_;
         off_ += (bytes + 255) & ~size_t(255);
+        ELA_REQUIRE(off_ <= cap_, ELATTN_ERR_PARAM, "workspace: scratch layout exceeds its reservation");
         return p;
     }
+    size_t mark() const { return off_; }
+    void reset(size_t m) { off_ = m; }
 
    private:
     char* base_ = nullptr;
     size_t off_ = 0;
     bool owned_ = false;
     cudaStream_t st_;
+    size_t cap_ = 0;
 };
 
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
@@ -203,6 +239,128 @@ void output_projection(const elattn_gpu_params_s* p, const void* C, int64_t R, v
                        cudaStream_t st) {
     v_projection(p, C, R, V, st);
     o_projection(p, V, R, out, st);
+}
+
+// ---------------------------------------------------------------- fp32 path on tensor cores
+// 3xTF32 (tf32_gemm.cu): every stage of a layer step as a tcgen05 kind::tf32 GEMM at fp32
+// accuracy; the decode as S = q'.H^T (per input), softmax, C = P.H (with a transposed hi/lo
+// copy of H).  Envelope: d_m, d_k, h*d_k multiples of 32, 16-byte aligned buffers.
+bool al16p(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+
+bool use_tf32_path(const elattn_gpu_params_s* p) {
+    return p->dtype == ELATTN_DTYPE_F32 && p->WqT_s[0] != nullptr && p->d_m % 32 == 0 && p->d_k % 32 == 0 &&
+           (p->h * p->d_k) % 32 == 0;
+}
+
+int64_t pad32(int64_t n) { return (n + 31) / 32 * 32; }
+
+// hi / lo views of one fp32 operand in the workspace
+struct Split {
+    float* hi = nullptr;
+    float* lo = nullptr;
+};
+Split take_split(Scratch& s, size_t count) {
+    Split r;
+    r.hi = static_cast<float*>(s.take(count * 4));
+    r.lo = static_cast<float*>(s.take(count * 4));
+    return r;
+}
+size_t split_bytes(size_t count) { return 2 * align256(count * 4); }
+
+// H split once per call (or per decoder step): H_s [B][n][d_m], HT_s [B][d_m][n_pad]
+size_t tf32_h_bytes(const elattn_gpu_params_s* p, int B, int n) {
+    return split_bytes(size_t(B) * n * p->d_m) + split_bytes(size_t(B) * p->d_m * pad32(n));
+}
+// per-layer intermediates for R = B * x query rows
+size_t tf32_layer_bytes(const elattn_gpu_params_s* p, int B, int x, int n) {
+    const size_t R = size_t(B) * x, hk = size_t(p->h) * p->d_k, hm = size_t(p->h) * p->d_m;
+    const size_t rows = size_t(x) * p->h;
+    return split_bytes(R * p->d_m) + split_bytes(R * hk) + split_bytes(R * hm) +
+           align256(size_t(B) * rows * pad32(n) * 4) + split_bytes(size_t(B) * rows * pad32(n)) + split_bytes(R * hm) +
+           split_bytes(R * hk);
+}
+
+void tf32_gemm(const Split& A, int64_t lda, int64_t sAz, const float* const (&W)[2], const Split* Bop,
+               int64_t ldb, int64_t sBz, float* C, float* C_lo, int64_t ldc, int64_t sCz, const float* bias,
+               int64_t sbz, int M, int N, int K, int Z, cudaStream_t st) {
+    Tf32GemmArgs g{};
+    g.A_hi = A.hi, g.A_lo = A.lo, g.lda = lda, g.sAz = sAz;
+    g.B_hi = Bop ? Bop->hi : W[0], g.B_lo = Bop ? Bop->lo : W[1], g.ldb = ldb, g.sBz = sBz;
+    g.C = C, g.C_lo = C_lo, g.ldc = ldc, g.sCz = sCz, g.bias = bias, g.sbz = sbz;
+    g.M = M, g.N = N, g.K = K, g.Z = Z, g.alpha = 1.f;
+    launch_tf32_gemm(g, st);
+}
+
+struct Tf32H {
+    Split H, HT;
+    int B = 0, n = 0;
+};
+Tf32H tf32_split_h(const elattn_gpu_params_s* p, Scratch& s, const float* H, const int* npi, int B, int n,
+                   cudaStream_t st) {
+    Tf32H h;
+    h.B = B, h.n = n;
+    h.H = take_split(s, size_t(B) * n * p->d_m);
+    h.HT = take_split(s, size_t(B) * p->d_m * pad32(n));
+    launch_tf32_split(H, int64_t(B) * n, p->d_m, p->d_m, h.H.hi, h.H.lo, npi, n, st);
+    launch_tf32_split_t(H, B, n, p->d_m, int(pad32(n)), npi, h.HT.hi, h.HT.lo, st);
+    return h;
+}
+
+// stage (1) from split rows Y: Q (split) and q' (split, or plain into qp_out)
+void tf32_query(const elattn_gpu_params_s* p, const Split& Y, int64_t R, const Split& Q, const Split& qp,
+                float* qp_out, cudaStream_t st) {
+    const int h = p->h, d_m = p->d_m, d_k = p->d_k, hk = h * d_k;
+    const float* const Wq[2] = {p->WqT_s[0], p->WqT_s[1]};
+    const float* const Wk[2] = {p->Wk_s[0], p->Wk_s[1]};
+    tf32_gemm(Y, d_m, 0, Wq, nullptr, d_m, 0, Q.hi, Q.lo, hk, 0, p->bq, 0, int(R), hk, d_m, 1, st);
+    tf32_gemm(Q, hk, d_k, Wk, nullptr, d_k, int64_t(d_m) * d_k, qp_out ? qp_out : qp.hi, qp_out ? nullptr : qp.lo,
+              int64_t(h) * d_m, d_m, nullptr, 0, int(R), d_m, d_k, h, st);
+}
+
+// stage (2): ctx rows (split, or plain into ctx_out) from split q' over the split H
+void tf32_decode(const elattn_gpu_params_s* p, Scratch& s, const Split& qp, const Tf32H& hs, const int* npi,
+                 int rows, const Split& ctx, float* ctx_out, float2* stats, cudaStream_t st) {
+    const int B = hs.B, n = hs.n, d_m = p->d_m;
+    const int64_t np = pad32(n);
+    float* S = static_cast<float*>(s.take(size_t(B) * rows * np * 4));
+    const Split P = take_split(s, size_t(B) * rows * np);
+    const float* const none[2] = {nullptr, nullptr};
+    // S_b = q'_b . H_b^T  (scores, scale applied in the softmax)
+    // (all n_pad columns: keys past n read as zeros; the softmax uses the first n_b)
+    tf32_gemm(qp, d_m, int64_t(rows) * d_m, none, &hs.H, d_m, int64_t(n) * d_m, S, nullptr, np, int64_t(rows) * np,
+              nullptr, 0, rows, int(np), d_m, B, st);
+    launch_tf32_softmax(S, int64_t(B) * rows, rows, n, int(np), npi, float(1.0 / std::sqrt(double(p->d_k))), P.hi,
+                        P.lo, stats, st);
+    // C_b = P_b . H_b  (B operand: H_b^T [d_m][n_pad], K-major over keys)
+    tf32_gemm(P, np, int64_t(rows) * np, none, &hs.HT, np, int64_t(d_m) * np, ctx_out ? ctx_out : ctx.hi,
+              ctx_out ? nullptr : ctx.lo, d_m, int64_t(rows) * d_m, nullptr, 0, rows, d_m, int(np), B, st);
+}
+
+// stage (3): out = sum_i (C_i.W_V,i + b_V,i).W_O,i + b_O from split ctx rows
+void tf32_output(const elattn_gpu_params_s* p, const Split& ctx, int64_t R, const Split& V, float* out,
+                 cudaStream_t st) {
+    const int h = p->h, d_m = p->d_m, d_k = p->d_k, hk = h * d_k;
+    const float* const Wv[2] = {p->WvT_s[0], p->WvT_s[1]};
+    const float* const Wo[2] = {p->WoT_s[0], p->WoT_s[1]};
+    tf32_gemm(ctx, int64_t(h) * d_m, d_m, Wv, nullptr, d_m, int64_t(d_k) * d_m, V.hi, V.lo, hk, d_k, p->bv, d_k,
+              int(R), d_k, d_m, h, st);
+    tf32_gemm(V, hk, 0, Wo, nullptr, hk, 0, out, nullptr, d_m, 0, p->bo, 0, int(R), d_m, hk, 1, st);
+}
+
+// one layer step on the fp32 tensor-core path (H already split)
+void tf32_layer(const elattn_gpu_params_s* p, Scratch& s, const float* Y, const Tf32H& hs, const int* npi, int x,
+                float* out, cudaStream_t st) {
+    const int64_t R = int64_t(hs.B) * x;
+    const size_t hk = size_t(p->h) * p->d_k, hm = size_t(p->h) * p->d_m;
+    const Split Ys = take_split(s, size_t(R) * p->d_m);
+    const Split Q = take_split(s, size_t(R) * hk);
+    const Split qp = take_split(s, size_t(R) * hm);
+    launch_tf32_split(Y, R, p->d_m, p->d_m, Ys.hi, Ys.lo, nullptr, 1, st);
+    tf32_query(p, Ys, R, Q, qp, nullptr, st);
+    const Split ctx = take_split(s, size_t(R) * hm);
+    tf32_decode(p, s, qp, hs, npi, x * p->h, ctx, nullptr, nullptr, st);
+    const Split V = take_split(s, size_t(R) * hk);
+    tf32_output(p, ctx, R, V, out, st);
 }
 
 bool use_tc_decode(const elattn_gpu_params_s* p, int rows_per_input) {
@@ -285,6 +443,12 @@ int elattn_gpu_params_create(int h, int d_m, int d_k, int dtype, int include_key
         p->bk = upload_f32(vbk);
         p->bv = upload_f32(vbv);
         p->bo = upload_f32(vbo);
+        if (dtype == ELATTN_DTYPE_F32) {
+            upload_split(wqT, p->WqT_s);
+            upload_split(wk, p->Wk_s);
+            upload_split(wvT, p->WvT_s);
+            upload_split(woT, p->WoT_s);
+        }
         *out = p.release();
     });
 }
@@ -304,8 +468,8 @@ int elattn_gpu_params_info(elattn_gpu_params_t p, int* h, int* d_m, int* d_k, in
 }
 
 size_t elattn_gpu_workspace_size(elattn_gpu_params_t p, int B, int g, int n) {
-    (void)n;
     if (!p || B < 1 || g < 1) return 0;
+    if (use_tf32_path(p) && n >= 1) return tf32_h_bytes(p, B, n) + tf32_layer_bytes(p, B, g, n);
     return step_workspace(p, int64_t(B) * g);
 }
 
@@ -322,6 +486,30 @@ int elattn_gpu_build_el_query(elattn_gpu_params_t p, const void* Y, int R, void*
         ELA_REQUIRE(Y && qprime, ELATTN_ERR_PARAM, "build_el_query: null buffer");
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         const size_t qbytes = size_t(R) * p->h * p->d_k * dtype_bytes(p->dtype);
+        if (use_tf32_path(p) && al16p(Y) && al16p(qprime)) {
+            // fp32 on the tensor cores: Q plain (for s), then split for q' = Q_i.W_K,i^T
+            const size_t hk = size_t(p->h) * p->d_k;
+            Scratch scratch(ws, ws_bytes, split_bytes(size_t(R) * p->d_m) + align256(qbytes) + split_bytes(R * hk), st);
+            const Split Ys = take_split(scratch, size_t(R) * p->d_m);
+            float* Q = static_cast<float*>(scratch.take(qbytes));
+            const Split Qs = take_split(scratch, size_t(R) * hk);
+            launch_tf32_split(static_cast<const float*>(Y), R, p->d_m, p->d_m, Ys.hi, Ys.lo, nullptr, 1, st);
+            const float* const Wq[2] = {p->WqT_s[0], p->WqT_s[1]};
+            const float* const Wk[2] = {p->Wk_s[0], p->Wk_s[1]};
+            tf32_gemm(Ys, p->d_m, 0, Wq, nullptr, p->d_m, 0, Q, nullptr, int64_t(hk), 0, p->bq, 0, R, int(hk), p->d_m,
+                      1, st);
+            launch_tf32_split(Q, R, int(hk), int64_t(hk), Qs.hi, Qs.lo, nullptr, 1, st);
+            tf32_gemm(Qs, int64_t(hk), p->d_k, Wk, nullptr, p->d_k, int64_t(p->d_m) * p->d_k,
+                      static_cast<float*>(qprime), nullptr, int64_t(p->h) * p->d_m, p->d_m, nullptr, 0, R, p->d_m,
+                      p->d_k, p->h, st);
+            if (s) {
+                if (p->include_key_bias)
+                    launch_key_bias_scalars(p->dtype, Q, p->bk, R, p->h, p->d_k, s, st);
+                else
+                    ELA_CHECK_CUDA(cudaMemsetAsync(s, 0, sizeof(float) * size_t(R) * p->h, st));
+            }
+            return;
+        }
         Scratch scratch(ws, ws_bytes, align256(qbytes), st);
         void* Q = scratch.take(qbytes);
         query_expansion(p, Y, R, Q, qprime, st);
@@ -346,6 +534,19 @@ int elattn_gpu_el_attention_folded(elattn_gpu_params_t p, const void* qprime, co
         ELA_REQUIRE(qprime && H && out, ELATTN_ERR_PARAM, "el_attention_folded: null buffer");
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         const int64_t R = int64_t(B) * g;
+        if (use_tf32_path(p) && al16p(qprime) && al16p(H) && al16p(out)) {
+            Scratch scratch(ws, ws_bytes, tf32_h_bytes(p, B, n) + tf32_layer_bytes(p, B, g, n), st);
+            const size_t hm = size_t(R) * p->h * p->d_m;
+            const Split qs = take_split(scratch, hm);
+            launch_tf32_split(static_cast<const float*>(qprime), int64_t(R) * p->h, p->d_m, p->d_m, qs.hi, qs.lo,
+                              nullptr, 1, st);
+            const Tf32H hs = tf32_split_h(p, scratch, static_cast<const float*>(H), n_per_input, B, n, st);
+            const Split ctx = take_split(scratch, hm);
+            tf32_decode(p, scratch, qs, hs, n_per_input, g * p->h, ctx, nullptr, nullptr, st);
+            const Split V = take_split(scratch, size_t(R) * p->h * p->d_k);
+            tf32_output(p, ctx, R, V, static_cast<float*>(out), st);
+            return;
+        }
         const size_t e = dtype_bytes(p->dtype);
         const size_t cbytes = size_t(R) * p->h * p->d_m * e, vbytes = size_t(R) * p->h * p->d_k * e;
         Scratch scratch(ws, ws_bytes, align256(cbytes) + align256(vbytes) + decode_scratch(p), st);
@@ -366,6 +567,19 @@ int elattn_gpu_el_attention_decode(elattn_gpu_params_t p, const void* qprime, co
         ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "el_attention_decode: empty context");
         ELA_REQUIRE(qprime && H && ctx, ELATTN_ERR_PARAM, "el_attention_decode: null buffer");
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        if (use_tf32_path(p) && al16p(qprime) && al16p(H) && al16p(ctx)) {
+            const size_t qn = size_t(B) * rows * p->d_m, np = size_t(pad32(n));
+            Scratch scratch(nullptr, 0,
+                            split_bytes(qn) + tf32_h_bytes(p, B, n) + align256(size_t(B) * rows * np * 4) +
+                                split_bytes(size_t(B) * rows * np),
+                            st);
+            const Split qs = take_split(scratch, qn);
+            launch_tf32_split(static_cast<const float*>(qprime), int64_t(B) * rows, p->d_m, p->d_m, qs.hi, qs.lo,
+                              nullptr, 1, st);
+            const Tf32H hs = tf32_split_h(p, scratch, static_cast<const float*>(H), n_per_input, B, n, st);
+            tf32_decode(p, scratch, qs, hs, n_per_input, rows, Split{}, static_cast<float*>(ctx), nullptr, st);
+            return;
+        }
         Scratch scratch(nullptr, 0, decode_scratch(p), st);
         decode(p, qprime, H, n_per_input, B, rows, n, ctx, static_cast<float*>(scratch.take(decode_scratch(p))), st);
     });
@@ -381,6 +595,12 @@ int elattn_gpu_el_attention_step(elattn_gpu_params_t p, const void* Y, const voi
         ELA_REQUIRE(Y && H && out, ELATTN_ERR_PARAM, "el_attention_step: null buffer");
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         const int64_t R = int64_t(B) * x;
+        if (use_tf32_path(p) && al16p(Y) && al16p(H) && al16p(out)) {
+            Scratch scratch(ws, ws_bytes, tf32_h_bytes(p, B, n) + tf32_layer_bytes(p, B, x, n), st);
+            const Tf32H hs = tf32_split_h(p, scratch, static_cast<const float*>(H), n_per_input, B, n, st);
+            tf32_layer(p, scratch, static_cast<const float*>(Y), hs, n_per_input, x, static_cast<float*>(out), st);
+            return;
+        }
         const size_t e = dtype_bytes(p->dtype);
         const size_t qb = size_t(R) * p->h * p->d_k * e, qpb = size_t(R) * p->h * p->d_m * e;
         Scratch scratch(ws, ws_bytes, step_workspace(p, R), st);
@@ -440,6 +660,32 @@ extern "C" int elattn_gpu_testing_set_gemm_trace(unsigned long long* trace) {
     return ELATTN_OK;
 }
 
+extern "C" int elattn_gpu_testing_gemm_tf32x3(const float* A, int64_t lda, int64_t sAz, const float* B, int64_t ldb,
+                                              int64_t sBz, float* C, float* C_lo, int64_t ldc,
+                                              int64_t sCz, const float* bias, int64_t sbz, int M, int N, int K, int Z,
+                                              float alpha, elattn_stream_t stream) {
+    return guarded([&] {
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        // operands split into (hi, lo) copies, then the 3xTF32 GEMM
+        const int64_t a_rows = (sAz == 0 || Z == 1) ? M : int64_t(Z) * sAz / lda;
+        const int64_t b_rows = (sBz == 0 || Z == 1) ? N : int64_t(Z) * sBz / ldb;
+        const size_t abytes = sizeof(float) * size_t(a_rows) * lda, bbytes = sizeof(float) * size_t(b_rows) * ldb;
+        Scratch sc(nullptr, 0, 2 * align256(abytes) + 2 * align256(bbytes), st);
+        float* Ah = static_cast<float*>(sc.take(abytes));
+        float* Al = static_cast<float*>(sc.take(abytes));
+        float* Bh = static_cast<float*>(sc.take(bbytes));
+        float* Bl = static_cast<float*>(sc.take(bbytes));
+        launch_tf32_split(A, a_rows, int(lda), lda, Ah, Al, nullptr, 1, st);
+        launch_tf32_split(B, b_rows, int(ldb), ldb, Bh, Bl, nullptr, 1, st);
+        Tf32GemmArgs g{};
+        g.A_hi = Ah, g.A_lo = Al, g.lda = lda, g.sAz = sAz;
+        g.B_hi = Bh, g.B_lo = Bl, g.ldb = ldb, g.sBz = sBz;
+        g.C = C, g.C_lo = C_lo, g.ldc = ldc, g.sCz = sCz, g.bias = bias, g.sbz = sbz;
+        g.M = M, g.N = N, g.K = K, g.Z = Z, g.alpha = alpha;
+        launch_tf32_gemm(g, st);
+    });
+}
+
 extern "C" int elattn_gpu_testing_set_decode_trace(unsigned long long* trace) {
     g_decode_trace = trace;
     return ELATTN_OK;
@@ -473,6 +719,7 @@ struct elattn_gpu_decoder_s {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int64_t kernels = 0;
+    bool tf32 = false;  // fp32 layers on the tensor-core path
 };
 
 namespace elattn_gpu {
@@ -496,6 +743,21 @@ void decoder_free(elattn_gpu_decoder_s* d) {
 void decoder_enqueue(elattn_gpu_decoder_s* d, const void* H, const int* npi, const void* Y_in, void* out) {
     const elattn_gpu_params_s* p0 = d->layers[0];
     const int64_t R = int64_t(d->B) * d->x;
+    if (d->tf32) {
+        // fp32 on the tensor cores: H split once per step, shared by the L layers
+        Scratch s(d->ws, d->ws_bytes, d->ws_bytes, d->st);
+        const Tf32H hs = tf32_split_h(p0, s, static_cast<const float*>(H), npi, d->B, d->n, d->st);
+        const size_t mark = s.mark();
+        const float* y = static_cast<const float*>(Y_in);
+        const int L = int(d->layers.size());
+        for (int l = 0; l < L; ++l) {
+            float* dst = static_cast<float*>((l == L - 1) ? out : d->ybuf[l & 1]);
+            s.reset(mark);
+            tf32_layer(d->layers[l], s, y, hs, npi, d->x, dst, d->st);
+            y = dst;
+        }
+        return;
+    }
     const size_t e = dtype_bytes(p0->dtype);
     const size_t qb = size_t(R) * p0->h * p0->d_k * e, qpb = size_t(R) * p0->h * p0->d_m * e;
     char* base = static_cast<char*>(d->ws);
@@ -543,7 +805,8 @@ extern "C" int elattn_gpu_decoder_create(const elattn_gpu_params_t* layers, int 
         ELA_CHECK_CUDA(cudaStreamCreateWithFlags(&d->st, cudaStreamNonBlocking));
         ELA_CHECK_CUDA(cudaMalloc(&d->ybuf[0], rows_bytes));
         ELA_CHECK_CUDA(cudaMalloc(&d->ybuf[1], rows_bytes));
-        d->ws_bytes = step_workspace(p0, R);
+        d->tf32 = use_tf32_path(p0) && al16p(H) && al16p(Y_in) && al16p(out);
+        d->ws_bytes = d->tf32 ? tf32_h_bytes(p0, B, n) + tf32_layer_bytes(p0, B, x, n) : step_workspace(p0, R);
         ELA_CHECK_CUDA(cudaMalloc(&d->ws, d->ws_bytes));
         // eager run first (surfaces launch errors directly).  The private stream does not
         // order after the caller's streams: wait for all prior device work (the caller may

@@ -50,6 +50,38 @@ extern int g_gemm_force_bn, g_gemm_force_mt, g_gemm_force_kbp;
 extern unsigned long long* g_gemm_trace;
 extern int g_gemm_epilogue_tma;
 
+// fp32 path on the tensor cores (tf32_gemm.cu): 3xTF32 GEMM
+//   C[z][m][n] = alpha * sum_k (A_hi B_hi + A_hi B_lo + A_lo B_hi) + bias[z][n]
+// A [z][m][k], B [z][n][k] (both K-major); C fp32, written as (C, C_lo) = (tf32(C),
+// C - tf32(C)) when C_lo != null.  K % 32 == 0.
+struct Tf32GemmArgs {
+    const float* A_hi;
+    const float* A_lo;
+    int64_t lda, sAz;
+    const float* B_hi;
+    const float* B_lo;
+    int64_t ldb, sBz;
+    float* C;
+    float* C_lo;
+    int64_t ldc, sCz;
+    const float* bias;
+    int64_t sbz;
+    int M, N, K, Z;
+    float alpha;
+};
+bool tf32_gemm_supported(const Tf32GemmArgs& g);
+void launch_tf32_gemm(const Tf32GemmArgs& g, cudaStream_t st);
+// X [rows][cols] (row stride ld) -> hi, lo [rows][cols]; rows r with npi and
+// r % n_stride >= npi[r / n_stride] are zeroed.
+void launch_tf32_split(const float* X, int64_t rows, int cols, int64_t ld, float* hi, float* lo, const int* npi,
+                       int n_stride, cudaStream_t st);
+// H [B][n][d_m] -> transposed hi/lo [B][d_m][n_pad], keys >= n_b (npi) or >= n zeroed
+void launch_tf32_split_t(const float* H, int B, int n, int d_m, int n_pad, const int* npi, float* hi, float* lo,
+                         cudaStream_t st);
+// softmax over the first n_b of each score row (see tf32_gemm.cu) -> (P_hi, P_lo), stats
+void launch_tf32_softmax(const float* S, int64_t total_rows, int rows, int n_stride, int ld, const int* npi,
+                         float scale, float* P_hi, float* P_lo, float2* stats, cudaStream_t st);
+
 // MHA baseline decode over per-input K/V caches [h][B][n_stride][d_k] (mha.cu).
 bool mha_decode_supported(int x, int d_k, int dtype);
 void launch_mha_decode(int dtype, const void* Q, const void* Kc, const void* Vc, const int* npi, int B, int x, int h,

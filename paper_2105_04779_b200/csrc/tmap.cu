@@ -27,6 +27,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                            const uint32_t* box, int swizzle_bytes) {
+    return make_tmap(base, 2, rank, dims, strides_bytes, box, swizzle_bytes);
+}
+
+CUtensorMap make_tmap(const void* base, int elem_bytes, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                      const uint32_t* box, int swizzle_bytes) {
     CUtensorMap m;
     ELA_REQUIRE(rank >= 1 && rank <= 5, ELATTN_ERR_PARAM, "tensor map rank must be 1..5");
     cuuint32_t elem_strides[5] = {1, 1, 1, 1, 1};
@@ -37,7 +42,8 @@ CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims, con
         boxd[i] = box[i];
     }
     for (int i = 0; i + 1 < rank; ++i) gstrides[i] = strides_bytes[i];
-    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, cuuint32_t(rank), const_cast<void*>(base),
+    const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUresult r = encode_fn()(&m, dt, cuuint32_t(rank), const_cast<void*>(base),
                              gdims, gstrides, boxd, elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE,
                              swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                              : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B

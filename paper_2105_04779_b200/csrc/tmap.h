@@ -16,5 +16,8 @@ namespace elattn_gpu {
 // on loads and clipped on stores.
 CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                            const uint32_t* box, int swizzle_bytes = 128);
+// same for bf16 (elem_bytes 2) or fp32 (elem_bytes 4) elements
+CUtensorMap make_tmap(const void* base, int elem_bytes, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                      const uint32_t* box, int swizzle_bytes = 128);
 
 }  // namespace elattn_gpu

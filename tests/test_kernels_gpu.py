@@ -299,3 +299,38 @@ def test_decode_instrumented_instantiation_matches():
     L.elattn_gpu_testing_set_decode_trace(None)
     assert torch.equal(outs[0], outs[1])
     assert int((tr != 0).sum()) > 0
+
+
+@pytest.mark.parametrize("M,N,K,Z,split", [
+    (128, 128, 64, 1, 0), (300, 1024, 1024, 1, 1),   # Q = Y.W_Q (fp32 path), M tail, split out
+    (64, 1000, 1024, 4, 0),                          # scores q'.H^T per input (N tail)
+    (64, 1024, 320, 3, 1),                           # C = P.H^T-copy per input, split out
+    (77, 64, 4096, 2, 0),                            # long K: chunked accumulation keeps fp32 accuracy
+])
+def test_tf32x3_gemm_vs_fp64(M, N, K, Z, split):
+    """The fp32 path's 3xTF32 tensor-core GEMM (split epilogue) against an fp64 reference:
+    fp32-class accuracy independent of K (each 32-wide k-block is its own MMA chain)."""
+    mn = 0
+    import torch
+
+    L, capi = _testing_lib()
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    L.elattn_gpu_testing_gemm_tf32x3.argtypes = [vp, i64, i64, vp, i64, i64, vp, vp, i64, i64, vp, i64,
+                                                 i32, i32, i32, i32, ctypes.c_float, vp]
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.rand(Z, M, K, generator=g, device="cuda") * 2 - 1
+    Bm = torch.rand(Z, K, N, generator=g, device="cuda") * 2 - 1 if mn else \
+        torch.rand(Z, N, K, generator=g, device="cuda") * 2 - 1
+    bias = torch.rand(Z, N, generator=g, device="cuda")
+    C = torch.zeros(Z, M, N, device="cuda")
+    C2 = torch.zeros_like(C) if split else None
+    ldb, sBz = (N, K * N) if mn else (K, N * K)
+    capi.check(L.elattn_gpu_testing_gemm_tf32x3(A.data_ptr(), K, M * K, Bm.data_ptr(), ldb, sBz, C.data_ptr(),
+                                                C2.data_ptr() if split else None, N, M * N, bias.data_ptr(), N,
+                                                M, N, K, Z, 0.75, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    Bk = Bm.double().transpose(1, 2) if mn else Bm.double()
+    want = 0.75 * torch.einsum("zmk,znk->zmn", A.double(), Bk) + bias.double()[:, None, :]
+    got = C.double() + (C2.double() if split else 0)
+    err = ((got - want).abs().max() / want.abs().max()).item()
+    assert err < 2e-6, err

@@ -180,11 +180,15 @@ def test_batch_bookkeeping_is_exact(gpu, dtype):
     assert np.array_equal(out2.reshape(B, c["x"], -1), out.reshape(B, c["x"], -1)[perm])
 
 
-def test_bf16_full_size_strided_subset(gpu):
-    """BART-large at B = 320 (the bench shape): a strided subset against the oracle."""
+@pytest.mark.parametrize("c,B,picks", [
+    (BART_CFG, 320, (0, 1, 157, 318, 319)),          # config 2 at the bench shape (stream-K / tail-split)
+    (TBIG_GREEDY_CFG, 512, (0, 255, 511)),           # config 3: greedy, 16 rows per input
+    (BEAM12_CFG, 32, (0, 13, 31)),                   # config 5: beam 12 = 3 virtual 64-row inputs
+])
+def test_bf16_full_size_strided_subset(gpu, c, B, picks):
+    """BASELINE configs 2, 3 and 5 at full batch on the GPU, a strided subset of inputs
+    checked against the oracle."""
     E = gpu
-    c = BART_CFG
-    B = 320
     import torch
 
     p = O.params_random(c["h"], c["d_m"], c["d_k"], O.OracleRng(1))
@@ -196,7 +200,7 @@ def test_bf16_full_size_strided_subset(gpu):
     out = layer.step(Yd, Hd).double().cpu().numpy()
     assert np.all(np.isfinite(out))
     pr = round_params(p, E.DTYPE_BF16)
-    for b in (0, 1, 157, 318, 319):
+    for b in picks:
         Yb = Yd[b * c["x"]:(b + 1) * c["x"]].double().cpu().numpy()
         Hb = Hd[b:b + 1].double().cpu().numpy()
         want = O.el_layer_step(pr, Yb, Hb, c["x"])

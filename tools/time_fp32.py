@@ -39,3 +39,14 @@ for B in (8, 32):
     print(json.dumps({"dtype": "fp32", "B": B, "layer_ms": round(ms_step, 3), "query_expansion_ms": round(ms_q, 3),
                       "folded_decode_and_projection_ms": round(ms_fold, 3),
                       "H_GBps": round(B * n * d_m * 4 / (ms_step / 1e3) / 1e9, 1)}), flush=True)
+
+# the decoder step (12 fp32 layers over the shared H: H split once per step)
+for B in (8, 32):
+    layers = [E.ElAttentionLayer(E.AttentionParams.random(h, d_m, d_k, E.Rng(1 + l)), E.DTYPE_F32) for l in range(12)]
+    H = torch.rand(B, n, d_m, device="cuda") * 2 - 1
+    dec = E.DecoderStep(layers, H, B, x)
+    dec.Y.copy_(torch.rand(B * x, d_m, device="cuda") * 2 - 1)
+    ms = timed(lambda: dec.run(), reps=5)
+    print(json.dumps({"dtype": "fp32", "B": B, "decoder_step_ms_12_layers": round(ms, 3),
+                      "per_layer_ms": round(ms / 12, 3)}), flush=True)
+    del dec, layers, H
