@@ -16,6 +16,7 @@ ap.add_argument("--B", type=int, default=320)
 ap.add_argument("--cfg", type=int, nargs=3, default=[0, 0, 0])
 ap.add_argument("--only", default=None)
 ap.add_argument("--warm", type=int, default=2)
+ap.add_argument("--kernel", type=int, default=1)
 a = ap.parse_args()
 L = capi.lib()
 vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
@@ -50,7 +51,7 @@ for name, (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z) in shape
     for _ in range(a.warm + 1):
         capi.check(L.elattn_gpu_testing_gemm_bf16(A.data_ptr(), lda, sAz, Bm.data_ptr(), ldb, sBz, C.data_ptr(), ldc,
                                                   sCz, bs.data_ptr() if bs is not None else None, sbz, M, N, K, Z,
-                                                  1.0, 1, torch.cuda.current_stream().cuda_stream))
+                                                  1.0, a.kernel, torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
 print("done")
 
@@ -66,7 +67,7 @@ for name, (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z) in shape
     e0.record()
     capi.check(L.elattn_gpu_testing_gemm_bf16(A.data_ptr(), lda, sAz, Bm.data_ptr(), ldb, sBz, C.data_ptr(), ldc,
                                               sCz, bs.data_ptr() if bs is not None else None, sbz, M, N, K, Z,
-                                              1.0, 1, torch.cuda.current_stream().cuda_stream))
+                                              1.0, a.kernel, torch.cuda.current_stream().cuda_stream))
     e1.record()
     torch.cuda.synchronize()
     capi.check(L.elattn_gpu_testing_set_gemm_trace(None))

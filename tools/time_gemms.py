@@ -18,6 +18,7 @@ ap.add_argument("--only", default=None, help="substring of the GEMM name to run"
 ap.add_argument("--no-cublas", action="store_true")
 ap.add_argument("--sweep", action="store_true", help="time every block-shape instantiation")
 ap.add_argument("--tma-epilogue", action="store_true")
+ap.add_argument("--kernel", type=int, default=1, help="1: tcgen05 with stream-K scratch, 2: data-parallel only")
 a = ap.parse_args()
 L = capi.lib()
 vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
@@ -83,7 +84,7 @@ for (A, lda, sAz, Bm, ldb, sBz, C, ldc, sCz, bs, sbz, M, N, K, Z), name, cfg in 
     def run():
         capi.check(L.elattn_gpu_testing_gemm_bf16(A.data_ptr(), lda, sAz, Bm.data_ptr(), ldb, sBz, C.data_ptr(), ldc,
                                                   sCz, bs.data_ptr() if bs is not None else None, sbz, M, N, K, Z,
-                                                  1.0, 1, torch.cuda.current_stream().cuda_stream))
+                                                  1.0, a.kernel, torch.cuda.current_stream().cuda_stream))
     run()
     torch.cuda.synchronize()
     us = graph_time(run, a.reps)
