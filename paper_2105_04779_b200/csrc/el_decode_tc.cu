@@ -136,7 +136,14 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 }
 
 // b is a VIRTUAL input: inputs with more than 64 query rows (beam > 4 at 16 heads) are
-// processed as rows/64 virtual inputs of 64 rows each that share H_{b / vchunks}.
+// processed as ceil(rows / 64) virtual inputs of up to 64 rows that share H_{b / vchunks}:
+// virtual input b covers query rows [vrow0, vrow0 + vnrows) of the q' / C matrices.
+__device__ __forceinline__ int vrow0(int b, int rows, int vchunks) {
+    return (b / vchunks) * rows + (b % vchunks) * kRowsQ;
+}
+__device__ __forceinline__ int vnrows(int b, int rows, int vchunks) {
+    return min(kRowsQ, rows - (b % vchunks) * kRowsQ);
+}
 __device__ __forceinline__ int tiles_of(const int* npi, int b, int n_stride, int vchunks) {
     const int n_b = npi ? npi[b / vchunks] : n_stride;
     return (n_b >= 1 && n_b <= n_stride) ? (n_b + kNT - 1) / kNT : 0;
@@ -272,7 +279,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t rank = ptx::cluster_ctarank(), peer = rank ^ 1u;
     const int cl = int(blockIdx.x >> 1), ncl = int(gridDim.x >> 1);
     const int dm_half = d_m / 2, dm_off = int(rank) * dm_half;
-    const int total_rows = B * rows;
+    const int total_rows = (B / sa.vchunks) * rows;  // B counts virtual inputs, rows real rows per input
 
     if (warp == 0) {
         if (ptx::elect_one()) {
@@ -357,7 +364,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (jj == (T > kQPrefetchTiles ? T - kQPrefetchTiles : 0) && nb >= 0 && nb != b) {
                         // warm L2 with the NEXT segment's q' (this CTA's d_m half) a few tiles
                         // before the transition (earlier, the streaming H evicts it again)
-                        for (int c = 0; c < 2 * UNITS; ++c) ptx::tma_prefetch_2d(&tm_q, dm_off + 64 * c, nb * rows);
+                        for (int c = 0; c < 2 * UNITS; ++c)
+                            ptx::tma_prefetch_2d(&tm_q, dm_off + 64 * c, vrow0(nb, rows, sa.vchunks));
                     }
                     if (jj == 0 && L::kQSmemUnits > 0) {
                         // this input's smem half of q', once the previous input's S no longer reads it
@@ -366,7 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         ptx::mbar_arrive_expect_tx(q_full, L::kQBytes);
                         for (int c = 0; c < 2 * L::kQSmemUnits; ++c)
                             ptx::tma_load_2d(sq + c * 8192, &tm_q, q_full, dm_off + 128 * L::kQTmemUnits + 64 * c,
-                                             b * rows, ptx::kEvictNormal);
+                                             vrow0(b, rows, sa.vchunks), ptx::kEvictNormal);
                     }
                 }
                 G += T;
@@ -507,9 +515,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 const int q = int(qd) * 16 + int(lane >> 2) + 8 * half;
-                const bool ok = int64_t(bb) * rows + q < int64_t(total_rows);
+                const int r0 = vrow0(bb, rows, sa.vchunks);
+                const bool ok = r0 + q < total_rows;
                 const uint2* src =
-                    reinterpret_cast<const uint2*>(qp_rows + (int64_t(bb) * rows + q) * d_m + dm_off) + (lane & 3);
+                    reinterpret_cast<const uint2*>(qp_rows + (int64_t(r0) + q) * d_m + dm_off) + (lane & 3);
 #pragma unroll
                 for (int u = 0; u < L::kQTmemUnits; ++u)
 #pragma unroll
@@ -778,12 +787,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // each instruction writes 8 query rows x 64 bytes (no TMA-store round trip,
                 // so the next unit can be staged at once and the next input's softmax is
                 // not held up behind store-read latency)
-                __nv_bfloat16* dst = ctx + int64_t(b) * rows * d_m + dm_off + m * 128 + int(qd) * 32;
+                __nv_bfloat16* dst = ctx + int64_t(vrow0(b, rows, sa.vchunks)) * d_m + dm_off + m * 128 + int(qd) * 32;
+                const int nr = vnrows(b, rows, sa.vchunks);
 #pragma unroll
                 for (int s8 = 0; s8 < 8; ++s8) {
                     const int q = s8 * 8 + int(lane >> 2), j = int(lane & 3);
                     const uint4 v = ptx::lds_u4(ptx::smem_u32(my_stage) + q * 64 + ((j ^ ((q >> 1) & 3)) << 4));
-                    if (q < rows && !(TRACE && tune.skip_c_store))
+                    if (q < nr && !(TRACE && tune.skip_c_store))
                         *reinterpret_cast<uint4*>(dst + int64_t(q) * d_m + 8 * j) = v;
                 }
                 if (warp == 2 && lane == 0) ELA_TRACE(28, li * 4 + m);
@@ -794,8 +804,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     s_l[ra] = 1.f / l_a;
                     s_l[rb] = 1.f / l_b;
                     if (stats != nullptr && rank == 0) {  // softmax stats in log2 units (both CTAs agree)
-                        if (ra < rows) stats[int64_t(b) * rows + ra] = make_float2(m_a * scale_log2, l_a);
-                        if (rb < rows) stats[int64_t(b) * rows + rb] = make_float2(m_b * scale_log2, l_b);
+                        const int r0 = vrow0(b, rows, sa.vchunks), nr = vnrows(b, rows, sa.vchunks);
+                        if (ra < nr) stats[r0 + ra] = make_float2(m_a * scale_log2, l_a);
+                        if (rb < nr) stats[r0 + rb] = make_float2(m_b * scale_log2, l_b);
                     }
                 }
                 softmax_bar_sync();
@@ -874,8 +885,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int b = cl; b < B; b += ncl) {
             if (tiles_of(n_per_input, b, n_stride, sa.vchunks) != 0) continue;
             const int tid = int(threadIdx.x) - 64;
-            for (int e = tid; e < rows * dm_half; e += 128)
-                ctx[(int64_t(b) * rows + e / dm_half) * d_m + dm_off + e % dm_half] =
+            const int r0 = vrow0(b, rows, sa.vchunks);
+            for (int e = tid; e < vnrows(b, rows, sa.vchunks) * dm_half; e += 128)
+                ctx[(int64_t(r0) + e / dm_half) * d_m + dm_off + e % dm_half] =
                     __float2bfloat16_rn(__int_as_float(0x7fc00000));
         }
     }
@@ -910,7 +922,7 @@ int num_sms_decode() {
 constexpr int kMaxSegs = 8;
 template <int UNITS>
 __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __restrict__ part, int T, int W, int ncl,
-                                                              int rows, int d_m, float scale_log2,
+                                                              int rows, int vchunks, int d_m, float scale_log2,
                                                               __nv_bfloat16* __restrict__ ctx,
                                                               float2* __restrict__ stats, int Bw) {
     constexpr int kPF = kPartFloatsHdr + UNITS * kPartFloatsUnit;
@@ -957,8 +969,8 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
                 L += ls[s] * w;
             }
         s_inv[tid] = 1.f / L;
-        if (stats != nullptr && rank == 0 && m == 0 && tid < rows)
-            stats[int64_t(b) * rows + tid] = make_float2(M * scale_log2, L);
+        if (stats != nullptr && rank == 0 && m == 0 && tid < vnrows(b, rows, vchunks))
+            stats[vrow0(b, rows, vchunks) + tid] = make_float2(M * scale_log2, L);
     }
     __syncthreads();
     // fragment float4 e = (h * 8 + i4) * 128 + t of the unit; this thread takes e = tid + 256 j
@@ -993,9 +1005,10 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
     }
     __syncthreads();
     const int dm_off = rank * (d_m / 2) + m * 128;
-    for (int e = tid; e < rows * 16; e += 256) {
+    const int r0 = vrow0(b, rows, vchunks);
+    for (int e = tid; e < vnrows(b, rows, vchunks) * 16; e += 256) {
         const int q = e >> 4, v = e & 15;
-        *reinterpret_cast<uint4*>(ctx + (int64_t(b) * rows + q) * d_m + dm_off + 8 * v) =
+        *reinterpret_cast<uint4*>(ctx + (int64_t(r0) + q) * d_m + dm_off + 8 * v) =
             *reinterpret_cast<const uint4*>(&tile[q][8 * v]);
     }
 }
@@ -1019,13 +1032,12 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
                   float scale_log2, void* ctx, cudaStream_t st, float2* stats, float* part) {
     // > 64 query rows per input: rows/64 virtual inputs of 64 rows each (q' and C rows are
     // contiguous per input, so virtual input v owns rows [64 v, 64 v + 64)); H_b is shared
-    const int vchunks = rows > kRowsQ ? rows / kRowsQ : 1;
+    const int vchunks = rows > kRowsQ ? (rows + kRowsQ - 1) / kRowsQ : 1;
     const int B_h = B;
-    B *= vchunks;
-    rows /= vchunks;
+    B *= vchunks;  // virtual inputs; `rows` stays the real rows per input
     // q' viewed as [B*rows][d_m]; box 64 rows (rows < 64 pad with the next input's
     // rows or OOB zeros; only the first `rows` outputs are written).
-    const uint64_t qdims[2] = {uint64_t(d_m), uint64_t(B) * rows};
+    const uint64_t qdims[2] = {uint64_t(d_m), uint64_t(B_h) * rows};
     const uint64_t qstr[1] = {uint64_t(d_m) * 2};
     const uint32_t qbox[2] = {64, kRowsQ};
     CUtensorMap tq = make_tmap_bf16(qp, 2, qdims, qstr, qbox);
@@ -1035,8 +1047,8 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     CUtensorMap th = make_tmap_bf16(H, 3, hdims, hstr, hbox);
     // C viewed as [B*rows][d_m]; box = one input's rows x 32 columns (one softmax warp's
     // d slab of a unit), SWIZZLE_64B to match the stmatrix stage layout
-    const uint64_t cdims[2] = {uint64_t(d_m), uint64_t(B) * rows};
-    const uint32_t cbox[2] = {32, uint32_t(rows)};
+    const uint64_t cdims[2] = {uint64_t(d_m), uint64_t(B_h) * rows};
+    const uint32_t cbox[2] = {32, uint32_t(rows < kRowsQ ? rows : kRowsQ)};
     CUtensorMap tc = make_tmap_bf16(ctx, 2, cdims, qstr, cbox, 64);
     // instrumented instantiation (trace hook, lookahead knobs) only when asked for
     const bool instr = g_decode_trace != nullptr || g_tuning.s_ahead != 4 || g_tuning.l2_ahead != 0;
@@ -1110,7 +1122,7 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
         const int Bw = B - last_round;
         const int gx = sa.W < 0 ? last_round : clusters - 1;
         launch_ex(el_decode_merge_kernel<UNITS>, dim3(gx, 2, UNITS), dim3(256), 0, st, 1, static_cast<const float*>(sa.part),
-                  sa.T, sa.W, clusters, rows, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx), stats, Bw);
+                  sa.T, sa.W, clusters, rows, vchunks, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx), stats, Bw);
         ELA_CHECK_LAUNCH();
     }
 }
@@ -1118,10 +1130,8 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
 }  // namespace
 
 bool el_decode_tc_supported(int rows_per_input, int d_m) {
-    // > 64 rows: as virtual inputs of 64 rows sharing H (multiples of 64 only, so every
-    // virtual input is full and the output boxes never cross an input)
-    const bool rows_ok = (rows_per_input >= 1 && rows_per_input <= kRowsQ) ||
-                         (rows_per_input % kRowsQ == 0 && rows_per_input <= 8 * kRowsQ);
+    // > 64 rows: as ceil(rows / 64) virtual inputs of up to 64 rows sharing H
+    const bool rows_ok = rows_per_input >= 1 && rows_per_input <= 8 * kRowsQ;
     return rows_ok && d_m % 256 == 0 && d_m >= 256 && d_m <= 1024;
 }
 
@@ -1129,7 +1139,7 @@ void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, 
                          int n_stride, int d_m, float scale, void* ctx, cudaStream_t st, float2* stats,
                          float* part) {
     ELA_REQUIRE(el_decode_tc_supported(rows_per_input, d_m), ELATTN_ERR_UNSUPPORTED,
-                "tcgen05 decode: rows <= 64 or a multiple of 64 (<= 512), d_m in {256, 512, 768, 1024}");
+                "tcgen05 decode: rows <= 512, d_m in {256, 512, 768, 1024}");
     ELA_REQUIRE((reinterpret_cast<uintptr_t>(qp) & 15) == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(ctx) & 15) == 0,
                 ELATTN_ERR_PARAM, "tcgen05 decode: q', H and C must be 16-byte aligned");

@@ -118,6 +118,7 @@ def decode_ref(qp, H, rows, scale, npi=None):
 @pytest.mark.parametrize("B,rows,n,d_m", [
     (1, 64, 32, 512), (2, 64, 1024, 1024), (3, 16, 77, 1024), (2, 48, 300, 256), (5, 64, 129, 768),
     (2, 128, 300, 1024), (3, 192, 1024, 512), (80, 192, 256, 1024),  # beam 8 / 12: virtual inputs
+    (2, 80, 300, 1024), (3, 96, 129, 512), (5, 160, 257, 1024),      # beam 5 / 6 / 10: partial virtual inputs
 ])
 def test_decode_vs_torch(kernel, B, rows, n, d_m):
     import torch

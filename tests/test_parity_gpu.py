@@ -117,7 +117,12 @@ def test_errors_are_reference_types(gpu):
 
 
 # ---------------------------------------------------------------- bf16 path
-@pytest.mark.parametrize("cfg,B", [(BART_CFG, 2), (ORACLE_CFG, 2), (TBIG_GREEDY_CFG, 3), (BEAM12_CFG, 1)])
+BEAM5_CFG = dict(BART_CFG, x=5)    # 80 query rows per input: a partial second 64-row virtual input
+BEAM10_CFG = dict(BART_CFG, x=10)  # 160 rows
+
+
+@pytest.mark.parametrize("cfg,B", [(BART_CFG, 2), (ORACLE_CFG, 2), (TBIG_GREEDY_CFG, 3), (BEAM12_CFG, 1),
+                                   (BEAM5_CFG, 3), (BEAM10_CFG, 2)])
 def test_bf16_step_vs_oracle(gpu, cfg, B):
     E = gpu
     p, Y, H = make_case(cfg["h"], cfg["d_m"], cfg["d_k"], cfg["n"], B, cfg["x"])
