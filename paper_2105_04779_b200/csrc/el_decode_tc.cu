@@ -162,6 +162,7 @@ struct SplitArgs {
     int W;           // tiles per cluster chunk (uniform stream-K); -P: TAIL-SPLIT (see Sched)
     float* part;     // partial records [2 * ncl slots][2 ranks][kPartFloats]
     int vchunks;     // virtual inputs per real input (query rows / 64 when rows > 64)
+    uint64_t h_pol;  // L2 policy of the H stream (evict-last when H fits in L2: the layers re-read it)
 };
 struct Sched {
     int T, W, B, ncl, n_stride, vchunks;
@@ -356,7 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const int col = dm_off + 128 * u;
                         // sibling virtual inputs (same H_b, running on neighbouring clusters)
                         // re-read the tile from L2: keep it there
-                        const uint64_t pol = sa.vchunks > 1 ? ptx::kEvictNormal : ptx::kEvictFirst;
+                        const uint64_t pol = sa.h_pol;
                         ptx::tma_load_3d(dst, &tm_h, &unit_full[s], col, j * kNT, b / sa.vchunks, pol);
                         ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, b / sa.vchunks,
                                          pol);
@@ -1072,6 +1073,27 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
         const std::string v(e);
         return v == "streamk" ? 1 : v == "whole" ? 2 : v == "tail" ? 3 : 0;
     }();
+    // H's L2 policy: streamed once (evict-first) unless it fits in L2 with room to spare —
+    // then every layer of a decoder step re-reads it from L2 (evict-last; measured 2% per
+    // step at B = 16, tools/time_small_batch.py); sibling virtual inputs (> 64 rows) share
+    // H_b across neighbouring clusters (evict-normal).
+    // ELATTN_DECODE_H_POLICY = auto | first | normal | last, ELATTN_DECODE_H_KEEP_MB (48)
+    static const int h_pol_mode = [] {
+        const char* e = getenv("ELATTN_DECODE_H_POLICY");
+        const std::string v = e ? e : "";
+        return v == "first" ? 1 : v == "normal" ? 2 : v == "last" ? 3 : 0;
+    }();
+    static const size_t h_keep_bytes = [] {
+        const char* e = getenv("ELATTN_DECODE_H_KEEP_MB");
+        return size_t(e ? atoi(e) : 48) << 20;
+    }();
+    const size_t h_bytes = size_t(B_h) * n_stride * d_m * 2;
+    sa.h_pol = h_pol_mode == 1   ? ptx::kEvictFirst
+               : h_pol_mode == 2 ? ptx::kEvictNormal
+               : h_pol_mode == 3 ? ptx::kEvictLast
+               : h_bytes <= h_keep_bytes ? ptx::kEvictLast
+               : vchunks > 1     ? ptx::kEvictNormal
+                                 : ptx::kEvictFirst;
     const bool stream_k = npi == nullptr && last_round != 0 &&
                           (sched_mode == 1 || sched_mode == 3 || (sched_mode == 0 && 5 * last_round < 3 * max_cl));
     // TAIL-SPLIT instead of stream-K when there is at least one full round and the leftover

@@ -24,6 +24,9 @@
 //               head-strided outputs such as q' rows r*h + i and V_i columns i*d_k are
 //               written in place).
 #include "common.cuh"
+
+#include <cstdlib>
+#include <string>
 #include "kernels.h"
 #include "ptx_sm100.cuh"
 #include "tmap.h"
@@ -84,6 +87,7 @@ struct GemmParams {
     __nv_bfloat16* C;      // output for the direct epilogue: C + z * sCz + m * ldc + n
     int64_t ldc, sCz;
     unsigned long long* trace;  // testing: %globaltimer stamps of CTA 0 (null = off)
+    uint64_t b_pol;             // L2 policy of the B (weight) loads
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -187,9 +191,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tma_load_4d(dst, &tmA, &full[s], 0, m0 + mt * kBM, za, kb, ptx::kEvictNormal);
                     }
                     if (p.b_zm)
-                        ptx::tma_load_4d(b, &tmB, &full[s], 0, z, n0, kb, ptx::kEvictLast);
+                        ptx::tma_load_4d(b, &tmB, &full[s], 0, z, n0, kb, p.b_pol);
                     else
-                        ptx::tma_load_4d(b, &tmB, &full[s], 0, n0, z, kb, ptx::kEvictLast);
+                        ptx::tma_load_4d(b, &tmB, &full[s], 0, n0, z, kb, p.b_pol);
                 }
             }
         }
@@ -427,6 +431,14 @@ void launch_cfg(const GemmArgs& g, cudaStream_t st) {
     p.direct = g_gemm_epilogue_tma < 0 ? (BN == 256 ? 0 : 1) : (g_gemm_epilogue_tma ? 0 : 1);
     p.C = static_cast<__nv_bfloat16*>(g.C), p.ldc = g.ldc, p.sCz = g.sCz;
     p.trace = g_gemm_trace;
+    // weights: evict-last keeps a weight tile in L2 while every M-block of this GEMM reads
+    // it; ELATTN_GEMM_W_POLICY=normal|first for L2 experiments (H residency at small B)
+    static const uint64_t w_pol = [] {
+        const char* e = getenv("ELATTN_GEMM_W_POLICY");
+        const std::string v = e ? e : "";
+        return v == "normal" ? ptx::kEvictNormal : v == "first" ? ptx::kEvictFirst : ptx::kEvictLast;
+    }();
+    p.b_pol = w_pol;
     CUtensorMap ta = load_map(g.A, g.lda, g.sAz, g.M, g.K, p.a_bcast ? 1 : g.Z, kBM, KBP, &p.a_zm);
     CUtensorMap tb = load_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, BN, KBP, &p.b_zm);
     CUtensorMap tc = store_map(g.C, g.ldc, g.sCz, g.M, g.N, g.Z, kBM, S::kPiece, &p.c_zm);

@@ -193,8 +193,8 @@ def test_decode_ragged_garbage_padding(kernel):
     (2, 16, 130, 512),      # rows < 64 and a masked last tile in a split input
 ])
 def test_decode_stream_k_schedules(B, rows, n, d_m):
-    """The stream-K schedule (inputs split across clusters, partial records merged by
-    el_decode_merge_kernel) against torch fp32, against the whole-input schedule (the same
+    """The stream-K schedule (inputs split across clusters, partial records merged inside
+    the decode kernel by the last segment to finish) against torch fp32, against the whole-input schedule (the same
     inputs passed with n_per_input), and run-to-run determinism."""
     import torch
 
@@ -245,7 +245,7 @@ def test_decode_virtual_inputs_ragged():
 def test_decode_schedules_agree_over_random_batches():
     """Stream-K (short last round) and whole-input schedules agree for a sweep of batch
     sizes / context lengths around the 74-cluster boundaries (first-boundary-in-input and
-    record-slot bookkeeping of the merge), and the result matches torch fp32."""
+    record-slot bookkeeping of the in-kernel merge), and the result matches torch fp32."""
     import torch
 
     L, capi = _testing_lib()
@@ -335,3 +335,52 @@ def test_tf32x3_gemm_vs_fp64(M, N, K, Z, split):
     got = C.double() + (C2.double() if split else 0)
     err = ((got - want).abs().max() / want.abs().max()).item()
     assert err < 2e-6, err
+
+
+@pytest.mark.parametrize("B", [20, 75, 320])
+def test_decode_split_records_garbage_workspace_and_graph_replay(B):
+    """Split inputs keep their partial records in the caller's workspace: a workspace full
+    of garbage bytes, a reused one, and repeated replays of a captured step all give the
+    bits of a fresh run.
+    B = 20 / 75: stream-K; B = 320: tail-split (4 full rounds + 24 inputs in 3 parts)."""
+    import torch
+
+    import paper_2105_04779_b200 as E
+    from paper_2105_04779_b200 import capi
+
+    h, d_m, d_k, x, n = 16, 1024, 64, 4, 1024
+    layer = E.ElAttentionLayer(E.AttentionParams.random(h, d_m, d_k, E.Rng(3)), E.DTYPE_BF16)
+    g = torch.Generator(device="cuda").manual_seed(B)
+    H = (torch.rand((B, n, d_m), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    Y = (torch.rand((B * x, d_m), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    L = capi.lib()
+    need = layer.dev.workspace_size(B, x, n)
+    st = torch.cuda.current_stream()
+
+    def run(ws, out):
+        capi.check(L.elattn_gpu_el_attention_step(layer.dev.handle, Y.data_ptr(), H.data_ptr(), None, B, x, n,
+                                                  out.data_ptr(), ws.data_ptr(), need, st.cuda_stream))
+
+    ref = torch.empty_like(Y)
+    run(torch.zeros(need, dtype=torch.uint8, device="cuda"), ref)
+    for fill in (0xFF, 0x5A):
+        ws = torch.full((need,), fill, dtype=torch.uint8, device="cuda")
+        for _ in range(2):  # reused workspace: counters left reset by the previous launch
+            out = torch.full_like(Y, float("nan"))
+            run(ws, out)
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref), fill
+    ws = torch.randint(0, 256, (need,), dtype=torch.uint8, device="cuda", generator=g)
+    out = torch.full_like(Y, float("nan"))
+    s2 = torch.cuda.Stream()
+    s2.wait_stream(st)
+    with torch.cuda.stream(s2):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s2):
+            capi.check(L.elattn_gpu_el_attention_step(layer.dev.handle, Y.data_ptr(), H.data_ptr(), None, B, x, n,
+                                                      out.data_ptr(), ws.data_ptr(), need, s2.cuda_stream))
+    for _ in range(3):
+        out.fill_(float("nan"))
+        gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
