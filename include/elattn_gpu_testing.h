@@ -29,6 +29,11 @@ int elattn_gpu_testing_gemm_bf16(const void* A, int64_t lda, int64_t sAz, const 
  * instantiation make the next GEMM fail with ELATTN_ERR_UNSUPPORTED. */
 int elattn_gpu_testing_gemm_config(int bn, int mt, int kbp);
 
+/* Small-M split-K GEMM (a cluster of sk CTAs per 128 x 64 output tile, partials reduced
+ * through DSMEM): sk in {2, 4, 8} forces it where the shape allows, 0 disables it, -1 =
+ * automatic (default: used when the plain tile grid would fill less than half the SMs). */
+int elattn_gpu_testing_gemm_splitk(int sk);
+
 /* GEMM epilogue: 0 = coalesced st.global through a per-warp smem transpose, 1 = 128-row
  * TMA tensor stores, -1 = per shape (default: TMA stores for the write-bound q' expansion). */
 int elattn_gpu_testing_gemm_epilogue(int tma);

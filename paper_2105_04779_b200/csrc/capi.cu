@@ -645,6 +645,14 @@ extern "C" int elattn_gpu_testing_gemm_config(int bn, int mt, int kbp) {
     });
 }
 
+extern "C" int elattn_gpu_testing_gemm_splitk(int sk) {
+    return guarded([&] {
+        ELA_REQUIRE(sk == -1 || sk == 0 || sk == 2 || sk == 4 || sk == 8, ELATTN_ERR_PARAM,
+                    "gemm_splitk: sk in {-1, 0, 2, 4, 8}");
+        g_gemm_force_splitk = sk;
+    });
+}
+
 extern "C" int elattn_gpu_testing_gemm_epilogue(int tma) {
     g_gemm_epilogue_tma = tma < 0 ? -1 : (tma ? 1 : 0);
     return ELATTN_OK;

@@ -34,6 +34,7 @@
 namespace elattn_gpu {
 
 int g_gemm_force_bn = 0, g_gemm_force_mt = 0, g_gemm_force_kbp = 0;  // testing / tuning override (0 = auto)
+int g_gemm_force_splitk = -1;  // testing / tuning override of the small-M split-K (-1 = auto, 0 = off)
 unsigned long long* g_gemm_trace = nullptr;                            // testing: timeline of CTA 0
 int g_gemm_epilogue_tma = -1;                                          // testing / tuning: 1 TMA stores, 0 st.global, -1 auto
 
@@ -363,6 +364,185 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------- split-K (small M)
+// For the projections of a SMALL batch (M = B*x rows <= a few hundred) the tile grid
+// above has 8-16 CTAs, each streaming the whole K through one TMA engine: latency-bound
+// (~9 us for a 128 x 1024 x 1024 GEMM).  Here a CLUSTER of SK CTAs shares one 128 x 64
+// output tile: CTA r multiplies k-blocks [r*nkb/SK, (r+1)*nkb/SK) (one TMA box per
+// operand, all in flight at once), then the partial accumulators are REDUCE-SCATTERED
+// through DSMEM: CTA r owns columns [r*W, (r+1)*W) (W = 64/SK), receives those columns
+// of the other SK-1 partials (st.async + mbarrier complete_tx) and sums all SK in rank
+// order (deterministic), adds the bias and stores bf16.
+//   warp 0: TMA (A and B boxes of this CTA's k-slice); warp 1: TMEM owner + MMA issuer;
+//   warps 2..5: TMEM lane quadrants (rows 32 qd ..): exchange, reduction, epilogue.
+constexpr int kSkBN = 64;
+constexpr int kSkThreads = 192;
+
+struct SkParams {
+    int M, N, K, Z, tiles_m, tiles_n, kbp, a_zm, b_zm, a_bcast, pdl;
+    float alpha;
+    const float* bias;
+    int64_t sbz;
+    __nv_bfloat16* C;
+    int64_t ldc, sCz;
+};
+
+template <int SK>
+struct SkSmem {
+    static constexpr int kW = kSkBN / SK;  // columns owned per CTA
+    static constexpr uint32_t kRecvBytes = uint32_t(SK - 1) * kBM * kW * 4;
+    static constexpr uint32_t kMaxKbp = 8;
+    static constexpr uint32_t kABytes = kBM * kBK * 2, kBBytes = kSkBN * kBK * 2;
+    static constexpr uint32_t kBOff = kMaxKbp * kABytes;
+    static constexpr uint32_t kRecvOff = kBOff + kMaxKbp * kBBytes;
+    static constexpr uint32_t kBarOff = kRecvOff + kRecvBytes;
+    static constexpr uint32_t kTotal = kBarOff + 64 + 1024;
+    static_assert(kTotal <= 232448, "split-K shared memory");
+};
+
+template <int SK, bool BIAS, bool SCALE>
+__global__ void __launch_bounds__(kSkThreads, 1)
+    tc_gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          SkParams p) {
+    using S = SkSmem<SK>;
+    constexpr int kW = S::kW;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + S::kBOff;
+    float* recv = reinterpret_cast<float*>(smem + S::kRecvOff);  // [SK-1][128 rows][kW]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOff);
+    uint64_t* acc_full = full + 1;
+    uint64_t* recv_full = full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 3);
+    const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+    const int rank = int(ptx::cluster_ctarank());
+    const int t = int(blockIdx.x) / SK;
+    const int z = t % p.Z, r_ = t / p.Z;
+    const int m0 = (r_ / p.tiles_n) * kBM, n0 = (r_ % p.tiles_n) * kSkBN;
+    const int kb0 = rank * p.kbp;
+
+    if (warp == 0) {
+        if (ptx::elect_one()) {
+            ptx::prefetch_tmap(&tmA);
+            ptx::prefetch_tmap(&tmB);
+            ptx::mbar_init(full, 1);
+            ptx::mbar_init(acc_full, 1);
+            ptx::mbar_init(recv_full, 1);
+            ptx::fence_mbar_init();
+            // the peers' partial columns may arrive before this CTA reaches its wait
+            if (SK > 1) ptx::mbar_arrive_expect_tx(recv_full, S::kRecvBytes);
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        ptx::tmem_alloc<64>(tmem_slot);
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // barriers initialised before any peer st.async targets them
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (p.pdl) {
+        ptx::griddep_launch_dependents();
+        ptx::griddep_wait();
+    }
+    if (warp == 0) {
+        if (ptx::elect_one()) {
+            ptx::mbar_arrive_expect_tx(full, uint32_t(p.kbp) * (S::kABytes + S::kBBytes));
+            const int za = p.a_bcast ? 0 : z;
+            if (p.a_zm)
+                ptx::tma_load_4d(sA, &tmA, full, 0, za, m0, kb0, ptx::kEvictNormal);
+            else
+                ptx::tma_load_4d(sA, &tmA, full, 0, m0, za, kb0, ptx::kEvictNormal);
+            if (p.b_zm)
+                ptx::tma_load_4d(sB, &tmB, full, 0, z, n0, kb0, ptx::kEvictLast);
+            else
+                ptx::tma_load_4d(sB, &tmB, full, 0, n0, z, kb0, ptx::kEvictLast);
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = ptx::idesc_bf16(kBM, kSkBN, 0, 0);
+        ptx::mbar_wait(full, 0);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+            const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA), 0, 1024);
+            const uint64_t b0 = ptx::sdesc_sw128(ptx::smem_u32(sB), 0, 1024);
+            for (int j = 0; j < p.kbp; ++j)
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                    ptx::mma_bf16(tmem, a0 + uint64_t((j * S::kABytes) >> 4) + uint64_t(2 * k),
+                                  b0 + uint64_t((j * S::kBBytes) >> 4) + uint64_t(2 * k), idesc, (j | k) != 0);
+            ptx::mma_commit(acc_full);
+        }
+        __syncwarp();
+    } else {
+        const uint32_t qd = warp & 3;
+        const int row = int(qd) * 32 + int(lane), m = m0 + row;
+        float bcol[kW];
+#pragma unroll
+        for (int j = 0; j < kW; ++j) {
+            const int n = n0 + rank * kW + j;
+            bcol[j] = (BIAS && n < p.N) ? __ldg(p.bias + z * p.sbz + n) : 0.f;
+        }
+        ptx::mbar_wait(acc_full, 0);
+        ptx::tc_fence_after();
+        uint32_t v[64];
+        ptx::tmem_ld32(tmem + ((qd * 32) << 16), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        ptx::tmem_ld32(tmem + ((qd * 32) << 16) + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        ptx::tmem_ld_wait();
+        if (SK > 1) {
+            // send column slice p of this row to CTA p (slot = this CTA's index among p's sources)
+#pragma unroll
+            for (int pr = 0; pr < SK; ++pr) {
+                if (pr == rank) continue;
+                const int slot = rank - (rank > pr ? 1 : 0);
+                const uint32_t dst = ptx::mapa(ptx::smem_u32(recv + (slot * kBM + row) * kW), uint32_t(pr));
+                const uint32_t bar = ptx::mapa(ptx::smem_u32(recv_full), uint32_t(pr));
+#pragma unroll
+                for (int j = 0; j < kW; j += 4)
+                    ptx::st_async_v4(dst + 4 * j, __uint_as_float(v[pr * kW + j]), __uint_as_float(v[pr * kW + j + 1]),
+                                     __uint_as_float(v[pr * kW + j + 2]), __uint_as_float(v[pr * kW + j + 3]), bar);
+            }
+            ptx::mbar_wait(recv_full, 0);
+        }
+        float acc[kW];
+#pragma unroll
+        for (int j = 0; j < kW; ++j) acc[j] = 0.f;
+#pragma unroll
+        for (int sr = 0; sr < SK; ++sr) {  // rank order: deterministic
+            if (sr == rank) {
+#pragma unroll
+                for (int j = 0; j < kW; ++j) acc[j] += __uint_as_float(v[rank * kW + j]);
+            } else {
+                const float* src = recv + ((sr - (sr > rank ? 1 : 0)) * kBM + row) * kW;
+#pragma unroll
+                for (int j = 0; j < kW; ++j) acc[j] += src[j];
+            }
+        }
+        if (m < p.M) {
+            __nv_bfloat16* dst = p.C + z * p.sCz + int64_t(m) * p.ldc + n0 + rank * kW;
+#pragma unroll
+            for (int j = 0; j < kW; j += 8) {
+                if (n0 + rank * kW + j + 8 > p.N) break;
+                uint4 o;
+                float f[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] = (SCALE ? acc[j + i] * p.alpha : acc[j + i]) + bcol[j + i];
+                o.x = pack2(f[0], f[1]);
+                o.y = pack2(f[2], f[3]);
+                o.z = pack2(f[4], f[5]);
+                o.w = pack2(f[6], f[7]);
+                *reinterpret_cast<uint4*>(dst + j) = o;
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // no CTA leaves while its partial columns are still in flight to a peer
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<64>(tmem);
+    }
+}
+
 // Maps over an operand X[z][r][k] (r = M or N rows, k contiguous).  Loads use 4-D maps
 // (64 k, r | z, z | r, k-block) whose k-block dimension has stride 128 B, so one box
 // carries `kbp` k-blocks of `box_rows` rows as [kb][row][64] — KBP SWIZZLE_128B K-major
@@ -491,6 +671,61 @@ Cfg choose(const GemmArgs& g) {
     return c;
 }
 
+// split-K for small M: cluster size SK (2, 4, 8), 0 when the tile grid already fills the GPU
+
+int choose_splitk(const GemmArgs& g) {
+    const int nkb = g.K / kBK;
+    const int64_t tiles = ceil_div(g.M, kBM) * ceil_div(g.N, kSkBN) * g.Z;
+    auto ok = [&](int sk) { return nkb % sk == 0 && nkb / sk <= int(SkSmem<2>::kMaxKbp) && (kSkBN / sk) % 8 == 0; };
+    if (g_gemm_force_splitk >= 0) return (g_gemm_force_splitk > 1 && ok(g_gemm_force_splitk)) ? g_gemm_force_splitk : 0;
+    static const int env = [] {
+        const char* e = getenv("ELATTN_GEMM_SPLITK");
+        return e ? atoi(e) : -1;
+    }();
+    if (env >= 0) return (env > 1 && ok(env)) ? env : 0;
+    if (nkb < 4 || 2 * tiles > num_sms()) return 0;
+    // one wave of co-resident clusters (tools/probes/cluster_occupancy_probe.cu on B200:
+    // 74 clusters of 2, 33 of 4, 15 of 8 for a one-CTA-per-SM kernel)
+    const int sms = num_sms();
+    const int64_t max_cl[3] = {sms / 2, (sms * 33) / 148, (sms * 15) / 148};
+    const int sks[3] = {2, 4, 8};
+    // the widest split that keeps about 64 CTAs (measured best at B = 16..128, beam 4:
+    // tools/time_small_batch.py), else pairs while one wave of pairs holds the tiles
+    for (int i = 2; i >= 0; --i)
+        if (ok(sks[i]) && tiles <= max_cl[i] && (tiles * sks[i] <= 64 || sks[i] == 2)) return sks[i];
+    return 0;
+}
+
+template <int SK, bool BIAS, bool SCALE>
+void launch_splitk_cfg(const GemmArgs& g, cudaStream_t st) {
+    using S = SkSmem<SK>;
+    SkParams p{};
+    p.M = g.M, p.N = g.N, p.K = g.K, p.Z = g.Z;
+    p.tiles_m = int(ceil_div(g.M, kBM));
+    p.tiles_n = int(ceil_div(g.N, kSkBN));
+    p.kbp = g.K / kBK / SK;
+    p.a_bcast = (g.Z > 1 && g.sAz == 0) ? 1 : 0;
+    p.pdl = pdl_enabled() ? 1 : 0;
+    p.alpha = g.alpha, p.bias = g.bias, p.sbz = g.sbz;
+    p.C = static_cast<__nv_bfloat16*>(g.C), p.ldc = g.ldc, p.sCz = g.sCz;
+    CUtensorMap ta = load_map(g.A, g.lda, g.sAz, g.M, g.K, p.a_bcast ? 1 : g.Z, kBM, p.kbp, &p.a_zm);
+    CUtensorMap tb = load_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, kSkBN, p.kbp, &p.b_zm);
+    auto kern = tc_gemm_splitk_kernel<SK, BIAS, SCALE>;
+    ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::kTotal)));
+    const int clusters = p.Z * p.tiles_m * p.tiles_n;
+    launch_ex(kern, dim3(clusters * SK), dim3(kSkThreads), S::kTotal, st, SK, ta, tb, p);
+    ELA_CHECK_LAUNCH();
+}
+
+template <int SK>
+void launch_splitk(const GemmArgs& g, cudaStream_t st) {
+    const bool bias = g.bias != nullptr, scale = g.alpha != 1.f;
+    if (bias && scale) return launch_splitk_cfg<SK, true, true>(g, st);
+    if (bias) return launch_splitk_cfg<SK, true, false>(g, st);
+    if (scale) return launch_splitk_cfg<SK, false, true>(g, st);
+    return launch_splitk_cfg<SK, false, false>(g, st);
+}
+
 }  // namespace
 
 bool tc_gemm_supported(const GemmArgs& g) {
@@ -500,6 +735,14 @@ bool tc_gemm_supported(const GemmArgs& g) {
 }
 
 void launch_tc_gemm(const GemmArgs& g, cudaStream_t st) {
+    if (!g_gemm_force_bn && !g_gemm_force_mt && !g_gemm_force_kbp) {
+        switch (choose_splitk(g)) {
+            case 8: return launch_splitk<8>(g, st);
+            case 4: return launch_splitk<4>(g, st);
+            case 2: return launch_splitk<2>(g, st);
+            default: break;
+        }
+    }
     const Cfg c = choose(g);
     const int key = c.bn * 100 + c.mt * 10 + c.kbp;
     switch (key) {

@@ -98,6 +98,30 @@ def test_gemm_block_shapes(bn, mt, kbp, M, N, K, Z, layout):
         capi.check(L.elattn_gpu_testing_gemm_epilogue(-1))
 
 
+@pytest.mark.parametrize("sk", [0, 2, 4, 8])
+@pytest.mark.parametrize("M,N,K,Z,layout", [
+    (128, 1024, 1024, 1, "plain"),      # Q = Y.W_Q / out = V.W_O at B = 32 (beam 4)
+    (128, 64, 1024, 16, "heads"),       # V_i = C_i.W_V,i at B = 32 (head-strided A and C)
+    (77, 192, 512, 3, "plain"),         # M and N tails
+    (256, 128, 1024, 2, "heads"),       # two m-tiles
+])
+def test_gemm_splitk(sk, M, N, K, Z, layout):
+    """The small-M split-K GEMM (cluster of sk CTAs per 128 x 64 tile, DSMEM reduce-scatter
+    of the partial accumulators) against torch fp32, against the plain tile kernel
+    (sk = 0), and bit-reproducible across runs (rank-ordered reduction)."""
+    L, capi = _testing_lib()
+    L.elattn_gpu_testing_gemm_splitk.argtypes = [ctypes.c_int]
+    capi.check(L.elattn_gpu_testing_gemm_splitk(sk))
+    try:
+        got, want = gemm_case(1, M, N, K, Z, layout, seed=M + N + K + sk, alpha=0.5)
+        err = (got - want).abs().max().item() / want.abs().max().item()
+        assert err < 1e-2, err
+        again, _ = gemm_case(1, M, N, K, Z, layout, seed=M + N + K + sk, alpha=0.5)
+        assert (again == got).all()
+    finally:
+        capi.check(L.elattn_gpu_testing_gemm_splitk(-1))
+
+
 def decode_ref(qp, H, rows, scale, npi=None):
     """torch fp32: C[b*rows+q] = softmax(q' H_b^T * scale) H_b."""
     import torch
