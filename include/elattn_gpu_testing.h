@@ -59,6 +59,11 @@ int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H, const int*
                                    int rows, int n, int d_m, float scale, void* ctx, int kernel,
                                    elattn_stream_t stream);
 
+/* Schedule of the tcgen05 decode for every following launch: 0 = automatic, 1 = stream-K,
+ * 2 = whole inputs strided over the clusters, 3 = tail-split.  With n_per_input the
+ * automatic choice is ragged stream-K up to 8 inputs per cluster. */
+int elattn_gpu_testing_decode_sched(int mode);
+
 /* Device buffer (>= 2*24*64 u64) that receives clock64 stamps from the first
  * cluster of every following tcgen05 decode launch; NULL disables tracing. */
 int elattn_gpu_testing_set_decode_trace(unsigned long long* trace);

@@ -645,6 +645,13 @@ extern "C" int elattn_gpu_testing_gemm_config(int bn, int mt, int kbp) {
     });
 }
 
+extern "C" int elattn_gpu_testing_decode_sched(int mode) {
+    return guarded([&] {
+        ELA_REQUIRE(mode >= 0 && mode <= 3, ELATTN_ERR_PARAM, "decode_sched: 0 auto, 1 stream-K, 2 whole, 3 tail");
+        g_decode_sched_override = mode;
+    });
+}
+
 extern "C" int elattn_gpu_testing_gemm_splitk(int sk) {
     return guarded([&] {
         ELA_REQUIRE(sk == -1 || sk == 0 || sk == 2 || sk == 4 || sk == 8, ELATTN_ERR_PARAM,

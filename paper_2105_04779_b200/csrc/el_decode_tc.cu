@@ -51,6 +51,7 @@
 namespace elattn_gpu {
 
 unsigned long long* g_decode_trace = nullptr;  // testing hook (elattn_gpu_testing_set_decode_trace)
+int g_decode_sched_override = 0;  // testing hook: 0 auto, 1 stream-K, 2 whole inputs, 3 tail-split
 
 namespace {
 
@@ -67,7 +68,15 @@ constexpr int kEpiWarpBytes = 4096;  // per-warp epilogue stage (64 q x 32 d bf1
 constexpr int kPartFloatsHdr = 128;
 constexpr int kPartFloatsUnit = 128 * 32;  // 32-bit words: 64 bf16 values per softmax thread
 constexpr int kQPrefetchTiles = 8;  // next segment's q' is prefetched into L2 this many tiles ahead
-constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale only when max grows by > 2^8
+constexpr float kRescaleThreshold = 8.0f;
+constexpr int kLptMaxTiles = 64;   // ragged longest-first: tile-count buckets (n_stride <= 2048)
+constexpr int kLptMaxList = 32;    // ragged longest-first: inputs per cluster
+// ragged schedules (static shared memory: the Sched objects of the six roles carry no
+// pointer to them): stream-K chunk {g0, g_end, b0, prefix} / longest-first list length,
+// the longest-first input list and the tile-count histogram
+__shared__ int s_rsched[4];
+__shared__ uint16_t s_lpt_list[kLptMaxList];
+__shared__ int s_lpt_hist[kLptMaxTiles + 1];  // log2 domain: rescale only when max grows by > 2^8
 
 // Tuning knobs (runtime so they can be swept):
 //   s_ahead  — how many tiles S may run ahead of O (<= kSBuf);
@@ -102,8 +111,10 @@ struct DecLayout {
     static constexpr uint32_t kLOff = kAlphaOff + 2 * 64 * 4;         // 64 fp32
     static constexpr uint32_t kBarOff = kLOff + 64 * 4;
     static constexpr int kNumBars = 2 * kRing + 24;
+    // + tmem slot; the ragged schedules' state is static shared memory (s_rsched, s_lpt_*)
+    static constexpr uint32_t kStaticSmem = 16 + kLptMaxList * 2 + (kLptMaxTiles + 1) * 4 + 64;
     static constexpr uint32_t kTotal = kBarOff + kNumBars * 8 + 16 + 1024;
-    static_assert(kTotal <= 232448, "shared memory budget");
+    static_assert(kTotal + kStaticSmem <= 232448, "shared memory budget");
     static_assert(kQTmemUnits >= 1, "at least one q' unit in TMEM");
     static_assert(4 * kEpiWarpBytes <= 2 * 8192, "epilogue stages alias the two P buffers");
 };
@@ -155,29 +166,49 @@ __device__ __forceinline__ int tiles_of(const int* npi, int b, int n_stride, int
 // still use every SM).  An input cut by a chunk boundary is processed as SEGMENTS by
 // consecutive clusters; each writes a partial record (unnormalised O, running max m, sum
 // l) and el_decode_merge_kernel combines them in cluster order (deterministic).
-// Otherwise (full last round, or ragged n_per_input): whole inputs, cluster c takes c,
+// RAGGED STREAM-K (n_per_input given, moderate B): the same cut over the sum of the
+// inputs' tile counts; every CTA finds its chunk start with a warp scan over n_per_input
+// (the prefix is not known on the host) and the merge kernel repeats the scan.
+// Otherwise (full last round, or many ragged inputs): whole inputs, cluster c takes c,
 // c+ncl, ...
+// RAGGED LONGEST-FIRST (default with n_per_input, no splitting): every CTA counting-sorts
+// the inputs by tile count (descending, stable) in its prologue and takes sorted positions
+// in boustrophedon order (round r: clusters 0..ncl-1, then ncl-1..0), the classic
+// longest-processing-time-first approximation — whole inputs, no partial records.
 struct SplitArgs {
-    int T;           // tiles per input (uniform mode), 0 = ragged / strided whole inputs
-    int W;           // tiles per cluster chunk (uniform stream-K); -P: TAIL-SPLIT (see Sched)
+    int T;           // tiles per input (uniform mode), 0 = ragged whole inputs (strided), -1 = ragged
+                     // stream-K, -2 = ragged longest-first (list per cluster)
+    int W;           // tiles per cluster chunk (uniform stream-K); -P: TAIL-SPLIT (see Sched);
+                     // ragged stream-K: the minimum chunk (the chunk is max(W, ceil(tiles / ncl)))
     float* part;     // partial records [2 * ncl slots][2 ranks][kPartFloats]
     int vchunks;     // virtual inputs per real input (query rows / 64 when rows > 64)
     uint64_t h_pol;  // L2 policy of the H stream (evict-last when H fits in L2: the layers re-read it)
 };
+// RAGGED: the ragged schedules (T < 0) are compiled only into the MASK instantiations (the
+// ones launched with n_per_input); the production kernel keeps its schedule state minimal.
+template <bool RAGGED>
 struct Sched {
     int T, W, B, ncl, n_stride, vchunks;
     const int* npi;
     int g, g_end, b;
     bool first;
-    __device__ Sched(const SplitArgs& sa, int cl, int ncl_, int B_, int n_stride_, const int* npi_)
+    // rs: ragged stream-K chunk of this cluster {g0, g_end, b0, prefix(b0)} (computed once per CTA)
+    __device__ Sched(const SplitArgs& sa, int cl, int ncl_, int B_, int n_stride_, const int* npi_, const int* rs)
         : T(sa.T), W(sa.W), B(B_), ncl(ncl_), n_stride(n_stride_), vchunks(sa.vchunks), npi(npi_), first(true) {
         if (T > 0) {
             g = cl * W;
             g_end = min(B * T, g + W);
+            b = cl;
+        } else if (RAGGED && T == -1) {
+            g = rs[0], g_end = rs[1], b = rs[2];
+            W = rs[3];  // ragged stream-K: W holds the prefix (first global tile) of input b
+        } else if (RAGGED && T == -2) {
+            g = 0, g_end = rs[0];  // ragged longest-first: position in / length of this cluster's list
+            b = 0;
         } else {
             g = g_end = 0;
+            b = cl;
         }
-        b = cl;
     }
     // next segment: input bb, tiles [j0, j1) of its Tb; kind -1 = whole input, 0 = first
     // segment of this cluster's chunk, 1 = last segment (partial-record slot 2*cl + kind)
@@ -201,6 +232,31 @@ struct Sched {
             j1 = (T * (c % P + 1)) / P;
             Tb = T, kind = 0;
             return j1 > j0;
+        }
+        if (RAGGED && T == -2) {
+            while (g < g_end) {
+                bb = s_lpt_list[g++];
+                Tb = tiles_of(npi, bb, n_stride, vchunks);
+                if (Tb == 0) continue;
+                j0 = 0, j1 = Tb, kind = -1;
+                return true;
+            }
+            return false;
+        }
+        if (RAGGED && T < 0) {
+            if (g >= g_end) return false;
+            int tb = tiles_of(npi, b, n_stride, vchunks);
+            while (W + tb <= g) {  // advance to the input holding tile g (W = its prefix)
+                W += tb;
+                tb = tiles_of(npi, ++b, n_stride, vchunks);
+            }
+            bb = b, Tb = tb;
+            j0 = g - W;
+            j1 = min(tb, g_end - W);
+            kind = (j0 == 0 && j1 == tb) ? -1 : (first ? 0 : 1);
+            first = false;
+            g = W + j1;
+            return true;
         }
         if (T > 0) {
             if (g >= g_end) return false;
@@ -226,6 +282,46 @@ struct Sched {
         return false;
     }
 };
+
+// Ragged stream-K bookkeeping (one warp, all lanes): total tiles of the B (virtual) inputs,
+// the chunk W = max(W_min, ceil(total / ncl)), and the input holding global tile g with its
+// prefix (first global tile).  Inputs with an out-of-contract length count 0 tiles.
+struct RaggedPos {
+    int total, W, b, prefix;
+};
+__device__ __forceinline__ RaggedPos ragged_locate(const int* npi, int B, int n_stride, int vchunks, int ncl,
+                                                   int W_min, int chunk_index, int g_override) {
+    const int lane = int(threadIdx.x & 31);
+    int tot = 0;
+    for (int i = lane; i < B; i += 32) tot += tiles_of(npi, i, n_stride, vchunks);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    RaggedPos r;
+    r.total = tot;
+    r.W = max(W_min, (tot + ncl - 1) / ncl);
+    const int g = g_override >= 0 ? g_override : chunk_index * r.W;
+    r.b = B, r.prefix = tot;
+    int base = 0;
+    for (int i0 = 0; i0 < B && g < tot; i0 += 32) {
+        const int t = i0 + lane < B ? tiles_of(npi, i0 + lane, n_stride, vchunks) : 0;
+        int incl = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int excl = base + incl - t;
+        const unsigned m = __ballot_sync(0xffffffffu, t > 0 && excl <= g && g < excl + t);
+        if (m) {
+            const int src = __ffs(m) - 1;
+            r.b = i0 + src;
+            r.prefix = __shfl_sync(0xffffffffu, excl, src);
+            break;
+        }
+        base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    return r;
+}
 
 template <int UNITS, bool TRACE, bool MASK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -275,6 +371,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* unit_empty = unit_full + kRing;
     uint64_t* o_done1 = unit_empty + kRing;  // per odd tile: O MMAs complete
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done1 + 1);
+    int* rsched = s_rsched;
+    uint16_t* lpt_list = s_lpt_list;
+    int* lpt_hist = s_lpt_hist;
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
     const uint32_t rank = ptx::cluster_ctarank(), peer = rank ^ 1u;
@@ -327,18 +426,86 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::griddep_launch_dependents();
         ptx::griddep_wait();
     }
+    if (MASK && sa.T == -2) {  // ragged longest-first: this cluster's inputs (n_per_input is read after the
+                       // PDL wait: a preceding kernel may have written it)
+        if (warp == 0) {
+            const uint32_t lt_mask = (1u << lane) - 1u;
+            // tile counts of inputs 512 s + 32 k + lane, k < 16: one round of sixteen loads in
+            // flight per lane covers B <= 512 (reused by both passes)
+            auto load16 = [&](int g0, int (&tl)[16]) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int i = g0 + 32 * k + int(lane);
+                    tl[k] = i < B ? min(tiles_of(n_per_input, i, n_stride, sa.vchunks), kLptMaxTiles) : -1;
+                }
+            };
+            for (int t = int(lane); t <= kLptMaxTiles; t += 32) lpt_hist[t] = 0;
+            __syncwarp();
+            int tl[16];
+            load16(0, tl);
+            for (int g0 = 0; g0 < B; g0 += 512) {  // histogram of tile counts
+                if (g0 > 0) load16(g0, tl);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {  // one add per distinct count (equal lengths: one per k)
+                    const uint32_t peers = __match_any_sync(0xffffffffu, tl[k]);
+                    if (tl[k] >= 0 && (peers & lt_mask) == 0) lpt_hist[tl[k]] += __popc(peers);
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {  // bucket starts, longest first (then by input index)
+                int acc = 0;
+                for (int t = kLptMaxTiles; t >= 0; --t) {
+                    const int c = lpt_hist[t];
+                    lpt_hist[t] = acc;
+                    acc += c;
+                }
+            }
+            __syncwarp();
+            int mine = 0;
+            for (int g0 = 0; g0 < B; g0 += 512) {  // sorted position of every input -> its cluster
+                if (g0 > 0 || B > 512) load16(g0, tl);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int t = tl[k];
+                    const uint32_t peers = __match_any_sync(0xffffffffu, t);
+                    const int pos = t >= 0 ? lpt_hist[t] + __popc(peers & lt_mask) : 0;
+                    __syncwarp();
+                    if (t >= 0 && (peers & lt_mask) == 0) lpt_hist[t] += __popc(peers);
+                    const int r = pos / ncl, kk = pos - r * ncl;
+                    const bool me = t >= 0 && ((r & 1) ? ncl - 1 - kk : kk) == cl;
+                    if (me) lpt_list[r] = uint16_t(g0 + 32 * k + int(lane));
+                    mine += __popc(__ballot_sync(0xffffffffu, me));
+                    __syncwarp();
+                }
+            }
+            if (lane == 0) rsched[0] = mine;  // positions r = 0..mine-1 are all filled (one per round)
+        }
+        __syncthreads();
+    } else if (MASK && sa.T == -1) {  // ragged stream-K: this cluster's chunk of the inputs' tiles
+        if (warp == 0) {
+            const RaggedPos r = ragged_locate(n_per_input, B, n_stride, sa.vchunks, ncl, sa.W, cl, -1);
+            if (lane == 0) {
+                rsched[0] = min(cl * r.W, r.total);
+                rsched[1] = min(cl * r.W + r.W, r.total);
+                rsched[2] = r.b;
+                rsched[3] = r.prefix;
+            }
+        }
+        __syncthreads();
+    }
 
     if (warp == 0) {
         // ================= TMA producer =================
         if (ptx::elect_one()) {
             int G = 0, li = 0;
-            Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+            Sched<MASK> sc(sa, cl, ncl, B, n_stride, n_per_input, rsched);
             int b, j0, j1, Tb, kind;
             while (sc.next(b, j0, j1, Tb, kind)) {
                 const int T = j1 - j0;
                 int nb = -1;  // input of the next segment (its q' is prefetched into L2)
                 {
-                    Sched pk = sc;
+                    Sched<MASK> pk = sc;
                     int a0, a1, a2, a3;
                     if (!pk.next(nb, a0, a1, a2, a3)) nb = -1;
                 }
@@ -392,7 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint64_t dQ = ptx::sdesc_sw128(ptx::smem_u32(sq), 0, 1024);
         const int parity_mine = warp == 1 ? 0 : 1;
         int G = 0, li = 0;
-        Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+        Sched<MASK> sc(sa, cl, ncl, B, n_stride, n_per_input, rsched);
         int b, j0, j1, Tb, kind;
         while (sc.next(b, j0, j1, Tb, kind)) {
             const int T = j1 - j0;
@@ -458,7 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint64_t dRingMN = ptx::sdesc_sw128(ptx::smem_u32(ring), kChunkBytes, 1024);
         const uint64_t dP = ptx::sdesc_sw128(ptx::smem_u32(sP), 0, 1024);
         int G = 0, li = 0;
-        Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+        Sched<MASK> sc(sa, cl, ncl, B, n_stride, n_per_input, rsched);
         int b, j0, j1, Tb, kind;
         while (sc.next(b, j0, j1, Tb, kind)) {
             const int T = j1 - j0;
@@ -532,7 +699,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             qv_b = bb;
         };
         int G = 0, li = 0;
-        Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+        Sched<MASK> sc(sa, cl, ncl, B, n_stride, n_per_input, rsched);
         int b, j0, j1, Tb, kind;
         while (sc.next(b, j0, j1, Tb, kind)) {
             const int T = j1 - j0;
@@ -549,7 +716,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (lane == 0) ptx::mbar_arrive(q_tmem_full);
                 if (warp == 6 && lane == 0) ELA_TRACE(18, li);
                 {
-                    Sched pk = sc;  // the next segment's q' is in flight while this one streams
+                    Sched<MASK> pk = sc;  // the next segment's q' is in flight while this one streams
                     int nb, a0, a1, a2, a3;
                     if (pk.next(nb, a0, a1, a2, a3) && nb != b) q_load(nb);
                 }
@@ -596,11 +763,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int G_total = 0;
         int b, j0, j1, Tb, kind;
         {
-            Sched pk(sa, cl, ncl, B, n_stride, n_per_input);
+            Sched<MASK> pk(sa, cl, ncl, B, n_stride, n_per_input, rsched);
             while (pk.next(b, j0, j1, Tb, kind)) G_total += j1 - j0;
         }
         int G = 0, li = 0;
-        Sched sc(sa, cl, ncl, B, n_stride, n_per_input);
+        Sched<MASK> sc(sa, cl, ncl, B, n_stride, n_per_input, rsched);
         while (sc.next(b, j0, j1, Tb, kind)) {
             const int T = j1 - j0;
             const int n_b = n_per_input ? n_per_input[b / sa.vchunks] : n_stride;
@@ -925,12 +1092,40 @@ template <int UNITS>
 __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __restrict__ part, int T, int W, int ncl,
                                                               int rows, int vchunks, int d_m, float scale_log2,
                                                               __nv_bfloat16* __restrict__ ctx,
-                                                              float2* __restrict__ stats, int Bw) {
+                                                              float2* __restrict__ stats, int Bw,
+                                                              const int* __restrict__ npi, int B, int n_stride) {
     constexpr int kPF = kPartFloatsHdr + UNITS * kPartFloatsUnit;
     ptx::griddep_wait();  // launched with PDL after the decode: its records must be complete
     const int rank = int(blockIdx.y), m = int(blockIdx.z);
     int b, c_first, nseg;
-    if (W < 0) {  // tail-split: input Bw + x in P = -W parts on clusters P x .. P x + P - 1 (slot 0)
+    int64_t first_tile = 0;  // b's first tile in the cut (stream-K): decides each segment's record slot
+    __shared__ int s_rag[4];  // ragged: b, prefix, tiles of b, chunk W (b < 0: no merge here)
+    if (T < 0) {
+        // ragged stream-K: the same scan as the decode kernel locates the input holding
+        // boundary k*W, its prefix and tile count
+        if (threadIdx.x < 32) {
+            const int k = int(blockIdx.x) + 1;
+            const RaggedPos r = ragged_locate(npi, B, n_stride, vchunks, ncl, W, k, -1);
+            const int gk = k * r.W;
+            const int tb = r.b < B ? tiles_of(npi, r.b, n_stride, vchunks) : 0;
+            // merged at b's first interior boundary only
+            const bool split = gk < r.total && gk != r.prefix && (k - 1) * r.W <= r.prefix;
+            if (threadIdx.x == 0) {
+                s_rag[0] = split ? r.b : -1;
+                s_rag[1] = r.prefix;
+                s_rag[2] = tb;
+                s_rag[3] = r.W;
+            }
+        }
+        __syncthreads();
+        if (s_rag[0] < 0) return;
+        b = s_rag[0];
+        const int pb = s_rag[1];
+        W = s_rag[3];
+        first_tile = pb;
+        c_first = pb / W;
+        nseg = min(kMaxSegs, (pb + s_rag[2] - 1) / W - c_first + 1);
+    } else if (W < 0) {  // tail-split: input Bw + x in P = -W parts on clusters P x .. P x + P - 1 (slot 0)
         b = Bw + int(blockIdx.x);
         c_first = int(blockIdx.x) * -W;
         nseg = -W;
@@ -939,7 +1134,8 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
         const int64_t gk = int64_t(k) * W;
         b = int(gk / T);
         if (gk % T == 0 || int64_t(k - 1) * W > int64_t(b) * T) return;  // not a split, or not b's first boundary
-        c_first = int((int64_t(b) * T) / W);
+        first_tile = int64_t(b) * T;
+        c_first = int(first_tile / W);
         nseg = min(kMaxSegs, int((int64_t(b) * T + T - 1) / W) - c_first + 1);
     }
     __shared__ const float* s_rec[kMaxSegs];
@@ -949,7 +1145,7 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
     const int tid = int(threadIdx.x);
     if (tid < nseg) {
         const int c2 = c_first + tid;
-        const int kd = (W < 0 || int64_t(c2) * W >= int64_t(b) * T) ? 0 : 1;  // b's segment is c2's first?
+        const int kd = (W < 0 || int64_t(c2) * W >= first_tile) ? 0 : 1;  // b's segment is c2's first?
         s_rec[tid] = part + (int64_t(2 * c2 + kd) * 2 + rank) * kPF;
     }
     __syncthreads();
@@ -1027,6 +1223,7 @@ size_t el_decode_tc_scratch_bytes(int d_m) {
 namespace {
 
 constexpr int kMinChunkTiles = 8;  // bounds the segments per input (merge cost) at small B
+constexpr int kRaggedSkMaxInputs = 8;  // ragged stream-K up to 8 inputs per cluster (beyond: whole inputs)
 
 template <int UNITS>
 void launch_units(const void* qp, const void* H, const int* npi, int B, int rows, int n_stride, int d_m,
@@ -1067,12 +1264,13 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     // so splitting only pays when the tail is short; measured on B200 for B = 64..320).
     const int last_round = B % max_cl;
     // ELATTN_DECODE_SCHED = auto (default) | streamk | tail | whole: tuning override
-    static const int sched_mode = [] {
+    static const int sched_mode_env = [] {
         const char* e = getenv("ELATTN_DECODE_SCHED");
         if (!e) return 0;
         const std::string v(e);
         return v == "streamk" ? 1 : v == "whole" ? 2 : v == "tail" ? 3 : 0;
     }();
+    const int sched_mode = g_decode_sched_override ? g_decode_sched_override : sched_mode_env;
     // H's L2 policy: streamed once (evict-first) unless it fits in L2 with room to spare —
     // then every layer of a decoder step re-reads it from L2 (evict-last; measured 2% per
     // step at B = 16, tools/time_small_batch.py); sibling virtual inputs (> 64 rows) share
@@ -1094,6 +1292,15 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
                : h_bytes <= h_keep_bytes ? ptx::kEvictLast
                : vchunks > 1     ? ptx::kEvictNormal
                                  : ptx::kEvictFirst;
+    // ragged lengths, moderate batch: stream-K over the inputs' own tile counts (whole-input
+    // striding leaves the clusters with the short inputs idle); ELATTN_DECODE_SCHED=whole off
+    // ragged lengths: whole inputs, longest first (default); stream-K over the inputs' own tiles
+    // only on request (ELATTN_DECODE_SCHED=streamk: splitting costs more than it balances,
+    // profiles/r02b_ragged.md)
+    const int T_stride = (n_stride + kNT - 1) / kNT;
+    const bool ragged_sk = npi != nullptr && sched_mode == 1 && B <= kRaggedSkMaxInputs * max_cl;
+    const bool ragged_lpt = npi != nullptr && !ragged_sk && sched_mode != 2 && B > max_cl && T_stride <= kLptMaxTiles &&
+                            B < 65536 && (B + max_cl - 1) / max_cl <= kLptMaxList;
     const bool stream_k = npi == nullptr && last_round != 0 &&
                           (sched_mode == 1 || sched_mode == 3 || (sched_mode == 0 && 5 * last_round < 3 * max_cl));
     // TAIL-SPLIT instead of stream-K when there is at least one full round and the leftover
@@ -1103,7 +1310,18 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const int P_tail = last_round > 0 ? std::min(kMaxSegs, std::min(max_cl / last_round, T_all)) : 0;
     const bool tail_split = stream_k && B >= max_cl && sched_mode != 1 && P_tail >= 2 &&
                             (sched_mode == 3 || 4 * last_round * P_tail >= 3 * max_cl);
-    if (tail_split) {
+    if (ragged_lpt) {
+        sa.T = -2;
+        sa.vchunks = vchunks;
+        clusters = B < max_cl ? B : max_cl;
+    } else if (ragged_sk) {
+        const int T_all_r = (n_stride + kNT - 1) / kNT;
+        sa.T = -1;
+        sa.W = std::max(kMinChunkTiles, (T_all_r + kMaxSegs - 2) / (kMaxSegs - 1));  // minimum chunk
+        sa.vchunks = vchunks;
+        sa.part = part;
+        clusters = max_cl;
+    } else if (tail_split) {
         sa.T = T_all;
         sa.W = -P_tail;
         sa.vchunks = vchunks;
@@ -1139,12 +1357,13 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
               static_cast<const __nv_bfloat16*>(qp), npi, B, rows, n_stride, d_m, scale_log2,
               static_cast<__nv_bfloat16*>(ctx), g_decode_trace, g_tuning, sa, stats, pdl_enabled() ? 1 : 0);
     ELA_CHECK_LAUNCH();
-    if ((sa.T > 0 && (sa.W < 0 || sa.W % sa.T != 0)) && clusters > 1) {
+    if (((sa.T > 0 && (sa.W < 0 || sa.W % sa.T != 0)) || sa.T == -1) && clusters > 1) {
         ELA_REQUIRE(part != nullptr, ELATTN_ERR_PARAM, "tcgen05 decode: split schedule needs the partial-record scratch");
         const int Bw = B - last_round;
         const int gx = sa.W < 0 ? last_round : clusters - 1;
         launch_ex(el_decode_merge_kernel<UNITS>, dim3(gx, 2, UNITS), dim3(256), 0, st, 1, static_cast<const float*>(sa.part),
-                  sa.T, sa.W, clusters, rows, vchunks, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx), stats, Bw);
+                  sa.T, sa.W, clusters, rows, vchunks, d_m, scale_log2, static_cast<__nv_bfloat16*>(ctx), stats, Bw,
+                  npi, B, n_stride);
         ELA_CHECK_LAUNCH();
     }
 }

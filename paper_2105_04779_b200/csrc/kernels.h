@@ -46,6 +46,7 @@ bool tc_gemm_supported(const GemmArgs& g);
 void launch_tc_gemm(const GemmArgs& g, cudaStream_t st);
 
 // Testing / tuning override of the tcgen05 GEMM block shape (0 = automatic choice).
+extern int g_decode_sched_override;
 extern int g_gemm_force_bn, g_gemm_force_mt, g_gemm_force_kbp, g_gemm_force_splitk;
 extern unsigned long long* g_gemm_trace;
 extern int g_gemm_epilogue_tma;

@@ -408,3 +408,44 @@ def test_decode_split_records_garbage_workspace_and_graph_replay(B):
         gr.replay()
         torch.cuda.synchronize()
         assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("B,rows,d_m", [(5, 64, 1024), (37, 64, 512), (150, 64, 512), (9, 192, 1024)])
+def test_decode_ragged_schedules(B, rows, d_m):
+    """Ragged batches under every schedule: longest-first whole inputs (the automatic
+    choice: in-kernel counting sort by tile count, boustrophedon over the clusters), ragged
+    stream-K (chunks of the inputs' own tiles, split inputs merged in cluster order) and
+    strided whole inputs.  Against torch fp32 with NaN padding past n_b; deterministic."""
+    import torch
+
+    L, capi = _testing_lib()
+    L.elattn_gpu_testing_decode_sched.argtypes = [ctypes.c_int]
+    n = 700
+    g = torch.Generator(device="cuda").manual_seed(B * 3 + rows)
+    qp = (torch.randn(B * rows, d_m, generator=g, device="cuda") * 0.3).to(torch.bfloat16)
+    H = (torch.rand(B, n, d_m, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    npi = torch.randint(1, n + 1, (B,), generator=g, device="cuda", dtype=torch.int32)
+    npi[0] = n
+    Hg = H.clone()
+    for b in range(B):
+        Hg[b, int(npi[b]):] = float("nan")
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    try:
+        for mode in (0, 0, 2, 1, 1):
+            capi.check(L.elattn_gpu_testing_decode_sched(mode))
+            ctx = torch.full((B * rows, d_m), float("nan"), device="cuda", dtype=torch.bfloat16)
+            capi.check(L.elattn_gpu_testing_decode_bf16(qp.data_ptr(), Hg.data_ptr(), npi.data_ptr(), B, rows, n, d_m,
+                                                        0.125, ctx.data_ptr(), 1, st))
+            torch.cuda.synchronize()
+            outs.append(ctx.float())
+    finally:
+        capi.check(L.elattn_gpu_testing_decode_sched(0))
+    want = decode_ref(qp, H, rows, 0.125, npi)
+    for o in outs:
+        assert torch.isfinite(o).all()
+        assert (o - want).abs().max().item() / want.abs().max().item() < 2e-2
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[3], outs[4])
+    for o in outs[2:]:
+        assert (outs[0] - o).abs().max().item() / want.abs().max().item() < 1e-2
