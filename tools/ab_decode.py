@@ -13,6 +13,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("libs", nargs="+")
 ap.add_argument("--B", type=int, nargs="+", default=[320, 296])
 ap.add_argument("--rounds", type=int, default=3)
+ap.add_argument("--x", type=int, default=4, help="beams per input (rows = x * 16 heads)")
 ap.add_argument("--child", action="store_true")
 a = ap.parse_args()
 
@@ -22,7 +23,7 @@ if a.child:
     capi.LIB_PATH = Path(a.libs[0]).resolve()
     import torch
     import paper_2105_04779_b200 as E
-    h, d_m, d_k, x, n = 16, 1024, 64, 4, 1024
+    h, d_m, d_k, x, n = 16, 1024, 64, a.x, 1024
     layer = E.ElAttentionLayer(E.AttentionParams.random(h, d_m, d_k, E.Rng(1)), E.DTYPE_BF16)
     L = capi.lib()
     res = {}
@@ -58,7 +59,8 @@ if a.child:
 out = {lib: {B: [] for B in a.B} for lib in a.libs}
 for r in range(a.rounds):
     for lib in a.libs:
-        p = subprocess.run([sys.executable, __file__, lib, "--child", "--B", *map(str, a.B)], capture_output=True,
+        p = subprocess.run([sys.executable, __file__, lib, "--child", "--x", str(a.x), "--B", *map(str, a.B)],
+                           capture_output=True,
                            text=True, cwd=ROOT)
         d = json.loads(p.stdout.strip().splitlines()[-1])
         for B in a.B:
