@@ -651,7 +651,7 @@ struct Cfg {
 // Block shape per GEMM (B200, 148 SMs):
 //   * N <= 64 (per-head V projection, N = d_k): 128 x 64 tiles, two m-subtiles per CTA
 //     sharing the weight slice when that still leaves one wave;
-//   * K <= 128 (q' expansion, write-bound): 128 x 256 tiles, one k-step;
+//   * K <= 128 (q' expansion, write-bound): 128 x 256 tiles (128 x 128 for small M), one k-step;
 //   * otherwise (Y.W_Q, V.W_O): 128 x 128 tiles;
 // with two k-blocks per TMA box whenever K allows.
 Cfg choose(const GemmArgs& g) {
@@ -661,7 +661,10 @@ Cfg choose(const GemmArgs& g) {
         const int64_t tiles = ceil_div(g.M, kBM) * g.Z;
         if (g.K >= 256 && tiles > num_sms()) c.mt = 2;
     } else if (g.K <= 128) {
-        c = {g.N >= 256 ? 256 : 128, 1, 1};
+        // write-bound q' expansion: 256-wide tiles, unless that leaves half the SMs idle
+        // (small batches: 128-wide, measured 3.4 vs 4.3 us at B = 32, tools/time_gemms.py)
+        const int64_t tiles256 = ceil_div(g.M, kBM) * ceil_div(g.N, 256) * g.Z;
+        c = {(g.N >= 256 && 2 * tiles256 >= num_sms()) ? 256 : 128, 1, 1};
     }
     if (g.K / kBK < 2) c.kbp = 1;
     if (g_gemm_force_bn) c.bn = g_gemm_force_bn;
