@@ -190,7 +190,9 @@ size_t step_workspace(const elattn_gpu_params_s* p, int64_t R) {
 
 // Every bf16 projection runs on the tcgen05 GEMM family (tc_gemm.cu); shapes outside its
 // envelope (K not a multiple of 64, unaligned rows) and the fp32 path use the SIMT kernel.
-void gemm(const elattn_gpu_params_s* p, const GemmArgs& g, cudaStream_t st) {
+void gemm(const elattn_gpu_params_s* p, const GemmArgs& g_in, cudaStream_t st) {
+    GemmArgs g = g_in;
+    g.b_static = 1;  // every B here is a packed weight of the params handle (written once, at create)
     if (p->dtype == ELATTN_DTYPE_BF16 && tc_gemm_supported(g))
         launch_tc_gemm(g, st);
     else
@@ -368,11 +370,14 @@ bool use_tc_decode(const elattn_gpu_params_s* p, int rows_per_input) {
 }
 
 // (2) fused decode: C = softmax(q'.H^T / sqrt(d_k)) . H   (attention.hpp:272-280)
+// h_static: H is not written by any kernel of the stream while these kernels run (the
+// decoder step's graph), so the decode may start streaming it before its PDL wait
 void decode(const elattn_gpu_params_s* p, const void* qp, const void* H, const int* npi, int B,
-            int rows_per_input, int n, void* C, float* part, cudaStream_t st, float2* stats = nullptr) {
+            int rows_per_input, int n, void* C, float* part, cudaStream_t st, float2* stats = nullptr,
+            bool h_static = false) {
     const float scale = float(1.0 / std::sqrt(double(p->d_k)));
     if (use_tc_decode(p, rows_per_input))
-        launch_el_decode_tc(qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats, part);
+        launch_el_decode_tc(qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats, part, h_static);
     else
         launch_el_decode_simt(p->dtype, qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats);
 }
@@ -787,7 +792,7 @@ void decoder_enqueue(elattn_gpu_decoder_s* d, const void* H, const int* npi, con
         void* dst = (l == L - 1) ? out : d->ybuf[l & 1];
         const elattn_gpu_params_s* p = d->layers[l];
         query_expansion(p, y, R, Q, qp, d->st);
-        decode(p, qp, H, npi, d->B, d->x * p->h, d->n, C, part, d->st);
+        decode(p, qp, H, npi, d->B, d->x * p->h, d->n, C, part, d->st, nullptr, /*h_static=*/true);
         output_projection(p, C, R, V, dst, d->st);
         y = dst;
     }

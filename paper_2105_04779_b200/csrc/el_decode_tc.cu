@@ -183,6 +183,8 @@ struct SplitArgs {
     float* part;     // partial records [2 * ncl slots][2 ranks][kPartFloats]
     int vchunks;     // virtual inputs per real input (query rows / 64 when rows > 64)
     uint64_t h_pol;  // L2 policy of the H stream (evict-last when H fits in L2: the layers re-read it)
+    int h_pre;       // H static across the stream's kernels (decoder step): tiles of the first segment
+                     // loaded BEFORE the programmatic-dependent-launch wait (0 = after it)
 };
 // RAGGED: the ragged schedules (T < 0) are compiled only into the MASK instantiations (the
 // ones launched with n_per_input); the production kernel keeps its schedule state minimal.
@@ -421,9 +423,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::cluster_sync();  // peer barriers initialised before any st.async / remote arrive targets them
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    int n_pre = 0;  // tiles of the first segment already in flight (issued before the PDL wait)
     if (pdl) {
         // prologue done (TMEM held): the next kernel may launch; wait for the previous one
         ptx::griddep_launch_dependents();
+        if constexpr (!MASK) {
+            // H does not depend on the preceding kernels (the decoder step reads the encoder
+            // state it was created with): start filling the ring now, so the first tiles'
+            // HBM latency overlaps the q' expansion's tail; q' itself follows after the wait
+            n_pre = sa.h_pre;
+            if (warp == 0 && n_pre > 0) {
+                Sched<MASK> pk(sa, cl, ncl, B, n_stride, n_per_input, rsched);
+                int b0, j0, j1, Tb0, k0;
+                if (!pk.next(b0, j0, j1, Tb0, k0)) j1 = j0;
+                n_pre = min(n_pre, j1 - j0);
+                if (ptx::elect_one()) {
+                    for (int jj = 0; jj < n_pre; ++jj)
+                        for (int u = 0; u < UNITS; ++u) {
+                            const int s = jj * UNITS + u;  // first lap of the ring: slots are free
+                            uint8_t* dst = ring + s * kUnitBytes;
+                            ptx::mbar_arrive_expect_tx(&unit_full[s], kUnitBytes);
+                            const int col = dm_off + 128 * u;
+                            ptx::tma_load_3d(dst, &tm_h, &unit_full[s], col, (j0 + jj) * kNT, b0 / sa.vchunks, sa.h_pol);
+                            ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, (j0 + jj) * kNT,
+                                             b0 / sa.vchunks, sa.h_pol);
+                        }
+                }
+                __syncwarp();
+            }
+        }
         ptx::griddep_wait();
     }
     if (MASK && sa.T == -2) {  // ragged longest-first: this cluster's inputs (n_per_input is read after the
@@ -516,6 +544,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, b / sa.vchunks);
                     for (int u = 0; u < UNITS; ++u) {
                         const int g = Gt * UNITS + u, s = g % kRing;
+                        if (Gt < n_pre) break;  // issued before the PDL wait
                         if (u == 0) ELA_TRACE(0, Gt);
                         ptx::mbar_wait(&unit_empty[s], ((g / kRing) & 1) ^ 1);
                         if (u == 0) ELA_TRACE(1, Gt);
@@ -1227,7 +1256,7 @@ constexpr int kRaggedSkMaxInputs = 8;  // ragged stream-K up to 8 inputs per clu
 
 template <int UNITS>
 void launch_units(const void* qp, const void* H, const int* npi, int B, int rows, int n_stride, int d_m,
-                  float scale_log2, void* ctx, cudaStream_t st, float2* stats, float* part) {
+                  float scale_log2, void* ctx, cudaStream_t st, float2* stats, float* part, bool h_static) {
     // > 64 query rows per input: rows/64 virtual inputs of 64 rows each (q' and C rows are
     // contiguous per input, so virtual input v owns rows [64 v, 64 v + 64)); H_b is shared
     const int vchunks = rows > kRowsQ ? (rows + kRowsQ - 1) / kRowsQ : 1;
@@ -1301,6 +1330,7 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const bool ragged_sk = npi != nullptr && sched_mode == 1 && B <= kRaggedSkMaxInputs * max_cl;
     const bool ragged_lpt = npi != nullptr && !ragged_sk && sched_mode != 2 && B > max_cl && T_stride <= kLptMaxTiles &&
                             B < 65536 && (B + max_cl - 1) / max_cl <= kLptMaxList;
+    sa.h_pre = (h_static && npi == nullptr && pdl_enabled()) ? std::min(DecLayout<UNITS>::kRing / UNITS, 8) : 0;
     const bool stream_k = npi == nullptr && last_round != 0 &&
                           (sched_mode == 1 || sched_mode == 3 || (sched_mode == 0 && 5 * last_round < 3 * max_cl));
     // TAIL-SPLIT instead of stream-K when there is at least one full round and the leftover
@@ -1378,7 +1408,7 @@ bool el_decode_tc_supported(int rows_per_input, int d_m) {
 
 void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B, int rows_per_input,
                          int n_stride, int d_m, float scale, void* ctx, cudaStream_t st, float2* stats,
-                         float* part) {
+                         float* part, bool h_static) {
     ELA_REQUIRE(el_decode_tc_supported(rows_per_input, d_m), ELATTN_ERR_UNSUPPORTED,
                 "tcgen05 decode: rows <= 512, d_m in {256, 512, 768, 1024}");
     ELA_REQUIRE((reinterpret_cast<uintptr_t>(qp) & 15) == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0 &&
@@ -1393,10 +1423,10 @@ void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, 
     }();
     (void)env_read;
     switch (d_m / 256) {
-        case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part);
-        case 2: return launch_units<2>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part);
-        case 3: return launch_units<3>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part);
-        default: return launch_units<4>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part);
+        case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static);
+        case 2: return launch_units<2>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static);
+        case 3: return launch_units<3>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static);
+        default: return launch_units<4>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static);
     }
 }
 

@@ -24,6 +24,8 @@ struct GemmArgs {
     int64_t sbz;
     int M, N, K, Z;
     float alpha;
+    int b_static = 0;  // 1: B (the weights) is never written by a kernel of the stream: the GEMM may
+                       // fetch it before its programmatic-dependent-launch wait
 };
 void launch_simt_gemm(int dtype, const GemmArgs& g, cudaStream_t st);
 
@@ -69,6 +71,8 @@ struct Tf32GemmArgs {
     int64_t sbz;
     int M, N, K, Z;
     float alpha;
+    int b_static = 0;  // 1: B (the weights) is never written by a kernel of the stream: the GEMM may
+                       // fetch it before its programmatic-dependent-launch wait
 };
 bool tf32_gemm_supported(const Tf32GemmArgs& g);
 void launch_tf32_gemm(const Tf32GemmArgs& g, cudaStream_t st);
@@ -119,6 +123,6 @@ bool el_decode_tc_supported(int rows_per_input, int d_m);
 size_t el_decode_tc_scratch_bytes(int d_m);
 void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B,
                          int rows_per_input, int n_stride, int d_m, float scale, void* ctx,
-                         cudaStream_t st, float2* stats, float* part);
+                         cudaStream_t st, float2* stats, float* part, bool h_static = false);
 
 }  // namespace elattn_gpu

@@ -89,6 +89,7 @@ struct GemmParams {
     int64_t ldc, sCz;
     unsigned long long* trace;  // testing: %globaltimer stamps of CTA 0 (null = off)
     uint64_t b_pol;             // L2 policy of the B (weight) loads
+    int b_pre;                  // stages of the first tile whose B slice is loaded before the PDL wait
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -160,9 +161,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // weights (B) are never written by the preceding kernels: the producer issues the first
+    // stages' B slices BEFORE the programmatic-dependent-launch wait, so their latency
+    // overlaps the previous kernel's tail (A, written by it, follows after the wait)
+    const int b_pre = (p.pdl && int(blockIdx.x) < num_tiles) ? p.b_pre : 0;
     if (p.pdl) {
         // prologue done (TMEM held): the next kernel may launch; wait for the previous one
         ptx::griddep_launch_dependents();
+        if (warp == 0 && b_pre > 0 && ptx::elect_one()) {
+            int z, m0, n0;
+            tile_coords(int(blockIdx.x), z, m0, n0);
+            for (int s = 0; s < b_pre; ++s) {
+                uint8_t* b = smem + s * S::kStageBytes + KBP * MT * S::kABytes;
+                ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
+                if (p.b_zm)
+                    ptx::tma_load_4d(b, &tmB, &full[s], 0, z, n0, s * KBP, p.b_pol);
+                else
+                    ptx::tma_load_4d(b, &tmB, &full[s], 0, n0, z, s * KBP, p.b_pol);
+            }
+        }
+        __syncwarp();
         ptx::griddep_wait();
     }
     if (tr && threadIdx.x == 0) p.trace[1] = gtimer();
@@ -180,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
                     uint8_t* a = smem + s * S::kStageBytes;
                     uint8_t* b = a + KBP * MT * S::kABytes;
-                    ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
+                    const bool pre = it < b_pre;  // B already in flight (issued before the PDL wait)
+                    if (!pre) ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
                     const int kb = ks * KBP;
                     if (tr && it < 4) p.trace[52 + it] = gtimer();
 #pragma unroll
@@ -191,10 +210,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else
                             ptx::tma_load_4d(dst, &tmA, &full[s], 0, m0 + mt * kBM, za, kb, ptx::kEvictNormal);
                     }
-                    if (p.b_zm)
-                        ptx::tma_load_4d(b, &tmB, &full[s], 0, z, n0, kb, p.b_pol);
-                    else
-                        ptx::tma_load_4d(b, &tmB, &full[s], 0, n0, z, kb, p.b_pol);
+                    if (!pre) {
+                        if (p.b_zm)
+                            ptx::tma_load_4d(b, &tmB, &full[s], 0, z, n0, kb, p.b_pol);
+                        else
+                            ptx::tma_load_4d(b, &tmB, &full[s], 0, n0, z, kb, p.b_pol);
+                    }
                 }
             }
         }
@@ -379,7 +400,7 @@ constexpr int kSkBN = 64;
 constexpr int kSkThreads = 192;
 
 struct SkParams {
-    int M, N, K, Z, tiles_m, tiles_n, kbp, a_zm, b_zm, a_bcast, pdl;
+    int M, N, K, Z, tiles_m, tiles_n, kbp, a_zm, b_zm, a_bcast, pdl, b_static;
     float alpha;
     const float* bias;
     int64_t sbz;
@@ -441,22 +462,33 @@ __global__ void __launch_bounds__(kSkThreads, 1)
     ptx::cluster_sync();  // barriers initialised before any peer st.async targets them
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const bool b_early = p.pdl && p.b_static;  // weights: fetched before the PDL wait
     if (p.pdl) {
         ptx::griddep_launch_dependents();
+        if (warp == 0 && b_early && ptx::elect_one()) {
+            ptx::mbar_arrive_expect_tx(full, uint32_t(p.kbp) * (S::kABytes + S::kBBytes));
+            if (p.b_zm)
+                ptx::tma_load_4d(sB, &tmB, full, 0, z, n0, kb0, ptx::kEvictLast);
+            else
+                ptx::tma_load_4d(sB, &tmB, full, 0, n0, z, kb0, ptx::kEvictLast);
+        }
+        __syncwarp();
         ptx::griddep_wait();
     }
     if (warp == 0) {
         if (ptx::elect_one()) {
-            ptx::mbar_arrive_expect_tx(full, uint32_t(p.kbp) * (S::kABytes + S::kBBytes));
+            if (!b_early) ptx::mbar_arrive_expect_tx(full, uint32_t(p.kbp) * (S::kABytes + S::kBBytes));
             const int za = p.a_bcast ? 0 : z;
             if (p.a_zm)
                 ptx::tma_load_4d(sA, &tmA, full, 0, za, m0, kb0, ptx::kEvictNormal);
             else
                 ptx::tma_load_4d(sA, &tmA, full, 0, m0, za, kb0, ptx::kEvictNormal);
-            if (p.b_zm)
-                ptx::tma_load_4d(sB, &tmB, full, 0, z, n0, kb0, ptx::kEvictLast);
-            else
-                ptx::tma_load_4d(sB, &tmB, full, 0, n0, z, kb0, ptx::kEvictLast);
+            if (!b_early) {
+                if (p.b_zm)
+                    ptx::tma_load_4d(sB, &tmB, full, 0, z, n0, kb0, ptx::kEvictLast);
+                else
+                    ptx::tma_load_4d(sB, &tmB, full, 0, n0, z, kb0, ptx::kEvictLast);
+            }
         }
         __syncwarp();
     } else if (warp == 1) {
@@ -619,6 +651,10 @@ void launch_cfg(const GemmArgs& g, cudaStream_t st) {
         return v == "normal" ? ptx::kEvictNormal : v == "first" ? ptx::kEvictFirst : ptx::kEvictLast;
     }();
     p.b_pol = w_pol;
+    {
+        const int num_ks = int(ceil_div(g.K / kBK, KBP));
+        p.b_pre = (g.b_static && p.pdl) ? (num_ks < S::kStages ? num_ks : S::kStages) : 0;
+    }
     CUtensorMap ta = load_map(g.A, g.lda, g.sAz, g.M, g.K, p.a_bcast ? 1 : g.Z, kBM, KBP, &p.a_zm);
     CUtensorMap tb = load_map(g.B, g.ldb, g.sBz, g.N, g.K, g.Z, BN, KBP, &p.b_zm);
     CUtensorMap tc = store_map(g.C, g.ldc, g.sCz, g.M, g.N, g.Z, kBM, S::kPiece, &p.c_zm);
@@ -709,6 +745,7 @@ void launch_splitk_cfg(const GemmArgs& g, cudaStream_t st) {
     p.kbp = g.K / kBK / SK;
     p.a_bcast = (g.Z > 1 && g.sAz == 0) ? 1 : 0;
     p.pdl = pdl_enabled() ? 1 : 0;
+    p.b_static = g.b_static;
     p.alpha = g.alpha, p.bias = g.bias, p.sbz = g.sbz;
     p.C = static_cast<__nv_bfloat16*>(g.C), p.ldc = g.ldc, p.sCz = g.sCz;
     CUtensorMap ta = load_map(g.A, g.lda, g.sAz, g.M, g.K, p.a_bcast ? 1 : g.Z, kBM, p.kbp, &p.a_zm);
