@@ -94,7 +94,27 @@ def test_mha_bf16_bart_batched_vs_reference(gpu):
     for b in range(B):
         want = O.multi_head_attention(pr, round_to_dtype(Y[b * x:(b + 1) * x], 1), round_to_dtype(H[b], 1), impl=IMPL)
         assert rel_err(mha[b * x:(b + 1) * x], want) <= 2e-2
+        # the EL path directly against the reference's MHA (north-star parity "and its MHA path")
+        assert rel_err(el[b * x:(b + 1) * x], want) <= 2e-2
     assert rel_err(el, mha) <= 2e-2
+
+
+def test_el_bf16_bart_full_context_vs_reference_mha(gpu):
+    """The bf16 EL step at the full BART-large shape (n = 1024, beam 4) against the
+    reference's own multi_head_attention (materialised per-head K/V, fp64, bf16-rounded
+    inputs) — the north star's second parity target."""
+    import torch
+
+    import paper_2105_04779_b200 as E
+    from paper_2105_04779_b200.attention import round_to_dtype
+
+    c = BART_CFG
+    B, n, x = 1, 1024, 4
+    p, Y, H = make_case(c["h"], c["d_m"], c["d_k"], n, B, x, 41, 42)
+    layer = E.ElAttentionLayer(to_prod(p), E.DTYPE_BF16)
+    el = layer.step(torch.from_numpy(Y).to("cuda", torch.bfloat16), torch.from_numpy(H).to("cuda", torch.bfloat16))
+    want = O.multi_head_attention(round_params(p, 1), round_to_dtype(Y, 1), round_to_dtype(H[0], 1), impl=IMPL)
+    assert rel_err(el.double().cpu().numpy(), want) <= 2e-2
 
 
 def test_mha_bf16_ragged_lengths(gpu):
