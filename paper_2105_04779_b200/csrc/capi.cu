@@ -212,6 +212,7 @@ void query_expansion(const elattn_gpu_params_s* p, const void* Y, int64_t R, voi
     b.A = Q, b.lda = hk, b.sAz = d_k;                         // head i: columns i*d_k..
     b.B = p->Wk, b.ldb = d_k, b.sBz = int64_t(d_m) * d_k;     // W_K,i [d_m][d_k] is K-major
     b.C = qp, b.ldc = int64_t(h) * d_m, b.sCz = d_m;          // row r*h + i
+    b.c_keep = 1;  // q' is read back by the decode while H streams through L2
     b.M = int(R), b.N = d_m, b.K = d_k, b.Z = h, b.alpha = 1.f;
     (void)e;
     gemm(p, b, st);

@@ -571,7 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         ptx::mbar_arrive_expect_tx(q_full, L::kQBytes);
                         for (int c = 0; c < 2 * L::kQSmemUnits; ++c)
                             ptx::tma_load_2d(sq + c * 8192, &tm_q, q_full, dm_off + 128 * L::kQTmemUnits + 64 * c,
-                                             vrow0(b, rows, sa.vchunks), ptx::kEvictNormal);
+                                             vrow0(b, rows, sa.vchunks), ptx::kEvictFirst);  // q' is dead after this load
                     }
                 }
                 G += T;

@@ -26,6 +26,7 @@ struct GemmArgs {
     float alpha;
     int b_static = 0;  // 1: B (the weights) is never written by a kernel of the stream: the GEMM may
                        // fetch it before its programmatic-dependent-launch wait
+    int c_keep = 0;    // 1: keep C in L2 (evict-last stores): the next kernel reads it back
 };
 void launch_simt_gemm(int dtype, const GemmArgs& g, cudaStream_t st);
 
@@ -73,6 +74,7 @@ struct Tf32GemmArgs {
     float alpha;
     int b_static = 0;  // 1: B (the weights) is never written by a kernel of the stream: the GEMM may
                        // fetch it before its programmatic-dependent-launch wait
+    int c_keep = 0;    // 1: keep C in L2 (evict-last stores): the next kernel reads it back
 };
 bool tf32_gemm_supported(const Tf32GemmArgs& g);
 void launch_tf32_gemm(const Tf32GemmArgs& g, cudaStream_t st);

@@ -90,6 +90,7 @@ struct GemmParams {
     unsigned long long* trace;  // testing: %globaltimer stamps of CTA 0 (null = off)
     uint64_t b_pol;             // L2 policy of the B (weight) loads
     int b_pre;                  // stages of the first tile whose B slice is loaded before the PDL wait
+    uint64_t c_pol;             // L2 policy of the TMA-store epilogue's output
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -362,9 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int nbase = n0 + int(grp) * kHalf + c0, r0 = m0 + mt * kBM;
                         if (nbase < p.N && r0 < p.M) {
                             if (p.c_zm)
-                                ptx::tma_store_3d(&tmC, stage, nbase, z, r0);
+                                ptx::tma_store_3d_hint(&tmC, stage, nbase, z, r0, p.c_pol);
                             else
-                                ptx::tma_store_3d(&tmC, stage, nbase, r0, z);
+                                ptx::tma_store_3d_hint(&tmC, stage, nbase, r0, z, p.c_pol);
                         }
                         ptx::bulk_commit_group();
                     }
@@ -651,6 +652,14 @@ void launch_cfg(const GemmArgs& g, cudaStream_t st) {
         return v == "normal" ? ptx::kEvictNormal : v == "first" ? ptx::kEvictFirst : ptx::kEvictLast;
     }();
     p.b_pol = w_pol;
+    // output: evict-last when the next kernel re-reads it while a large stream passes through
+    // L2 (the q' expansion, read by the decode while H streams evict-first)
+    static const uint64_t c_keep = [] {
+        const char* e = getenv("ELATTN_GEMM_C_POLICY");
+        const std::string v = e ? e : "";
+        return v == "normal" ? ptx::kEvictNormal : ptx::kEvictLast;
+    }();
+    p.c_pol = g.c_keep ? c_keep : ptx::kEvictNormal;
     {
         const int num_ks = int(ceil_div(g.K / kBK, KBP));
         p.b_pre = (g.b_static && p.pdl) ? (num_ks < S::kStages ? num_ks : S::kStages) : 0;
