@@ -527,7 +527,7 @@ def gpu_arm(args):
                        "global_batch": world * B, "beam": x, "n": n, "layers": L,
                        "parallelism": f"input-sharded x{world} (no collective in step)",
                        "l2": f"inputs larger than L2: H = {B * n * d_m * 2 / 1e6:.0f} MB per GPU",
-                       "decode_kernel": "tcgen05" if kind == 1 else "simt"},
+                       "decode_kernel": {1: "tcgen05", 2: "tcgen05 3xTF32"}.get(kind, "simt")},
             "clocks": clk,
             "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * x * d_m * 2,

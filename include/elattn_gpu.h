@@ -142,7 +142,9 @@ size_t elattn_gpu_workspace_size(elattn_gpu_params_t params, int B, int g, int n
 /*
  * Which decode kernel a (params, g) pair dispatches to:
  *   0 = SIMT (fp32 FFMA, or bf16 storage with fp32 FFMA),
- *   1 = tcgen05/TMEM/TMA fused decode (bf16, cluster of 2 CTAs per input).
+ *   1 = tcgen05/TMEM/TMA fused decode (bf16, cluster of 2 CTAs per input),
+ *   2 = 3xTF32 tcgen05 kind::tf32 (fp32 path: S = q'.H^T, softmax, P.H) for 16-byte aligned
+ *       buffers (unaligned fp32 buffers fall back to 0).
  */
 int elattn_gpu_decode_kernel_kind(elattn_gpu_params_t params, int g);
 

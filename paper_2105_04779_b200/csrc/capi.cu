@@ -481,6 +481,7 @@ size_t elattn_gpu_workspace_size(elattn_gpu_params_t p, int B, int g, int n) {
 
 int elattn_gpu_decode_kernel_kind(elattn_gpu_params_t p, int g) {
     if (!p || g < 1) return -1;
+    if (use_tf32_path(p)) return 2;
     return use_tc_decode(p, g * p->h) ? 1 : 0;
 }
 
