@@ -252,6 +252,33 @@ def test_decoder_step_graph_matches_layer_chain(gpu, npi_mode):
     assert rel_err(out, y) <= TOL[1]
 
 
+@pytest.mark.parametrize("B", [102, 148])
+def test_decoder_step_graph_schedules(gpu, B):
+    """The decoder step's graph (weights and H fetched before each kernel's PDL wait) is
+    bit-identical to the eager layer chain (no early fetches) under the tail-split (B = 102:
+    one full round + 28 inputs in 2 parts) and whole-input (B = 148: two full rounds)
+    decode schedules."""
+    import torch
+
+    E = gpu
+    c = BART_CFG
+    L, n = 2, 256
+    layers = [E.ElAttentionLayer(E.AttentionParams.random(c["h"], c["d_m"], c["d_k"], E.Rng(60 + l)), E.DTYPE_BF16)
+              for l in range(L)]
+    g = torch.Generator(device="cuda").manual_seed(B)
+    H = (torch.rand((B, n, c["d_m"]), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    dec = E.DecoderStep(layers, H, B, c["x"])
+    Y = (torch.rand((B * c["x"], c["d_m"]), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    got = dec.run(Y).clone()
+    again = dec.run(Y).clone()
+    torch.cuda.synchronize()
+    y = Y
+    for ly in layers:
+        y = ly.step(y, H)
+    torch.cuda.synchronize()
+    assert torch.equal(got, y) and torch.equal(again, y)
+
+
 @pytest.mark.parametrize("dtype", [0, 1])
 def test_hidden_state_cache_self_attention(gpu, dtype):
     """Decoder-only EL self-attention over per-lane hidden-state caches (config 4 form):
