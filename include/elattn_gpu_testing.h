@@ -34,6 +34,11 @@ int elattn_gpu_testing_gemm_config(int bn, int mt, int kbp);
  * automatic (default: used when the plain tile grid would fill less than half the SMs). */
 int elattn_gpu_testing_gemm_splitk(int sk);
 
+/* Fused small-batch query expansion (one launch: Q = Y.W_Q + b_Q reduced over a cluster of 4
+ * CTAs, then q' = Q_i.W_K,i^T): 0 disables it, 1 forces it where the shape allows (bf16,
+ * d_k = 64, up to 33 clusters of 4), -1 = automatic (up to 64 query rows). */
+int elattn_gpu_testing_qexp_fused(int mode);
+
 /* GEMM epilogue: 0 = coalesced st.global through a per-warp smem transpose, 1 = 128-row
  * TMA tensor stores, -1 = per shape (default: TMA stores for the write-bound q' expansion). */
 int elattn_gpu_testing_gemm_epilogue(int tma);

@@ -200,9 +200,14 @@ void gemm(const elattn_gpu_params_s* p, const GemmArgs& g_in, cudaStream_t st) {
 }
 
 // (1a) Q = Y.W_Q + b_Q ; (1b) q'_{r,i} = Q_{r,i}.W_K,i^T   (attention.hpp:205-206)
+// need_Q: the caller reads Q afterwards (key-bias scalars, mixed self-attention); otherwise a
+// small batch takes the fused one-launch expansion (Q stays on chip)
 void query_expansion(const elattn_gpu_params_s* p, const void* Y, int64_t R, void* Q, void* qp,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool need_Q = true) {
     const int h = p->h, d_m = p->d_m, d_k = p->d_k, hk = h * d_k;
+    if (!need_Q && p->dtype == ELATTN_DTYPE_BF16 && R < (int64_t(1) << 30) &&
+        tc_qexp_fused(Y, int(R), p->WqT, p->bq, p->Wk, qp, h, d_m, d_k, st))
+        return;
     GemmArgs a{};
     a.A = Y, a.lda = d_m, a.B = p->WqT, a.ldb = d_m, a.C = Q, a.ldc = hk, a.bias = p->bq;
     a.M = int(R), a.N = hk, a.K = d_m, a.Z = 1, a.alpha = 1.f;
@@ -519,7 +524,7 @@ int elattn_gpu_build_el_query(elattn_gpu_params_t p, const void* Y, int R, void*
         }
         Scratch scratch(ws, ws_bytes, align256(qbytes), st);
         void* Q = scratch.take(qbytes);
-        query_expansion(p, Y, R, Q, qprime, st);
+        query_expansion(p, Y, R, Q, qprime, st, /*need_Q=*/s != nullptr && p->include_key_bias);
         if (s) {
             if (p->include_key_bias)
                 launch_key_bias_scalars(p->dtype, Q, p->bk, R, p->h, p->d_k, s, st);
@@ -616,7 +621,7 @@ int elattn_gpu_el_attention_step(elattn_gpu_params_t p, const void* Y, const voi
         void* C = scratch.take(qpb);
         void* V = scratch.take(qb);
         float* part = static_cast<float*>(scratch.take(decode_scratch(p)));
-        query_expansion(p, Y, R, Q, qp, st);
+        query_expansion(p, Y, R, Q, qp, st, /*need_Q=*/false);
         decode(p, qp, H, n_per_input, B, x * p->h, n, C, part, st);
         output_projection(p, C, R, V, out, st);
     });
@@ -657,6 +662,11 @@ extern "C" int elattn_gpu_testing_decode_sched(int mode) {
         ELA_REQUIRE(mode >= 0 && mode <= 3, ELATTN_ERR_PARAM, "decode_sched: 0 auto, 1 stream-K, 2 whole, 3 tail");
         g_decode_sched_override = mode;
     });
+}
+
+extern "C" int elattn_gpu_testing_qexp_fused(int mode) {
+    g_qexp_fused = mode < 0 ? -1 : (mode ? 1 : 0);  // 1: forced (the tests sweep it up to 256 rows)
+    return ELATTN_OK;
 }
 
 extern "C" int elattn_gpu_testing_gemm_splitk(int sk) {
@@ -793,7 +803,7 @@ void decoder_enqueue(elattn_gpu_decoder_s* d, const void* H, const int* npi, con
     for (int l = 0; l < L; ++l) {
         void* dst = (l == L - 1) ? out : d->ybuf[l & 1];
         const elattn_gpu_params_s* p = d->layers[l];
-        query_expansion(p, y, R, Q, qp, d->st);
+        query_expansion(p, y, R, Q, qp, d->st, /*need_Q=*/false);
         decode(p, qp, H, npi, d->B, d->x * p->h, d->n, C, part, d->st, nullptr, /*h_static=*/true);
         output_projection(p, C, R, V, dst, d->st);
         y = dst;

@@ -46,10 +46,15 @@ void launch_el_decode_simt(int dtype, const void* qp, const void* H, const int* 
 // contract as launch_simt_gemm but requires K % 64 == 0, 16-byte aligned rows and
 // N % 16 == 0.  tc_gemm_supported returns false outside that envelope.
 bool tc_gemm_supported(const GemmArgs& g);
+// Fused small-batch query expansion q' = (Y.W_Q + b_Q)_i . W_K,i^T (bf16; one launch, cluster
+// of 4 CTAs per 128-row tile and head); returns false when the shape is outside its envelope.
+bool tc_qexp_fused(const void* Y, int M, const void* WqT, const float* bq, const void* Wk, void* qp, int h, int d_m,
+                   int d_k, cudaStream_t st);
 void launch_tc_gemm(const GemmArgs& g, cudaStream_t st);
 
 // Testing / tuning override of the tcgen05 GEMM block shape (0 = automatic choice).
 extern int g_decode_sched_override;
+extern int g_qexp_fused;
 extern int g_gemm_force_bn, g_gemm_force_mt, g_gemm_force_kbp, g_gemm_force_splitk;
 extern unsigned long long* g_gemm_trace;
 extern int g_gemm_epilogue_tma;

@@ -35,6 +35,7 @@ namespace elattn_gpu {
 
 int g_gemm_force_bn = 0, g_gemm_force_mt = 0, g_gemm_force_kbp = 0;  // testing / tuning override (0 = auto)
 int g_gemm_force_splitk = -1;  // testing / tuning override of the small-M split-K (-1 = auto, 0 = off)
+int g_qexp_fused = -1;         // testing / tuning: fused small-batch query expansion (-1 = auto, 0 = off)
 unsigned long long* g_gemm_trace = nullptr;                            // testing: timeline of CTA 0
 int g_gemm_epilogue_tma = -1;                                          // testing / tuning: 1 TMA stores, 0 st.global, -1 auto
 
@@ -576,6 +577,268 @@ __global__ void __launch_bounds__(kSkThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------- fused query expansion (small M)
+// q'_{r,i} = (y_r . W_Q,i + b_Q,i) . W_K,i^T for a small batch in ONE launch (replaces the Q
+// GEMM + the head-batched q' GEMM, both latency-bound at a few hundred rows).  A cluster of
+// 4 CTAs per (128-row tile, head i):
+//   1. CTA r multiplies its quarter of K = d_m: partial Q_i (128 x 64 fp32, TMEM);
+//   2. reduce-scatter over DSMEM (CTA r sums columns [16 r, 16 r + 16) of the four partials
+//      in rank order — deterministic — and adds b_Q), then ALL-GATHER of the bf16 slices into
+//      every CTA's smem as the SW128 K-major A operand Q_i (128 x 64);
+//   3. CTA r expands its quarter of d_m: q'[rows][256 r .. 256 r + 256) = Q_i . W_K,i^T, two
+//      128-column chunks (M128 N128 K64), stored straight to the q' rows r*h + i.
+// Q is rounded to bf16 before step 3, as the two-kernel path stores it.
+constexpr int kQxSK = 4;
+constexpr int kQxThreads = 192;
+struct QxSmem {
+    static constexpr int kW = 64 / kQxSK;                      // Q columns reduced per CTA
+    static constexpr uint32_t kABytes = kBM * kBK * 2;         // Y: 128 rows x 64 k
+    static constexpr uint32_t kBBytes = 64 * kBK * 2;          // W_Q slice: 64 rows x 64 k
+    static constexpr int kMaxKbp = 4;                          // d_m <= 1024
+    static constexpr uint32_t kBOff = kMaxKbp * kABytes;
+    static constexpr uint32_t kRecvOff = kBOff + kMaxKbp * kBBytes;
+    static constexpr uint32_t kRecvBytes = uint32_t(kQxSK - 1) * kBM * kW * 4;
+    static constexpr uint32_t kQOff = kRecvOff + kRecvBytes;   // Q_i bf16, 128 x 64, SW128 K-major
+    static constexpr uint32_t kWkOff = kQOff + kBM * 64 * 2;   // W_K chunks: 2 x (128 rows x 64 k)
+    static constexpr uint32_t kBarOff = kWkOff + 2 * 128 * 64 * 2;
+    static constexpr uint32_t kTotal = kBarOff + 128 + 1024;
+    static_assert(kTotal <= 232448, "fused query expansion shared memory");
+};
+struct QxParams {
+    int M, d_m, h, kbp, chunks, pdl;  // chunks: 128-column q' chunks per CTA (d_m / 4 / 128)
+    const float* bq;
+    __nv_bfloat16* qp;                 // [M * h][d_m]
+};
+
+__global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
+    tc_qexp_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmWq,
+                   const __grid_constant__ CUtensorMap tmWk, QxParams p) {
+    using S = QxSmem;
+    constexpr int kW = S::kW;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + S::kBOff;
+    float* recv = reinterpret_cast<float*>(smem + S::kRecvOff);
+    uint8_t* sQ = smem + S::kQOff;
+    uint8_t* sWk = smem + S::kWkOff;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOff);
+    uint64_t* acc_full = full + 1;
+    uint64_t* recv_full = full + 2;
+    uint64_t* wk_full = full + 3;   // [2]
+    uint64_t* p_full = full + 5;    // [2]
+    uint64_t* p_empty = full + 7;   // [2] (epilogue -> MMA: q' chunk accumulator read)
+    uint64_t* wk_empty = full + 9;  // [2] (MMA -> TMA: W_K chunk buffer consumed)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 11);
+    const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+    const int rank = int(ptx::cluster_ctarank());
+    const int t = int(blockIdx.x) / kQxSK;
+    const int z = t % p.h, m0 = (t / p.h) * kBM;  // head fastest: concurrent clusters share Y rows in L2
+    const int kb0 = rank * p.kbp;
+    const int col0 = rank * (p.d_m / kQxSK);     // this CTA's q' columns
+
+    if (warp == 0) {
+        if (ptx::elect_one()) {
+            ptx::prefetch_tmap(&tmY);
+            ptx::prefetch_tmap(&tmWq);
+            ptx::prefetch_tmap(&tmWk);
+            ptx::mbar_init(full, 1);
+            ptx::mbar_init(acc_full, 1);
+            ptx::mbar_init(recv_full, 1);
+            for (int i = 0; i < 2; ++i) {
+                ptx::mbar_init(&wk_full[i], 1);
+                ptx::mbar_init(&p_full[i], 1);
+                ptx::mbar_init(&p_empty[i], 4);
+                ptx::mbar_init(&wk_empty[i], 1);
+            }
+            ptx::fence_mbar_init();
+            ptx::mbar_arrive_expect_tx(recv_full, S::kRecvBytes);
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        ptx::tmem_alloc<512>(tmem_slot);
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tq = tmem, tp = tmem + 128;  // Q partial: 64 columns; q' chunks: 2 x 128 columns
+    if (p.pdl) {
+        ptx::griddep_launch_dependents();
+        // the weights do not depend on the preceding kernels: issue them before the wait
+        if (warp == 0 && ptx::elect_one()) {
+            ptx::mbar_arrive_expect_tx(full, uint32_t(p.kbp) * (S::kABytes + S::kBBytes));
+            ptx::tma_load_4d(sB, &tmWq, full, 0, z * 64, 0, kb0, ptx::kEvictLast);
+            for (int c = 0; c < 2 && c < p.chunks; ++c) {
+                ptx::mbar_arrive_expect_tx(&wk_full[c], 128 * 64 * 2);
+                ptx::tma_load_3d(sWk + c * 128 * 64 * 2, &tmWk, &wk_full[c], 0, col0 + c * 128, z, ptx::kEvictLast);
+            }
+        }
+        __syncwarp();
+        ptx::griddep_wait();
+    }
+    if (warp == 0) {
+        if (ptx::elect_one()) {
+            if (!p.pdl) {
+                ptx::mbar_arrive_expect_tx(full, uint32_t(p.kbp) * (S::kABytes + S::kBBytes));
+                ptx::tma_load_4d(sB, &tmWq, full, 0, z * 64, 0, kb0, ptx::kEvictLast);
+            }
+            ptx::tma_load_4d(sA, &tmY, full, 0, m0, 0, kb0, ptx::kEvictNormal);
+            for (int c = (p.pdl ? 2 : 0); c < 2 && c < p.chunks; ++c) {
+                ptx::mbar_arrive_expect_tx(&wk_full[c], 128 * 64 * 2);
+                ptx::tma_load_3d(sWk + c * 128 * 64 * 2, &tmWk, &wk_full[c], 0, col0 + c * 128, z, ptx::kEvictLast);
+            }
+        }
+        __syncwarp();
+        ptx::cluster_sync();  // (matches the all-gather barrier of the other warps; before any wait
+                              // on phase-2 progress, which needs that barrier)
+        if (ptx::elect_one()) {
+            for (int c = 2; c < p.chunks; ++c) {
+                const int bi = c & 1;
+                ptx::mbar_wait(&wk_empty[bi], ((c >> 1) - 1) & 1);
+                ptx::mbar_arrive_expect_tx(&wk_full[bi], 128 * 64 * 2);
+                ptx::tma_load_3d(sWk + bi * 128 * 64 * 2, &tmWk, &wk_full[bi], 0, col0 + c * 128, z, ptx::kEvictLast);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // phase 1: partial Q_i over this CTA's k-blocks
+        constexpr uint32_t idq = ptx::idesc_bf16(kBM, 64, 0, 0);
+        ptx::mbar_wait(full, 0);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+            const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA), 0, 1024);
+            const uint64_t b0 = ptx::sdesc_sw128(ptx::smem_u32(sB), 0, 1024);
+            for (int j = 0; j < p.kbp; ++j)
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                    ptx::mma_bf16(tq, a0 + uint64_t((j * S::kABytes) >> 4) + uint64_t(2 * k),
+                                  b0 + uint64_t((j * S::kBBytes) >> 4) + uint64_t(2 * k), idq, (j | k) != 0);
+            ptx::mma_commit(acc_full);
+        }
+        __syncwarp();
+        ptx::cluster_sync();  // Q_i gathered into every CTA's sQ (written by the epilogue warps)
+        ptx::tc_fence_after();
+        // phase 2: q' chunks, A = Q_i (smem), B = W_K,i rows of the chunk
+        constexpr uint32_t idp = ptx::idesc_bf16(kBM, 128, 0, 0);
+        const uint64_t aq = ptx::sdesc_sw128(ptx::smem_u32(sQ), 0, 1024);
+        const uint64_t bw = ptx::sdesc_sw128(ptx::smem_u32(sWk), 0, 1024);
+        for (int c = 0; c < p.chunks; ++c) {
+            const int bi = c & 1;
+            ptx::mbar_wait(&wk_full[bi], (c >> 1) & 1);
+            if (c >= 2) ptx::mbar_wait(&p_empty[bi], ((c >> 1) - 1) & 1);
+            ptx::tc_fence_after();
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    ptx::mma_bf16(tp + bi * 128, aq + uint64_t(2 * k),
+                                  bw + uint64_t((bi * 128 * 64 * 2) >> 4) + uint64_t(2 * k), idp, k != 0);
+                ptx::mma_commit(&wk_empty[bi]);
+                ptx::mma_commit(&p_full[bi]);
+            }
+            __syncwarp();
+        }
+    } else {
+        // epilogue warps: lane quadrant qd, row = 32 qd + lane of the 128-row tile
+        const uint32_t qd = warp & 3;
+        const int row = int(qd) * 32 + int(lane), m = m0 + row;
+        float bcol[kW];
+#pragma unroll
+        for (int j = 0; j < kW; ++j) bcol[j] = __ldg(p.bq + z * 64 + rank * kW + j);
+        ptx::mbar_wait(acc_full, 0);
+        ptx::tc_fence_after();
+        uint32_t v[64];
+        ptx::tmem_ld32(tq + ((qd * 32) << 16), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        ptx::tmem_ld32(tq + ((qd * 32) << 16) + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        ptx::tmem_ld_wait();
+        // reduce-scatter: columns [kW pr, kW pr + kW) of this row to CTA pr
+#pragma unroll
+        for (int pr = 0; pr < kQxSK; ++pr) {
+            if (pr == rank) continue;
+            const int slot = rank - (rank > pr ? 1 : 0);
+            const uint32_t dst = ptx::mapa(ptx::smem_u32(recv + (slot * kBM + row) * kW), uint32_t(pr));
+            const uint32_t bar = ptx::mapa(ptx::smem_u32(recv_full), uint32_t(pr));
+#pragma unroll
+            for (int j = 0; j < kW; j += 4)
+                ptx::st_async_v4(dst + 4 * j, __uint_as_float(v[pr * kW + j]), __uint_as_float(v[pr * kW + j + 1]),
+                                 __uint_as_float(v[pr * kW + j + 2]), __uint_as_float(v[pr * kW + j + 3]), bar);
+        }
+        ptx::mbar_wait(recv_full, 0);
+        float acc[kW];
+#pragma unroll
+        for (int j = 0; j < kW; ++j) acc[j] = 0.f;
+#pragma unroll
+        for (int sr = 0; sr < kQxSK; ++sr) {  // rank order: deterministic
+            if (sr == rank) {
+#pragma unroll
+                for (int j = 0; j < kW; ++j) acc[j] += __uint_as_float(v[rank * kW + j]);
+            } else {
+                const float* src = recv + ((sr - (sr > rank ? 1 : 0)) * kBM + row) * kW;
+#pragma unroll
+                for (int j = 0; j < kW; ++j) acc[j] += src[j];
+            }
+        }
+        // all-gather: this row's kW bf16 values of Q_i into every CTA's sQ (SW128 K-major:
+        // 16-byte chunk c of row r at r * 128 + ((c ^ (r & 7)) << 4)); kW = 16 -> two chunks
+        uint4 o[kW / 8];
+#pragma unroll
+        for (int c = 0; c < kW / 8; ++c) {
+            o[c].x = pack2(acc[8 * c + 0] + bcol[8 * c + 0], acc[8 * c + 1] + bcol[8 * c + 1]);
+            o[c].y = pack2(acc[8 * c + 2] + bcol[8 * c + 2], acc[8 * c + 3] + bcol[8 * c + 3]);
+            o[c].z = pack2(acc[8 * c + 4] + bcol[8 * c + 4], acc[8 * c + 5] + bcol[8 * c + 5]);
+            o[c].w = pack2(acc[8 * c + 6] + bcol[8 * c + 6], acc[8 * c + 7] + bcol[8 * c + 7]);
+        }
+#pragma unroll
+        for (int pr = 0; pr < kQxSK; ++pr)
+#pragma unroll
+            for (int c = 0; c < kW / 8; ++c) {
+                const int chunk = rank * (kW / 8) + c;
+                const uint32_t off = uint32_t(row) * 128u + (uint32_t(chunk ^ (row & 7)) << 4);
+                ptx::st_cluster_v4(ptx::mapa(ptx::smem_u32(sQ) + off, uint32_t(pr)), o[c]);
+            }
+        ptx::fence_proxy_async_cluster();
+        ptx::cluster_sync();
+        // phase-2 epilogue: q' chunks -> bf16 -> rows (m0 + row) * h + z
+        __nv_bfloat16* dst_row = p.qp + (int64_t(m) * p.h + z) * p.d_m + col0;
+        for (int c = 0; c < p.chunks; ++c) {
+            const int bi = c & 1;
+            ptx::mbar_wait(&p_full[bi], (c >> 1) & 1);
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t r[64];
+                ptx::tmem_ld32(tp + bi * 128 + half * 64 + ((qd * 32) << 16), *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+                ptx::tmem_ld32(tp + bi * 128 + half * 64 + 32 + ((qd * 32) << 16),
+                               *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+                ptx::tmem_ld_wait();
+                if (half == 1) {
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&p_empty[bi]);
+                }
+                if (m < p.M) {
+                    uint4* d = reinterpret_cast<uint4*>(dst_row + c * 128 + half * 64);
+#pragma unroll
+                    for (int q8 = 0; q8 < 8; ++q8) {
+                        uint4 w;
+                        w.x = pack2(__uint_as_float(r[8 * q8 + 0]), __uint_as_float(r[8 * q8 + 1]));
+                        w.y = pack2(__uint_as_float(r[8 * q8 + 2]), __uint_as_float(r[8 * q8 + 3]));
+                        w.z = pack2(__uint_as_float(r[8 * q8 + 4]), __uint_as_float(r[8 * q8 + 5]));
+                        w.w = pack2(__uint_as_float(r[8 * q8 + 6]), __uint_as_float(r[8 * q8 + 7]));
+                        d[q8] = w;
+                    }
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
 // Maps over an operand X[z][r][k] (r = M or N rows, k contiguous).  Loads use 4-D maps
 // (64 k, r | z, z | r, k-block) whose k-block dimension has stride 128 B, so one box
 // carries `kbp` k-blocks of `box_rows` rows as [kb][row][64] — KBP SWIZZLE_128B K-major
@@ -775,7 +1038,47 @@ void launch_splitk(const GemmArgs& g, cudaStream_t st) {
     return launch_splitk_cfg<SK, false, false>(g, st);
 }
 
+// fused query expansion for small batches (see tc_qexp_kernel); false = not applicable
+bool launch_qexp_fused(const void* Y, int M, const void* WqT, const float* bq, const void* Wk, void* qp, int h,
+                       int d_m, int d_k, cudaStream_t st) {
+    static const int env = [] {
+        const char* e = getenv("ELATTN_QEXP_FUSED");
+        return e ? atoi(e) : -1;
+    }();
+    if (env == 0 || g_qexp_fused == 0) return false;
+    const int items = int(ceil_div(M, kBM)) * h;
+    const int max_clusters = (num_sms() * 33) / 148;  // co-resident clusters of 4 (B200)
+    if (d_k != 64 || d_m % (128 * kQxSK) != 0 || d_m / kBK / kQxSK > QxSmem::kMaxKbp || items > max_clusters)
+        return false;
+    // measured faster than the two GEMMs only up to 64 rows (tools/probes/qexp_time.py: 8.4 vs
+    // 9.2-9.8 us at B <= 16, beam 4; 9.6 vs 9.4 at 128 rows): automatic use below that
+    if (g_qexp_fused < 0 && env < 0 && M > 64) return false;
+    if (!aligned16(Y) || !aligned16(WqT) || !aligned16(Wk) || !aligned16(qp)) return false;
+    QxParams p{};
+    p.M = M, p.d_m = d_m, p.h = h, p.kbp = d_m / kBK / kQxSK, p.chunks = d_m / kQxSK / 128;
+    p.pdl = pdl_enabled() ? 1 : 0;
+    p.bq = bq;
+    p.qp = static_cast<__nv_bfloat16*>(qp);
+    int zr = 0;
+    // Y [M][d_m]: 4-D map (64 k, rows, 1, k-block); W_Q^T [h*64][d_m] likewise; W_K [h][d_m][64]: 3-D (k, d, head)
+    CUtensorMap ty = load_map(Y, d_m, 0, M, d_m, 1, kBM, p.kbp, &zr);
+    CUtensorMap twq = load_map(WqT, d_m, 0, h * 64, d_m, 1, 64, p.kbp, &zr);
+    const uint64_t kd[3] = {uint64_t(d_k), uint64_t(d_m), uint64_t(h)};
+    const uint64_t ks[2] = {uint64_t(d_k) * 2, uint64_t(d_m) * d_k * 2};
+    const uint32_t kbox[3] = {64, 128, 1};
+    CUtensorMap twk = make_tmap_bf16(Wk, 3, kd, ks, kbox, 128);
+    ELA_CHECK_CUDA(cudaFuncSetAttribute(tc_qexp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(QxSmem::kTotal)));
+    launch_ex(tc_qexp_kernel, dim3(items * kQxSK), dim3(kQxThreads), QxSmem::kTotal, st, 1, ty, twq, twk, p);
+    ELA_CHECK_LAUNCH();
+    return true;
+}
+
 }  // namespace
+
+bool tc_qexp_fused(const void* Y, int M, const void* WqT, const float* bq, const void* Wk, void* qp, int h, int d_m,
+                   int d_k, cudaStream_t st) {
+    return launch_qexp_fused(Y, M, WqT, bq, Wk, qp, h, d_m, d_k, st);
+}
 
 bool tc_gemm_supported(const GemmArgs& g) {
     return g.K % kBK == 0 && g.K > 0 && g.N % 16 == 0 && g.M > 0 && g.lda % 8 == 0 && g.ldb % 8 == 0 &&

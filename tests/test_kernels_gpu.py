@@ -449,3 +449,40 @@ def test_decode_ragged_schedules(B, rows, d_m):
     assert torch.equal(outs[3], outs[4])
     for o in outs[2:]:
         assert (outs[0] - o).abs().max().item() / want.abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("R,d_m,h", [(128, 1024, 16), (256, 1024, 16), (77, 1024, 16), (200, 512, 8), (4, 1024, 16)])
+def test_fused_query_expansion(R, d_m, h):
+    """The fused small-batch query expansion (one launch: Q_i reduced over a cluster of 4
+    CTAs through DSMEM, all-gathered as bf16, then q' = Q_i.W_K,i^T) against torch fp32 of
+    (bf16(Y.W_Q + b_Q))_i.W_K,i^T, against the two-GEMM path, and run-to-run identical."""
+    import torch
+
+    import paper_2105_04779_b200 as E
+    from paper_2105_04779_b200 import capi
+
+    L = capi.lib()
+    L.elattn_gpu_testing_qexp_fused.argtypes = [ctypes.c_int]
+    d_k = 64
+    p = E.AttentionParams.random(h, d_m, d_k, E.Rng(R + d_m))
+    layer = E.ElAttentionLayer(p, E.DTYPE_BF16)
+    g = torch.Generator(device="cuda").manual_seed(R)
+    Y = (torch.rand((R, d_m), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    outs = []
+    try:
+        for mode in (1, 1, 0):
+            capi.check(L.elattn_gpu_testing_qexp_fused(mode))
+            outs.append(layer.build_el_query(Y).float())
+            torch.cuda.synchronize()
+    finally:
+        capi.check(L.elattn_gpu_testing_qexp_fused(-1))
+    Wq = torch.from_numpy(np.asarray(p.Wq)).cuda().to(torch.bfloat16).float()   # [h][d_m][d_k]
+    Wk = torch.from_numpy(np.asarray(p.Wk)).cuda().to(torch.bfloat16).float()
+    bq = torch.from_numpy(np.asarray(p.bq)).cuda().float().view(h, d_k)
+    Q = (torch.einsum("rd,hdk->rhk", Y.float(), Wq) + bq[None]).to(torch.bfloat16).float()
+    want = torch.einsum("rhk,hdk->rhd", Q, Wk).reshape(R * h, d_m)
+    scale = want.abs().max().item()
+    for o in outs:
+        assert (o - want).abs().max().item() / scale < 1e-2
+    assert torch.equal(outs[0], outs[1])
+    assert (outs[0] - outs[2]).abs().max().item() / scale < 1e-2
