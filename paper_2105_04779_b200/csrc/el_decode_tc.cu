@@ -325,7 +325,9 @@ __device__ __forceinline__ RaggedPos ragged_locate(const int* npi, int B, int n_
     return r;
 }
 
-template <int UNITS, bool TRACE, bool MASK>
+// R16: instantiation for inputs of at most 16 query rows (one beam x 16 heads) — the epilogue
+// moves a quarter of the O tile; the general instantiation keeps its register budget.
+template <int UNITS, bool TRACE, bool MASK, bool R16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     el_decode_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_h,
                         const __grid_constant__ CUtensorMap tm_c,
@@ -995,6 +997,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 if (warp == 2 && lane == 0) ELA_TRACE(28, li * 4 + m);
             };
+            // the same for inputs with at most 16 query rows (one beam x 16 heads: greedy
+            // decoding, decoder-only lanes): a quarter of the TMEM loads, transposes and stores
+            auto emit_unit16 = [&](int m, const uint32_t(&lo)[8], const uint32_t(&hi)[8], const float(&sc)[16]) {
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    uint32_t f[4];
+                    const uint32_t* src[2] = {lo, hi};
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            const uint32_t* r = src[h2] + 4 * k + 2 * half;
+                            f[2 * h2 + half] = pack_bf16x2(__uint_as_float(r[0]) * sc[2 * k],
+                                                           __uint_as_float(r[1]) * sc[2 * k + 1]);
+                        }
+                    const uint32_t q = 8u * k + stm_i;
+                    ptx::stmatrix_x4_trans(stm_base + k * 512 + ((stm_j ^ ((q >> 1) & 3u)) << 4), f[0], f[1], f[2],
+                                           f[3]);
+                }
+                __syncwarp();
+                __nv_bfloat16* dst = ctx + int64_t(vrow0(b, rows, sa.vchunks)) * d_m + dm_off + m * 128 + int(qd) * 32;
+                const int nr = vnrows(b, rows, sa.vchunks);
+#pragma unroll
+                for (int s8 = 0; s8 < 2; ++s8) {
+                    const int q = s8 * 8 + int(lane >> 2), j = int(lane & 3);
+                    const uint4 v = ptx::lds_u4(ptx::smem_u32(my_stage) + q * 64 + ((j ^ ((q >> 1) & 3)) << 4));
+                    if (q < nr && !(TRACE && tune.skip_c_store))
+                        *reinterpret_cast<uint4*>(dst + int64_t(q) * d_m + 8 * j) = v;
+                }
+            };
             if (kind < 0) {
                 // whole input: normalise by 1/l and write
                 if ((lane & 3) == 0) {
@@ -1018,6 +1051,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (warp == 2 && lane == 0) ELA_TRACE(19, li);
                 // unit by unit: TMEM -> registers -> bf16 stage -> st.global (the stores do
                 // not block, so no software pipelining is needed to hide them)
+                if constexpr (R16) {
+#pragma unroll 1
+                    for (int m = 0; m < UNITS; ++m) {
+                        uint32_t lo[8], hi[8];
+                        ptx::tmem_ld_16x256b_x2(t_lane + m * 64, lo);
+                        ptx::tmem_ld_16x256b_x2(t_lane + (16u << 16) + m * 64, hi);
+                        ptx::tmem_ld_wait();
+                        if (m == UNITS - 1) {  // O read out: the next segment may overwrite it
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(o_free);
+                        }
+                        emit_unit16(m, lo, hi, inv_l);
+                    }
+                } else
 #pragma unroll 1
                 for (int m = 0; m < UNITS; ++m) {
                     uint32_t lo[32], hi[32];
@@ -1280,7 +1328,9 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     // instrumented instantiation (trace hook, lookahead knobs) only when asked for
     const bool instr = g_decode_trace != nullptr || g_tuning.s_ahead != 4 || g_tuning.l2_ahead != 0;
     const bool mask = npi != nullptr || n_stride % kNT != 0;
+    const bool r16 = rows <= 16 && !instr;  // one beam x <= 16 heads (vchunks == 1)
     auto kern = instr ? (mask ? el_decode_tc_kernel<UNITS, true, true> : el_decode_tc_kernel<UNITS, true, false>)
+                : r16 ? (mask ? el_decode_tc_kernel<UNITS, false, true, true> : el_decode_tc_kernel<UNITS, false, false, true>)
                       : (mask ? el_decode_tc_kernel<UNITS, false, true> : el_decode_tc_kernel<UNITS, false, false>);
     constexpr uint32_t smem = DecLayout<UNITS>::kTotal;
     ELA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
