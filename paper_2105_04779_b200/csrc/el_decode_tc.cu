@@ -1388,7 +1388,11 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     // full rounds stay whole inputs (no records, no extra transitions)
     const int T_all = (n_stride + kNT - 1) / kNT;
     const int P_tail = last_round > 0 ? std::min(kMaxSegs, std::min(max_cl / last_round, T_all)) : 0;
-    const bool tail_split = stream_k && B >= max_cl && sched_mode != 1 && P_tail >= 2 &&
+    // (also with no full round, B < #clusters: every input in P parts, one segment per
+    // cluster — no pipeline transitions, unlike stream-K chunks that straddle inputs)
+    // (parts of >= 10 tiles there: shorter parts cost more in records and merging than the
+    // transitions they avoid; tools/time_small_batch.py: B = 24 / 32 -6% / -4%, B = 8 +5%)
+    const bool tail_split = stream_k && sched_mode != 1 && P_tail >= 2 && (B >= max_cl || T_all >= 10 * P_tail) &&
                             (sched_mode == 3 || 4 * last_round * P_tail >= 3 * max_cl);
     if (ragged_lpt) {
         sa.T = -2;
