@@ -77,9 +77,6 @@ struct Tf32GemmArgs {
     int64_t sbz;
     int M, N, K, Z;
     float alpha;
-    int b_static = 0;  // 1: B (the weights) is never written by a kernel of the stream: the GEMM may
-                       // fetch it before its programmatic-dependent-launch wait
-    int c_keep = 0;    // 1: keep C in L2 (evict-last stores): the next kernel reads it back
 };
 bool tf32_gemm_supported(const Tf32GemmArgs& g);
 void launch_tf32_gemm(const Tf32GemmArgs& g, cudaStream_t st);
