@@ -381,6 +381,33 @@ def test_mixed_self_attention_batched_vs_oracle(gpu, dtype):
             assert rel_err(out[r:r + 1], want) <= TOL[dtype], (step, r)
 
 
+def test_mixed_self_attention_split_prefixes_vs_oracle(gpu):
+    """The decode's softmax statistics {m, l} when inputs are split across clusters: 24 inputs
+    with full 1024-row prefixes run as 3 parts each (tail-split with no full round), merged by
+    the merge kernel, which also emits the statistics the mixed combine consumes."""
+    import torch
+
+    E = gpu
+    c = dict(BART_CFG)
+    B, x, n = 24, c["x"], 1024
+    p = O.params_random(c["h"], c["d_m"], c["d_k"], O.OracleRng(511))
+    layer = E.ElAttentionLayer(to_prod(p), E.DTYPE_BF16)
+    from paper_2105_04779_b200.attention import round_to_dtype
+
+    g = torch.Generator(device="cuda").manual_seed(512)
+    Pd = (torch.rand((B, n, c["d_m"]), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    Yd = (torch.rand((B * x, c["d_m"]), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    cache = E.KvCache(layer, B * x, 2)
+    cache.append(Yd)
+    out = E.mixed_self_attention_batched(layer, Yd, Pd, cache, x, None).double().cpu().numpy()
+    pr = round_params(p, E.DTYPE_BF16)
+    Y = Yd.double().cpu().numpy()
+    for r in (0, 5, 47, 95):
+        b = r // x
+        want = O.mixed_self_attention(pr, Y[r:r + 1], Pd[b].double().cpu().numpy(), Y[r:r + 1])
+        assert rel_err(out[r:r + 1], want) <= TOL[1], r
+
+
 @pytest.mark.parametrize("h,d_m", [(4, 256), (12, 768)])
 def test_bf16_step_other_model_widths(gpu, h, d_m):
     """d_m = 256 / 768 (UNITS = 1 / 3 of the tcgen05 decode), beam 4 and greedy."""
