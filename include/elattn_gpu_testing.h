@@ -69,9 +69,16 @@ int elattn_gpu_testing_decode_bf16(const void* qprime, const void* H, const int*
  * automatic choice is ragged stream-K up to 8 inputs per cluster. */
 int elattn_gpu_testing_decode_sched(int mode);
 
-/* Device buffer (>= 2*24*64 u64) that receives clock64 stamps from the first
- * cluster of every following tcgen05 decode launch; NULL disables tracing. */
+/* Device buffer (>= 2*32*64 + 2*grid u64, e.g. 8192) that receives clock64 stamps from
+ * the first cluster of every following tcgen05 decode launch (events x 64 tiles per CTA),
+ * then %globaltimer at entry and exit of every CTA; NULL disables tracing. */
 int elattn_gpu_testing_set_decode_trace(unsigned long long* trace);
+
+/* Measurement builds only (make EXTRA=-DELA_TIMELINE): every CTA of the projection GEMM,
+ * fused query-expansion, decode and merge kernels launched afterwards appends a 32-byte
+ * record {entry, after-PDL-wait, exit (%globaltimer ns), kind, block} at records[*count++]
+ * (up to capacity; NULL records disables).  ELATTN_ERR_UNSUPPORTED in production builds. */
+int elattn_gpu_testing_timeline(void* records, unsigned* count, unsigned capacity);
 
 #ifdef __cplusplus
 }

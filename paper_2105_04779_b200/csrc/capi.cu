@@ -718,6 +718,12 @@ extern "C" int elattn_gpu_testing_gemm_tf32x3(const float* A, int64_t lda, int64
     });
 }
 
+extern "C" int elattn_gpu_testing_timeline(void* records, unsigned* count, unsigned capacity) {
+    const bool ok = tl_set_gemm(static_cast<TlRec*>(records), count, capacity) &
+                    tl_set_decode(static_cast<TlRec*>(records), count, capacity);
+    return ok ? ELATTN_OK : ELATTN_ERR_UNSUPPORTED;
+}
+
 extern "C" int elattn_gpu_testing_set_decode_trace(unsigned long long* trace) {
     g_decode_trace = trace;
     return ELATTN_OK;

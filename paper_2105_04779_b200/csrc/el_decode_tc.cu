@@ -43,6 +43,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx_sm100.cuh"
+#include "timeline.cuh"
 #include "tmap.h"
 
 #include <algorithm>
@@ -385,6 +386,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int dm_half = d_m / 2, dm_off = int(rank) * dm_half;
     const int total_rows = (B / sa.vchunks) * rows;  // B counts virtual inputs, rows real rows per input
 
+    ELA_TL_DECL;
+    if (threadIdx.x == 0) ELA_TRACE(29, 0);  // kernel entry
+    if constexpr (TRACE)  // every CTA: %globaltimer at entry and exit (after the 2 x 32 x 64 event block)
+        if (trace != nullptr && threadIdx.x == 0) trace[4096 + 2 * blockIdx.x] = ptx::globaltimer();
     if (warp == 0) {
         if (ptx::elect_one()) {
             ptx::prefetch_tmap(&tm_q);
@@ -455,7 +460,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
         ptx::griddep_wait();
+        ELA_TL_WAIT();
     }
+    if (threadIdx.x == 0) ELA_TRACE(30, 0);  // setup done (after the PDL wait)
     if (MASK && sa.T == -2) {  // ragged longest-first: this cluster's inputs (n_per_input is read after the
                        // PDL wait: a preceding kernel may have written it)
         if (warp == 0) {
@@ -1138,7 +1145,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) ELA_TRACE(31, 0);  // all roles done
+    if constexpr (TRACE)
+        if (trace != nullptr && threadIdx.x == 0) trace[4096 + 2 * blockIdx.x + 1] = ptx::globaltimer();
     ptx::cluster_sync();
+    ELA_TL_EXIT(kTlDecode);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<kTmemCols>(tmem);
@@ -1172,7 +1183,12 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
                                                               float2* __restrict__ stats, int Bw,
                                                               const int* __restrict__ npi, int B, int n_stride) {
     constexpr int kPF = kPartFloatsHdr + UNITS * kPartFloatsUnit;
+    ELA_TL_DECL;
+    // the next kernel (the V projection) may launch now and stage its weights; it waits for
+    // this grid's completion before reading C
+    ptx::griddep_launch_dependents();
     ptx::griddep_wait();  // launched with PDL after the decode: its records must be complete
+    ELA_TL_WAIT();
     const int rank = int(blockIdx.y), m = int(blockIdx.z);
     int b, c_first, nseg;
     int64_t first_tile = 0;  // b's first tile in the cut (stream-K): decides each segment's record slot
@@ -1215,24 +1231,35 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
         c_first = int(first_tile / W);
         nseg = min(kMaxSegs, int((int64_t(b) * T + T - 1) / W) - c_first + 1);
     }
-    __shared__ const float* s_rec[kMaxSegs];
     __shared__ float s_w[kMaxSegs][64];
     __shared__ float s_inv[64];
     __shared__ __align__(16) __nv_bfloat16 tile[64][128 + 8];
     const int tid = int(threadIdx.x);
-    if (tid < nseg) {
-        const int c2 = c_first + tid;
-        const int kd = (W < 0 || int64_t(c2) * W >= first_tile) ? 0 : 1;  // b's segment is c2's first?
-        s_rec[tid] = part + (int64_t(2 * c2 + kd) * 2 + rank) * kPF;
-    }
-    __syncthreads();
+    auto rec_of = [&](int s) {  // record of segment s (cluster c_first + s; slot 0 unless b is its 2nd)
+        const int c2 = c_first + s;
+        const int kd = (W < 0 || int64_t(c2) * W >= first_tile) ? 0 : 1;
+        return part + (int64_t(2 * c2 + kd) * 2 + rank) * kPF;
+    };
+    // fragment float4 e = (h * 8 + i4) * 128 + t of the unit; this thread takes e = tid + 256 j.
+    // The fragments of the first kPre segments do not depend on the weights: all of their
+    // loads are issued before phase 1, so the merge costs ~one L2 round trip, not nseg + 1
+    constexpr int kPer = 2 * 8 * 128 / 256, kPre = 4;
+    uint2 vp[kPre][kPer];
+#pragma unroll
+    for (int s = 0; s < kPre; ++s)
+        if (s < nseg) {
+            const uint2* body = reinterpret_cast<const uint2*>(rec_of(s) + kPartFloatsHdr + m * kPartFloatsUnit);
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) vp[s][j] = __ldcg(body + tid + 256 * j);
+        }
     if (tid < 64) {
         float ms[kMaxSegs], ls[kMaxSegs], M = -INFINITY, L = 0.f;
 #pragma unroll
         for (int s = 0; s < kMaxSegs; ++s)
             if (s < nseg) {
-                ms[s] = __ldcg(s_rec[s] + tid);
-                ls[s] = __ldcg(s_rec[s] + 64 + tid);
+                const float* r = rec_of(s);
+                ms[s] = __ldcg(r + tid);
+                ls[s] = __ldcg(r + 64 + tid);
                 M = fmaxf(M, ms[s]);
             }
 #pragma unroll
@@ -1247,16 +1274,10 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
             stats[vrow0(b, rows, vchunks) + tid] = make_float2(M * scale_log2, L);
     }
     __syncthreads();
-    // fragment float4 e = (h * 8 + i4) * 128 + t of the unit; this thread takes e = tid + 256 j
-    constexpr int kPer = 2 * 8 * 128 / 256;
     float4 acc[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < nseg; ++s) {
-        const uint2* body = reinterpret_cast<const uint2*>(s_rec[s] + kPartFloatsHdr + m * kPartFloatsUnit);
-        uint2 v[kPer];
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) v[j] = __ldcg(body + tid + 256 * j);
+    auto accumulate = [&](int s, const uint2 (&v)[kPer]) {
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
             const int e = tid + 256 * j, t = e & 127, i4 = (e >> 7) & 7;
@@ -1266,6 +1287,16 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
             const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[j].y));
             acc[j].x += a.x * w0, acc[j].y += a.y * w1, acc[j].z += c.x * w0, acc[j].w += c.y * w1;
         }
+    };
+#pragma unroll
+    for (int s = 0; s < kPre; ++s)
+        if (s < nseg) accumulate(s, vp[s]);
+    for (int s = kPre; s < nseg; ++s) {
+        const uint2* body = reinterpret_cast<const uint2*>(rec_of(s) + kPartFloatsHdr + m * kPartFloatsUnit);
+        uint2 v[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) v[j] = __ldcg(body + tid + 256 * j);
+        accumulate(s, v);
     }
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
@@ -1285,9 +1316,12 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
         *reinterpret_cast<uint4*>(ctx + (int64_t(r0) + q) * d_m + dm_off + 8 * v) =
             *reinterpret_cast<const uint4*>(&tile[q][8 * v]);
     }
+    ELA_TL_EXIT(kTlMerge);
 }
 
 }  // namespace
+
+ELA_TL_SETTER(tl_set_decode)
 
 size_t el_decode_tc_scratch_bytes(int d_m) {
     // partial records of split inputs: 2 slots per cluster x 2 CTA ranks, at most one

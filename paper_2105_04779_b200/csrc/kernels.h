@@ -119,6 +119,11 @@ void launch_cache_gather(const void* src, const int* src_len, void* dst, int* ds
 // Testing hook: when non-null, the tcgen05 decode writes clock64 stamps of its
 // first cluster: trace[(cta*24 + event)*64 + tile].
 extern unsigned long long* g_decode_trace;
+// measurement builds (-DELA_TIMELINE, timeline.cuh): per-CTA step timeline buffers of the
+// GEMM and decode translation units (false when the build has no timeline)
+struct TlRec;
+bool tl_set_gemm(TlRec* buf, unsigned* cnt, unsigned cap);
+bool tl_set_decode(TlRec* buf, unsigned* cnt, unsigned cap);
 
 // tcgen05/TMA fused EL decode for bf16 (cluster of 2 CTAs per input, split d_m).
 bool el_decode_tc_supported(int rows_per_input, int d_m);

@@ -33,6 +33,11 @@ __device__ __forceinline__ bool elect_one() {
 
 __device__ __forceinline__ uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x / 32, 0); }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x % 32; }
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // 2^x on the SFU (MUFU.EX2, flush-to-zero); inputs are max-subtracted scores <= 0.
 __device__ __forceinline__ float ex2(float x) {

@@ -29,6 +29,7 @@
 #include <string>
 #include "kernels.h"
 #include "ptx_sm100.cuh"
+#include "timeline.cuh"
 #include "tmap.h"
 
 namespace elattn_gpu {
@@ -111,6 +112,7 @@ template <int BN, int MT, int KBP, bool BIAS, bool SCALE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmParams p) {
+    ELA_TL_DECL;
     using S = GemmSmem<BN, MT, KBP>;
     constexpr int kStages = S::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         ptx::griddep_wait();
+        ELA_TL_WAIT();
     }
     if (tr && threadIdx.x == 0) p.trace[1] = gtimer();
 
@@ -381,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
+    ELA_TL_EXIT(kTlGemm);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<S::kTmemCols>(tmem);
@@ -427,6 +431,7 @@ template <int SK, bool BIAS, bool SCALE>
 __global__ void __launch_bounds__(kSkThreads, 1)
     tc_gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           SkParams p) {
+    ELA_TL_DECL;
     using S = SkSmem<SK>;
     constexpr int kW = S::kW;
     extern __shared__ uint8_t smem_raw[];
@@ -476,6 +481,7 @@ __global__ void __launch_bounds__(kSkThreads, 1)
         }
         __syncwarp();
         ptx::griddep_wait();
+        ELA_TL_WAIT();
     }
     if (warp == 0) {
         if (ptx::elect_one()) {
@@ -571,6 +577,7 @@ __global__ void __launch_bounds__(kSkThreads, 1)
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();  // no CTA leaves while its partial columns are still in flight to a peer
+    ELA_TL_EXIT(kTlSplitK);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<64>(tmem);
@@ -613,6 +620,7 @@ struct QxParams {
 __global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
     tc_qexp_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmWq,
                    const __grid_constant__ CUtensorMap tmWk, QxParams p) {
+    ELA_TL_DECL;
     using S = QxSmem;
     constexpr int kW = S::kW;
     extern __shared__ uint8_t smem_raw[];
@@ -676,6 +684,7 @@ __global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
         }
         __syncwarp();
         ptx::griddep_wait();
+        ELA_TL_WAIT();
     }
     if (warp == 0) {
         if (ptx::elect_one()) {
@@ -833,6 +842,7 @@ __global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();
+    ELA_TL_EXIT(kTlQexp);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512>(tmem);
@@ -1113,5 +1123,7 @@ void launch_tc_gemm(const GemmArgs& g, cudaStream_t st) {
                                                      " MT " + std::to_string(c.mt) + " KBP " + std::to_string(c.kbp)};
     }
 }
+
+ELA_TL_SETTER(tl_set_gemm)
 
 }  // namespace elattn_gpu

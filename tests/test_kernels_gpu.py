@@ -312,7 +312,7 @@ def test_decode_instrumented_instantiation_matches():
     qp = (torch.randn(B * rows, d_m, generator=g, device="cuda") * 0.3).to(torch.bfloat16)
     H = (torch.rand(B, n, d_m, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
     st = torch.cuda.current_stream().cuda_stream
-    tr = torch.zeros(2 * 32 * 64, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(2 * 32 * 64 + 4096, dtype=torch.int64, device="cuda")
     outs = []
     for trace in (None, tr):
         L.elattn_gpu_testing_set_decode_trace(trace.data_ptr() if trace is not None else None)

@@ -19,7 +19,10 @@ ap.add_argument("--no-cublas", action="store_true")
 ap.add_argument("--sweep", action="store_true", help="time every block-shape instantiation")
 ap.add_argument("--tma-epilogue", action="store_true")
 ap.add_argument("--kernel", type=int, default=1, help="1: tcgen05 with stream-K scratch, 2: data-parallel only")
+ap.add_argument("--lib", default=None, help="library build to load (A/B runs)")
 a = ap.parse_args()
+if a.lib:
+    capi.LIB_PATH = Path(a.lib).resolve()
 L = capi.lib()
 vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
 L.elattn_gpu_testing_gemm_bf16.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, i64, vp, i64,

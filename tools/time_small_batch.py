@@ -17,11 +17,15 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch  # noqa: E402
 
 import paper_2105_04779_b200 as E  # noqa: E402
+from paper_2105_04779_b200 import capi  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--B", type=int, nargs="+", default=[16, 32, 48, 64])
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--lib", default=None, help="library build to load (A/B runs)")
 a = ap.parse_args()
+if a.lib:
+    capi.LIB_PATH = Path(a.lib).resolve()
 L, x, n, d_m = 12, 4, 1024, 1024
 layers = [E.ElAttentionLayer(E.AttentionParams.random(16, d_m, 64, E.Rng(1 + l)), E.DTYPE_BF16) for l in range(L)]
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")

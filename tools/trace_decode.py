@@ -24,7 +24,7 @@ B, rows, n, d_m = a.B, 64, a.n, 1024
 qp = (torch.randn(B * rows, d_m, device="cuda") * 0.3).to(torch.bfloat16)
 H = (torch.rand(B, n, d_m, device="cuda") * 2 - 1).to(torch.bfloat16)
 ctx = torch.empty_like(qp)
-tr = torch.zeros(2 * 32 * 64, dtype=torch.int64, device="cuda")
+tr = torch.zeros(2 * 32 * 64 + 4096, dtype=torch.int64, device="cuda")
 st = torch.cuda.current_stream().cuda_stream
 for i in range(3):
     L.elattn_gpu_testing_set_decode_trace(tr.data_ptr() if i == 2 else None)

@@ -44,7 +44,7 @@ for B in a.B:
     qp = (torch.randn(B * rows, d_m, device="cuda") * 0.3).to(torch.bfloat16)
     H = (torch.rand(B, n, d_m, device="cuda") * 2 - 1).to(torch.bfloat16)
     ctx = torch.empty_like(qp)
-    tr = torch.zeros(2 * NEV * NT, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(2 * NEV * NT + 4096, dtype=torch.int64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
     for i in range(3):
         L.elattn_gpu_testing_set_decode_trace(tr.data_ptr() if i == 2 else None)
@@ -52,7 +52,7 @@ for B in a.B:
                                                     ctx.data_ptr(), 1, st))
     L.elattn_gpu_testing_set_decode_trace(None)
     torch.cuda.synchronize()
-    t = tr.view(2, NEV, NT).cpu().numpy().astype(np.int64)
+    t = tr[:2 * NEV * NT].view(2, NEV, NT).cpu().numpy().astype(np.int64)
     print(f"B={B} n={n} rows={rows} d_m={d_m}  (cycles, median over steady-state tiles 4..{NT - 2})")
     for cta in range(2):
         g = np.arange(4, NT - 1)
