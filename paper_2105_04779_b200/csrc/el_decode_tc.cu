@@ -949,6 +949,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
                 if (warp == 2 && lane == 0) ELA_TRACE(13, Gt);
+                if (warp == 2 && lane == 0) {
+                    if (Gt == 0) ELA_TL_MARK(0);  // first P posted
+                    ELA_TL_MARK(1);               // (last) P posted
+                }
             }
 
             // ---- epilogue: C[b*rows + q][dm_off + d] = O^T[d][q] / l_q.
@@ -1130,6 +1134,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // of the next input
             softmax_bar_sync();
             if (warp == 2 && lane == 0) ELA_TRACE(15, li);
+            if (warp == 2 && lane == 0) ELA_TL_MARK(2);  // (last) epilogue done
             G += T;
             ++li;
         }

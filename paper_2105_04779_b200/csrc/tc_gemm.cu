@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ks = 0; ks < num_ks; ++ks, ++it) {
                 const int s = it % kStages;
                 ptx::mbar_wait(&full[s], (it / kStages) & 1);
+                if (it == 0 && lane == 0) ELA_TL_MARK(0);  // first stage landed
                 ptx::tc_fence_after();
                 if (tr && lane == 0 && it < 32) p.trace[2 + it] = gtimer();
                 if (lane == 0) {
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::mbar_wait(&acc_full[ab], (local >> 1) & 1);
+            if (warp == 2 && lane == 0) ELA_TL_MARK(1);  // (last) accumulator ready
             ptx::tc_fence_after();
             if (tr && warp == 2 && lane == 0 && local < 8) p.trace[34 + 2 * local] = gtimer();
 #pragma unroll 1
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (leader) ptx::bulk_wait_group_read<0>();
         __syncwarp();
         if (tr && warp == 2 && lane == 0) p.trace[50] = gtimer();
+        if (warp == 2 && lane == 0) ELA_TL_MARK(2);  // epilogue done
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -502,6 +505,7 @@ __global__ void __launch_bounds__(kSkThreads, 1)
     } else if (warp == 1) {
         constexpr uint32_t idesc = ptx::idesc_bf16(kBM, kSkBN, 0, 0);
         ptx::mbar_wait(full, 0);
+        if (lane == 0) ELA_TL_MARK(0);  // operands landed
         ptx::tc_fence_after();
         if (lane == 0) {
             const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA), 0, 1024);
@@ -524,18 +528,19 @@ __global__ void __launch_bounds__(kSkThreads, 1)
             bcol[j] = (BIAS && n < p.N) ? __ldg(p.bias + z * p.sbz + n) : 0.f;
         }
         ptx::mbar_wait(acc_full, 0);
+        if (warp == 2 && lane == 0) ELA_TL_MARK(1);  // accumulator ready
         ptx::tc_fence_after();
         uint32_t v[64];
         ptx::tmem_ld32(tmem + ((qd * 32) << 16), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
         ptx::tmem_ld32(tmem + ((qd * 32) << 16) + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
         ptx::tmem_ld_wait();
-        if (SK > 1) {
-            // send column slice p of this row to CTA p (slot = this CTA's index among p's sources)
+        if constexpr (SK == 2) {
+            // one peer: this row's other 32-column half goes straight from registers (st.async;
+            // the loop keeps the register indices compile-time)
 #pragma unroll
             for (int pr = 0; pr < SK; ++pr) {
                 if (pr == rank) continue;
-                const int slot = rank - (rank > pr ? 1 : 0);
-                const uint32_t dst = ptx::mapa(ptx::smem_u32(recv + (slot * kBM + row) * kW), uint32_t(pr));
+                const uint32_t dst = ptx::mapa(ptx::smem_u32(recv + row * kW), uint32_t(pr));
                 const uint32_t bar = ptx::mapa(ptx::smem_u32(recv_full), uint32_t(pr));
 #pragma unroll
                 for (int j = 0; j < kW; j += 4)
@@ -543,6 +548,36 @@ __global__ void __launch_bounds__(kSkThreads, 1)
                                      __uint_as_float(v[pr * kW + j + 2]), __uint_as_float(v[pr * kW + j + 3]), bar);
             }
             ptx::mbar_wait(recv_full, 0);
+            if (warp == 2 && lane == 0) ELA_TL_MARK(2);  // peer's partial columns received
+        } else if constexpr (SK > 2) {
+            // column slice p of the partial goes to CTA p (slot = this CTA's index among p's
+            // sources): staged as [p][128 rows][kW] in the A operand region (the MMAs that read
+            // it have completed), then ONE bulk shared::cta -> shared::cluster copy per peer
+            // (per-row st.async of 16 bytes made this exchange ~0.5 us slower at SK = 4)
+            float* send = reinterpret_cast<float*>(sA);
+#pragma unroll
+            for (int pr = 0; pr < SK; ++pr) {
+                if (pr == rank) continue;
+#pragma unroll
+                for (int j = 0; j < kW; j += 4)
+                    *reinterpret_cast<float4*>(send + (pr * kBM + row) * kW + j) =
+                        make_float4(__uint_as_float(v[pr * kW + j]), __uint_as_float(v[pr * kW + j + 1]),
+                                    __uint_as_float(v[pr * kW + j + 2]), __uint_as_float(v[pr * kW + j + 3]));
+            }
+            ptx::fence_proxy_async_smem();
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps staged their rows
+            if (warp == 2 && lane == 0) {
+#pragma unroll
+                for (int pr = 0; pr < SK; ++pr) {
+                    if (pr == rank) continue;
+                    const int slot = rank - (rank > pr ? 1 : 0);
+                    ptx::bulk_s2s_cluster(ptx::mapa(ptx::smem_u32(recv + slot * kBM * kW), uint32_t(pr)),
+                                          ptx::smem_u32(send + pr * kBM * kW), uint32_t(kBM * kW * 4),
+                                          ptx::mapa(ptx::smem_u32(recv_full), uint32_t(pr)));
+                }
+            }
+            ptx::mbar_wait(recv_full, 0);
+            if (warp == 2 && lane == 0) ELA_TL_MARK(2);  // peers' partial columns received
         }
         float acc[kW];
 #pragma unroll
@@ -574,6 +609,7 @@ __global__ void __launch_bounds__(kSkThreads, 1)
                 *reinterpret_cast<uint4*>(dst + j) = o;
             }
         }
+        if (warp == 2 && lane == 0) ELA_TL_MARK(3);  // stores issued
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();  // no CTA leaves while its partial columns are still in flight to a peer

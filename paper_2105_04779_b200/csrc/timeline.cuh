@@ -13,7 +13,7 @@
 namespace elattn_gpu {
 
 struct TlRec {
-    unsigned long long entry, wait, exit;
+    unsigned long long entry, wait, exit, mark[4];  // mark: kernel-specific phase ends (0 = unset)
     unsigned kind, block;
 };
 enum TlKind : unsigned { kTlGemm = 1, kTlSplitK = 2, kTlQexp = 3, kTlDecode = 4, kTlMerge = 5 };
@@ -24,14 +24,20 @@ __device__ TlRec* tl_buf_;
 __device__ unsigned* tl_cnt_;
 __device__ unsigned tl_cap_;
 }  // namespace
-#define ELA_TL_DECL unsigned long long tl_entry_ = ::elattn_gpu::ptx::globaltimer(), tl_wait_ = tl_entry_
+#define ELA_TL_DECL                                                                 \
+    unsigned long long tl_entry_ = ::elattn_gpu::ptx::globaltimer(), tl_wait_ = tl_entry_; \
+    __shared__ unsigned long long tl_mark_[4];                                      \
+    if (threadIdx.x < 4) tl_mark_[threadIdx.x] = 0
 #define ELA_TL_WAIT() (tl_wait_ = ::elattn_gpu::ptx::globaltimer())
+// any thread; read by thread 0 at exit (after the kernel's final CTA barrier)
+#define ELA_TL_MARK(i) (tl_mark_[i] = ::elattn_gpu::ptx::globaltimer())
 #define ELA_TL_EXIT(kind)                                                                             \
     do {                                                                                              \
         if (threadIdx.x == 0 && tl_buf_ != nullptr) {                                                 \
             const unsigned i_ = atomicAdd(tl_cnt_, 1u);                                               \
             if (i_ < tl_cap_)                                                                         \
                 tl_buf_[i_] = ::elattn_gpu::TlRec{tl_entry_, tl_wait_, ::elattn_gpu::ptx::globaltimer(), \
+                                                  {tl_mark_[0], tl_mark_[1], tl_mark_[2], tl_mark_[3]}, \
                                                   unsigned(kind),                                     \
                                                   blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)}; \
         }                                                                                             \
@@ -45,6 +51,7 @@ __device__ unsigned tl_cap_;
 #else
 #define ELA_TL_DECL
 #define ELA_TL_WAIT() ((void)0)
+#define ELA_TL_MARK(i) ((void)0)
 #define ELA_TL_EXIT(kind) ((void)0)
 #define ELA_TL_SETTER(name) \
     bool name(TlRec*, unsigned*, unsigned) { return false; }

@@ -31,6 +31,7 @@ ap.add_argument("--layers", type=int, default=12)
 ap.add_argument("--lib", default=str(ROOT / "paper_2105_04779_b200/csrc/build_tl/libtl.so"))
 ap.add_argument("--show", type=int, default=12, help="launches to print (the rest summarised)")
 ap.add_argument("--json", default=None)
+ap.add_argument("--dump", type=int, nargs="*", default=[], help="launch indices to print per CTA")
 a = ap.parse_args()
 capi.LIB_PATH = Path(a.lib).resolve()
 import paper_2105_04779_b200 as E  # noqa: E402
@@ -48,7 +49,7 @@ for B in a.B:
     H = (torch.rand((B, a.n, 1024), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
     dec = E.DecoderStep(layers, H, B, a.x)
     dec.Y.copy_((torch.rand((B * a.x, 1024), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
-    rec = torch.zeros(CAP * 4, dtype=torch.int64, device="cuda")
+    rec = torch.zeros(CAP * 8, dtype=torch.int64, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
     for _ in range(3):
         dec.run(stream=st)
@@ -61,10 +62,11 @@ for B in a.B:
     torch.cuda.synchronize()
     capi.check(L.elattn_gpu_testing_timeline(None, None, 0))
     n = min(int(cnt.item()), CAP)
-    r = rec[: n * 4].view(n, 4).cpu().numpy()
+    r = rec[: n * 8].view(n, 8).cpu().numpy()
     entry, wait, exit_ = r[:, 0].astype(np.int64), r[:, 1].astype(np.int64), r[:, 2].astype(np.int64)
-    kind = (r[:, 3] & 0xFFFFFFFF).astype(np.int64)
-    block = (r[:, 3] >> 32).astype(np.int64)
+    marks = r[:, 3:7].astype(np.int64)
+    kind = (r[:, 7] & 0xFFFFFFFF).astype(np.int64)
+    block = (r[:, 7] >> 32).astype(np.int64)
     t0 = entry.min()
     order = np.argsort(entry, kind="stable")
     launches = []  # per kind: the current launch (block ids seen)
@@ -86,16 +88,26 @@ for B in a.B:
         row = {"kind": KIND.get(c["kind"], c["kind"]), "ctas": len(ii), "entry0": en.min(), "entry1": en.max(),
                "wait_med": float(np.median(wa)), "wait1": wa.max(), "exit0": ex.min(), "exit_med": float(np.median(ex)),
                "exit1": ex.max(), "gap": None if prev_end is None else wa.min() - prev_end,
-               "busy_med": float(np.median(ex - wa))}
+               "busy_med": float(np.median(ex - wa)),
+               # kernel phase ends (timeline.cuh ELA_TL_MARK), median over CTAs, from the wait release
+               "marks": [None if not (marks[ii, k] > 0).any() else
+                         float(np.median((marks[ii, k][marks[ii, k] > 0] - wait[ii][marks[ii, k] > 0]) / 1e3))
+                         for k in range(4)]}
         prev_end = ex.max()
+        if len(rows) in a.dump:
+            print(f"  launch {len(rows)} ({row['kind']}) per CTA (block: entry wait marks... exit, us):")
+            for i in ii[np.argsort(block[ii])]:
+                mk = " ".join("-" if marks[i, k] == 0 else f"{(marks[i, k] - t0) / 1e3:7.2f}" for k in range(4))
+                print(f"    {block[i]:4d}: {(entry[i] - t0) / 1e3:7.2f} {(wait[i] - t0) / 1e3:7.2f} {mk} {(exit_[i] - t0) / 1e3:7.2f}")
         rows.append(row)
     step_us = e0.elapsed_time(e1) * 1e3
     print(f"B={B}: step {step_us:.1f} us (event), {len(rows)} launches, last exit {rows[-1]['exit1']:.1f} us")
-    print("   kind    ctas  entry0  entry1  wait_med  exit0  exit_med  exit1   gap  busy_med")
+    print("   kind    ctas  entry0  entry1  wait_med  exit0  exit_med  exit1   gap  busy_med  marks(from wait)")
     for row in rows[: a.show]:
         print(f"  {row['kind']:7s} {row['ctas']:5d} {row['entry0']:7.2f} {row['entry1']:7.2f} {row['wait_med']:8.2f} "
               f"{row['exit0']:6.2f} {row['exit_med']:8.2f} {row['exit1']:6.2f} "
-              f"{'' if row['gap'] is None else format(row['gap'], '6.2f'):>6s} {row['busy_med']:8.2f}")
+              f"{'' if row['gap'] is None else format(row['gap'], '6.2f'):>6s} {row['busy_med']:8.2f}  "
+              + " ".join("-" if m is None else f"{m:.2f}" for m in row["marks"]))
     # per kind: duration from the predecessor's end to this launch's end (its share of the step)
     share = {}
     for i, row in enumerate(rows):
