@@ -796,17 +796,29 @@ __global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
         ptx::tmem_ld32(tq + ((qd * 32) << 16), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
         ptx::tmem_ld32(tq + ((qd * 32) << 16) + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
         ptx::tmem_ld_wait();
-        // reduce-scatter: columns [kW pr, kW pr + kW) of this row to CTA pr
+        // reduce-scatter: columns [kW pr, kW pr + kW) of the partial to CTA pr, staged as
+        // [pr][128 rows][kW] in the drained Y buffer and sent with one bulk copy per peer
+        float* send = reinterpret_cast<float*>(sA);
 #pragma unroll
         for (int pr = 0; pr < kQxSK; ++pr) {
             if (pr == rank) continue;
-            const int slot = rank - (rank > pr ? 1 : 0);
-            const uint32_t dst = ptx::mapa(ptx::smem_u32(recv + (slot * kBM + row) * kW), uint32_t(pr));
-            const uint32_t bar = ptx::mapa(ptx::smem_u32(recv_full), uint32_t(pr));
 #pragma unroll
             for (int j = 0; j < kW; j += 4)
-                ptx::st_async_v4(dst + 4 * j, __uint_as_float(v[pr * kW + j]), __uint_as_float(v[pr * kW + j + 1]),
-                                 __uint_as_float(v[pr * kW + j + 2]), __uint_as_float(v[pr * kW + j + 3]), bar);
+                *reinterpret_cast<float4*>(send + (pr * kBM + row) * kW + j) =
+                    make_float4(__uint_as_float(v[pr * kW + j]), __uint_as_float(v[pr * kW + j + 1]),
+                                __uint_as_float(v[pr * kW + j + 2]), __uint_as_float(v[pr * kW + j + 3]));
+        }
+        ptx::fence_proxy_async_smem();
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps staged their rows
+        if (warp == 2 && lane == 0) {
+#pragma unroll
+            for (int pr = 0; pr < kQxSK; ++pr) {
+                if (pr == rank) continue;
+                const int slot = rank - (rank > pr ? 1 : 0);
+                ptx::bulk_s2s_cluster(ptx::mapa(ptx::smem_u32(recv + slot * kBM * kW), uint32_t(pr)),
+                                      ptx::smem_u32(send + pr * kBM * kW), uint32_t(kBM * kW * 4),
+                                      ptx::mapa(ptx::smem_u32(recv_full), uint32_t(pr)));
+            }
         }
         ptx::mbar_wait(recv_full, 0);
         float acc[kW];
