@@ -622,73 +622,74 @@ __global__ void __launch_bounds__(kSkThreads, 1)
 
 // ---------------------------------------------------------------- fused query expansion (small M)
 // q'_{r,i} = (y_r . W_Q,i + b_Q,i) . W_K,i^T for a small batch in ONE launch (replaces the Q
-// GEMM + the head-batched q' GEMM, both latency-bound at a few hundred rows).  A cluster of
-// 4 CTAs per (128-row tile, head i):
-//   1. CTA r multiplies its quarter of K = d_m: partial Q_i (128 x 64 fp32, TMEM);
-//   2. reduce-scatter over DSMEM (CTA r sums columns [16 r, 16 r + 16) of the four partials
-//      in rank order — deterministic — and adds b_Q), then ALL-GATHER of the bf16 slices into
-//      every CTA's smem as the SW128 K-major A operand Q_i (128 x 64);
-//   3. CTA r expands its quarter of d_m: q'[rows][256 r .. 256 r + 256) = Q_i . W_K,i^T, two
-//      128-column chunks (M128 N128 K64), stored straight to the q' rows r*h + i.
-// Q is rounded to bf16 before step 3, as the two-kernel path stores it.
-constexpr int kQxSK = 4;
-constexpr int kQxThreads = 192;
+// GEMM + the head-batched q' GEMM, both latency-bound at a few hundred rows).  CTA
+// (128-row tile, head i, quarter u):
+//   1. the whole Q_i tile (128 x 64, K = d_m) on the tensor cores, Y and W_Q,i streamed in
+//      3 stages of 2 k-blocks (the W_Q,i stages are issued before the PDL wait);
+//   2. Q_i + b_Q,i -> bf16 -> this CTA's shared memory as the SW128 K-major A operand;
+//   3. the CTA's quarter of d_m: q'[rows][d_m u / 4 ..) = Q_i . W_K,i^T in 128-column chunks
+//      (M128 N128 K64), stored straight to the q' rows r*h + i.
+// The four quarters recompute Q_i (the Y tile and W_Q,i are L2 hits) instead of splitting K
+// over a cluster: the DSMEM reduce-scatter + all-gather that version needed cost ~4 us of
+// latency, more than the recomputation (a CTA-pair variant that multicast each stage's two
+// k-blocks, halving the L2 requests, measured slower: the single-k-block boxes).  Q is
+// rounded to bf16 before step 3 and accumulated over K in one chain, as the two-kernel path
+// does, so the result is bit-identical to it.  Standalone (graph replay, beam 4): 7.0 us at
+// B <= 16 vs 9.1 for the two GEMMs; 8.3 vs 8.5 at B = 32, where the two-GEMM path is still
+// ahead inside the decoder step (the split-K Q GEMM spreads the 256 KB Y tile over 4 CTAs)
+constexpr int kQxThreads = 192, kQxKbp = 2, kQxStages = 3;
 struct QxSmem {
-    static constexpr int kW = 64 / kQxSK;                      // Q columns reduced per CTA
-    static constexpr uint32_t kABytes = kBM * kBK * 2;         // Y: 128 rows x 64 k
-    static constexpr uint32_t kBBytes = 64 * kBK * 2;          // W_Q slice: 64 rows x 64 k
-    static constexpr int kMaxKbp = 4;                          // d_m <= 1024
-    static constexpr uint32_t kBOff = kMaxKbp * kABytes;
-    static constexpr uint32_t kRecvOff = kBOff + kMaxKbp * kBBytes;
-    static constexpr uint32_t kRecvBytes = uint32_t(kQxSK - 1) * kBM * kW * 4;
-    static constexpr uint32_t kQOff = kRecvOff + kRecvBytes;   // Q_i bf16, 128 x 64, SW128 K-major
-    static constexpr uint32_t kWkOff = kQOff + kBM * 64 * 2;   // W_K chunks: 2 x (128 rows x 64 k)
+    static constexpr uint32_t kABytes = kBM * kBK * 2;  // Y: 128 rows x 64 k
+    static constexpr uint32_t kBBytes = 64 * kBK * 2;   // W_Q,i: 64 rows x 64 k
+    static constexpr uint32_t kStageBytes = kQxKbp * (kABytes + kBBytes);
+    static constexpr uint32_t kQOff = kQxStages * kStageBytes;  // Q_i bf16, 128 x 64, SW128 K-major
+    static constexpr uint32_t kWkOff = kQOff + kBM * 64 * 2;    // W_K chunks: 2 x (128 rows x 64 k)
     static constexpr uint32_t kBarOff = kWkOff + 2 * 128 * 64 * 2;
-    static constexpr uint32_t kTotal = kBarOff + 128 + 1024;
+    static constexpr uint32_t kTotal = kBarOff + 256 + 1024;
     static_assert(kTotal <= 232448, "fused query expansion shared memory");
 };
 struct QxParams {
-    int M, d_m, h, kbp, chunks, pdl;  // chunks: 128-column q' chunks per CTA (d_m / 4 / 128)
+    int M, d_m, h, nkb, nks, chunks, pdl;  // chunks: 128-column q' chunks per CTA (d_m / 4 / 128)
     const float* bq;
-    __nv_bfloat16* qp;                 // [M * h][d_m]
+    __nv_bfloat16* qp;                     // [M * h][d_m]
 };
 
-__global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
+__global__ void __launch_bounds__(kQxThreads, 1)
     tc_qexp_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmWq,
                    const __grid_constant__ CUtensorMap tmWk, QxParams p) {
     ELA_TL_DECL;
     using S = QxSmem;
-    constexpr int kW = S::kW;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + S::kBOff;
-    float* recv = reinterpret_cast<float*>(smem + S::kRecvOff);
     uint8_t* sQ = smem + S::kQOff;
     uint8_t* sWk = smem + S::kWkOff;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOff);
-    uint64_t* acc_full = full + 1;
-    uint64_t* recv_full = full + 2;
-    uint64_t* wk_full = full + 3;   // [2]
-    uint64_t* p_full = full + 5;    // [2]
-    uint64_t* p_empty = full + 7;   // [2] (epilogue -> MMA: q' chunk accumulator read)
-    uint64_t* wk_empty = full + 9;  // [2] (MMA -> TMA: W_K chunk buffer consumed)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 11);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOff);  // [kQxStages]
+    uint64_t* empty = full + kQxStages;                                // [kQxStages]
+    uint64_t* acc_full = empty + kQxStages;
+    uint64_t* q_full = acc_full + 1;   // epilogue warps -> MMA: Q_i staged in sQ
+    uint64_t* wk_full = q_full + 1;    // [2]
+    uint64_t* p_full = wk_full + 2;    // [2]
+    uint64_t* p_empty = p_full + 2;    // [2] (epilogue -> MMA: q' chunk accumulator read)
+    uint64_t* wk_empty = p_empty + 2;  // [2] (MMA -> TMA: W_K chunk buffer consumed)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wk_empty + 2);
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-    const int rank = int(ptx::cluster_ctarank());
-    const int t = int(blockIdx.x) / kQxSK;
-    const int z = t % p.h, m0 = (t / p.h) * kBM;  // head fastest: concurrent clusters share Y rows in L2
-    const int kb0 = rank * p.kbp;
-    const int col0 = rank * (p.d_m / kQxSK);     // this CTA's q' columns
+    const int quarter = int(blockIdx.x) & 3, t = int(blockIdx.x) >> 2;
+    const int z = t % p.h, m0 = (t / p.h) * kBM;  // quarter, then head fastest: neighbours share Y rows in L2
+    const int col0 = quarter * (p.d_m / 4);      // this CTA's q' columns
+    auto stage_a = [&](int s) { return smem + s * S::kStageBytes; };
+    auto stage_b = [&](int s) { return smem + s * S::kStageBytes + kQxKbp * S::kABytes; };
 
     if (warp == 0) {
         if (ptx::elect_one()) {
             ptx::prefetch_tmap(&tmY);
             ptx::prefetch_tmap(&tmWq);
             ptx::prefetch_tmap(&tmWk);
-            ptx::mbar_init(full, 1);
+            for (int s = 0; s < kQxStages; ++s) {
+                ptx::mbar_init(&full[s], 1);
+                ptx::mbar_init(&empty[s], 1);
+            }
             ptx::mbar_init(acc_full, 1);
-            ptx::mbar_init(recv_full, 1);
+            ptx::mbar_init(q_full, 4);
             for (int i = 0; i < 2; ++i) {
                 ptx::mbar_init(&wk_full[i], 1);
                 ptx::mbar_init(&p_full[i], 1);
@@ -696,27 +697,31 @@ __global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
                 ptx::mbar_init(&wk_empty[i], 1);
             }
             ptx::fence_mbar_init();
-            ptx::mbar_arrive_expect_tx(recv_full, S::kRecvBytes);
         }
         __syncwarp();
     } else if (warp == 1) {
         ptx::tmem_alloc<512>(tmem_slot);
     }
     ptx::tc_fence_before();
-    ptx::cluster_sync();
+    __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tq = tmem, tp = tmem + 128;  // Q partial: 64 columns; q' chunks: 2 x 128 columns
+    const uint32_t tq = tmem, tp = tmem + 128;  // Q_i: 64 columns; q' chunks: 2 x 128 columns
+    const int b_pre = p.pdl ? min(kQxStages, p.nks) : 0;
+    auto load_wk = [&](int c) {
+        const int bi = c & 1;
+        ptx::mbar_arrive_expect_tx(&wk_full[bi], 128 * 64 * 2);
+        ptx::tma_load_3d(sWk + bi * 128 * 64 * 2, &tmWk, &wk_full[bi], 0, col0 + c * 128, z, ptx::kEvictLast);
+    };
     if (p.pdl) {
         ptx::griddep_launch_dependents();
         // the weights do not depend on the preceding kernels: issue them before the wait
         if (warp == 0 && ptx::elect_one()) {
-            ptx::mbar_arrive_expect_tx(full, uint32_t(p.kbp) * (S::kABytes + S::kBBytes));
-            ptx::tma_load_4d(sB, &tmWq, full, 0, z * 64, 0, kb0, ptx::kEvictLast);
-            for (int c = 0; c < 2 && c < p.chunks; ++c) {
-                ptx::mbar_arrive_expect_tx(&wk_full[c], 128 * 64 * 2);
-                ptx::tma_load_3d(sWk + c * 128 * 64 * 2, &tmWk, &wk_full[c], 0, col0 + c * 128, z, ptx::kEvictLast);
+            for (int s = 0; s < b_pre; ++s) {
+                ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
+                ptx::tma_load_4d(stage_b(s), &tmWq, &full[s], 0, z * 64, 0, s * kQxKbp, ptx::kEvictLast);
             }
+            for (int c = 0; c < 2 && c < p.chunks; ++c) load_wk(c);
         }
         __syncwarp();
         ptx::griddep_wait();
@@ -724,47 +729,51 @@ __global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
     }
     if (warp == 0) {
         if (ptx::elect_one()) {
-            if (!p.pdl) {
-                ptx::mbar_arrive_expect_tx(full, uint32_t(p.kbp) * (S::kABytes + S::kBBytes));
-                ptx::tma_load_4d(sB, &tmWq, full, 0, z * 64, 0, kb0, ptx::kEvictLast);
+            if (!p.pdl)
+                for (int c = 0; c < 2 && c < p.chunks; ++c) load_wk(c);
+            for (int ks = 0; ks < p.nks; ++ks) {
+                const int s = ks % kQxStages;
+                ptx::mbar_wait(&empty[s], ((ks / kQxStages) & 1) ^ 1);
+                const bool pre = ks < b_pre;  // W_Q slice already in flight
+                if (!pre) ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
+                ptx::tma_load_4d(stage_a(s), &tmY, &full[s], 0, m0, 0, ks * kQxKbp, ptx::kEvictNormal);
+                if (!pre) ptx::tma_load_4d(stage_b(s), &tmWq, &full[s], 0, z * 64, 0, ks * kQxKbp, ptx::kEvictLast);
             }
-            ptx::tma_load_4d(sA, &tmY, full, 0, m0, 0, kb0, ptx::kEvictNormal);
-            for (int c = (p.pdl ? 2 : 0); c < 2 && c < p.chunks; ++c) {
-                ptx::mbar_arrive_expect_tx(&wk_full[c], 128 * 64 * 2);
-                ptx::tma_load_3d(sWk + c * 128 * 64 * 2, &tmWk, &wk_full[c], 0, col0 + c * 128, z, ptx::kEvictLast);
-            }
-        }
-        __syncwarp();
-        ptx::cluster_sync();  // (matches the all-gather barrier of the other warps; before any wait
-                              // on phase-2 progress, which needs that barrier)
-        if (ptx::elect_one()) {
             for (int c = 2; c < p.chunks; ++c) {
-                const int bi = c & 1;
-                ptx::mbar_wait(&wk_empty[bi], ((c >> 1) - 1) & 1);
-                ptx::mbar_arrive_expect_tx(&wk_full[bi], 128 * 64 * 2);
-                ptx::tma_load_3d(sWk + bi * 128 * 64 * 2, &tmWk, &wk_full[bi], 0, col0 + c * 128, z, ptx::kEvictLast);
+                ptx::mbar_wait(&wk_empty[c & 1], ((c >> 1) - 1) & 1);
+                load_wk(c);
             }
         }
         __syncwarp();
     } else if (warp == 1) {
-        // phase 1: partial Q_i over this CTA's k-blocks
+        // phase 1: Q_i over the whole K (one accumulation chain, k-blocks in order)
         constexpr uint32_t idq = ptx::idesc_bf16(kBM, 64, 0, 0);
-        ptx::mbar_wait(full, 0);
-        ptx::tc_fence_after();
-        if (lane == 0) {
-            const uint64_t a0 = ptx::sdesc_sw128(ptx::smem_u32(sA), 0, 1024);
-            const uint64_t b0 = ptx::sdesc_sw128(ptx::smem_u32(sB), 0, 1024);
-            for (int j = 0; j < p.kbp; ++j)
+        const uint64_t d0 = ptx::sdesc_sw128(ptx::smem_u32(smem), 0, 1024);
+        for (int ks = 0; ks < p.nks; ++ks) {
+            const int s = ks % kQxStages;
+            ptx::mbar_wait(&full[s], (ks / kQxStages) & 1);
+            if (ks == 0 && lane == 0) ELA_TL_MARK(0);  // first stage landed
+            ptx::tc_fence_after();
+            if (lane == 0) {
+                const uint64_t a = d0 + uint64_t((s * S::kStageBytes) >> 4);
+                const uint64_t b = a + uint64_t((kQxKbp * S::kABytes) >> 4);
 #pragma unroll
-                for (int k = 0; k < kBK / 16; ++k)
-                    ptx::mma_bf16(tq, a0 + uint64_t((j * S::kABytes) >> 4) + uint64_t(2 * k),
-                                  b0 + uint64_t((j * S::kBBytes) >> 4) + uint64_t(2 * k), idq, (j | k) != 0);
-            ptx::mma_commit(acc_full);
+                for (int j = 0; j < kQxKbp; ++j) {
+                    if (ks * kQxKbp + j >= p.nkb) break;
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k)
+                        ptx::mma_bf16(tq, a + uint64_t((j * S::kABytes) >> 4) + uint64_t(2 * k),
+                                      b + uint64_t((j * S::kBBytes) >> 4) + uint64_t(2 * k), idq, (ks | j | k) != 0);
+                }
+                ptx::mma_commit(&empty[s]);
+            }
+            __syncwarp();
         }
+        if (lane == 0) ptx::mma_commit(acc_full);
         __syncwarp();
-        ptx::cluster_sync();  // Q_i gathered into every CTA's sQ (written by the epilogue warps)
+        // phase 2: q' chunks, A = Q_i (smem, written by the epilogue warps), B = W_K,i rows
+        ptx::mbar_wait(q_full, 0);
         ptx::tc_fence_after();
-        // phase 2: q' chunks, A = Q_i (smem), B = W_K,i rows of the chunk
         constexpr uint32_t idp = ptx::idesc_bf16(kBM, 128, 0, 0);
         const uint64_t aq = ptx::sdesc_sw128(ptx::smem_u32(sQ), 0, 1024);
         const uint64_t bw = ptx::sdesc_sw128(ptx::smem_u32(sWk), 0, 1024);
@@ -787,74 +796,35 @@ __global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
         // epilogue warps: lane quadrant qd, row = 32 qd + lane of the 128-row tile
         const uint32_t qd = warp & 3;
         const int row = int(qd) * 32 + int(lane), m = m0 + row;
-        float bcol[kW];
+        // b_Q,i: every lane needs all 64 (its row): uniform-address vector loads
+        float bcol[64];
 #pragma unroll
-        for (int j = 0; j < kW; ++j) bcol[j] = __ldg(p.bq + z * 64 + rank * kW + j);
+        for (int j = 0; j < 64; j += 4) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bq + z * 64 + j));
+            bcol[j] = b4.x, bcol[j + 1] = b4.y, bcol[j + 2] = b4.z, bcol[j + 3] = b4.w;
+        }
         ptx::mbar_wait(acc_full, 0);
+        if (warp == 2 && lane == 0) ELA_TL_MARK(1);  // Q_i accumulated
         ptx::tc_fence_after();
         uint32_t v[64];
         ptx::tmem_ld32(tq + ((qd * 32) << 16), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
         ptx::tmem_ld32(tq + ((qd * 32) << 16) + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
         ptx::tmem_ld_wait();
-        // reduce-scatter: columns [kW pr, kW pr + kW) of the partial to CTA pr, staged as
-        // [pr][128 rows][kW] in the drained Y buffer and sent with one bulk copy per peer
-        float* send = reinterpret_cast<float*>(sA);
+        // Q_i row -> bf16 -> sQ (SW128 K-major: 16-byte chunk c of row r at r*128 + ((c ^ (r & 7)) << 4))
 #pragma unroll
-        for (int pr = 0; pr < kQxSK; ++pr) {
-            if (pr == rank) continue;
-#pragma unroll
-            for (int j = 0; j < kW; j += 4)
-                *reinterpret_cast<float4*>(send + (pr * kBM + row) * kW + j) =
-                    make_float4(__uint_as_float(v[pr * kW + j]), __uint_as_float(v[pr * kW + j + 1]),
-                                __uint_as_float(v[pr * kW + j + 2]), __uint_as_float(v[pr * kW + j + 3]));
+        for (int c = 0; c < 8; ++c) {
+            uint4 o;
+            o.x = pack2(__uint_as_float(v[8 * c + 0]) + bcol[8 * c + 0], __uint_as_float(v[8 * c + 1]) + bcol[8 * c + 1]);
+            o.y = pack2(__uint_as_float(v[8 * c + 2]) + bcol[8 * c + 2], __uint_as_float(v[8 * c + 3]) + bcol[8 * c + 3]);
+            o.z = pack2(__uint_as_float(v[8 * c + 4]) + bcol[8 * c + 4], __uint_as_float(v[8 * c + 5]) + bcol[8 * c + 5]);
+            o.w = pack2(__uint_as_float(v[8 * c + 6]) + bcol[8 * c + 6], __uint_as_float(v[8 * c + 7]) + bcol[8 * c + 7]);
+            *reinterpret_cast<uint4*>(sQ + uint32_t(row) * 128u + (uint32_t(c ^ (row & 7)) << 4)) = o;
         }
-        ptx::fence_proxy_async_smem();
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps staged their rows
-        if (warp == 2 && lane == 0) {
-#pragma unroll
-            for (int pr = 0; pr < kQxSK; ++pr) {
-                if (pr == rank) continue;
-                const int slot = rank - (rank > pr ? 1 : 0);
-                ptx::bulk_s2s_cluster(ptx::mapa(ptx::smem_u32(recv + slot * kBM * kW), uint32_t(pr)),
-                                      ptx::smem_u32(send + pr * kBM * kW), uint32_t(kBM * kW * 4),
-                                      ptx::mapa(ptx::smem_u32(recv_full), uint32_t(pr)));
-            }
-        }
-        ptx::mbar_wait(recv_full, 0);
-        float acc[kW];
-#pragma unroll
-        for (int j = 0; j < kW; ++j) acc[j] = 0.f;
-#pragma unroll
-        for (int sr = 0; sr < kQxSK; ++sr) {  // rank order: deterministic
-            if (sr == rank) {
-#pragma unroll
-                for (int j = 0; j < kW; ++j) acc[j] += __uint_as_float(v[rank * kW + j]);
-            } else {
-                const float* src = recv + ((sr - (sr > rank ? 1 : 0)) * kBM + row) * kW;
-#pragma unroll
-                for (int j = 0; j < kW; ++j) acc[j] += src[j];
-            }
-        }
-        // all-gather: this row's kW bf16 values of Q_i into every CTA's sQ (SW128 K-major:
-        // 16-byte chunk c of row r at r * 128 + ((c ^ (r & 7)) << 4)); kW = 16 -> two chunks
-        uint4 o[kW / 8];
-#pragma unroll
-        for (int c = 0; c < kW / 8; ++c) {
-            o[c].x = pack2(acc[8 * c + 0] + bcol[8 * c + 0], acc[8 * c + 1] + bcol[8 * c + 1]);
-            o[c].y = pack2(acc[8 * c + 2] + bcol[8 * c + 2], acc[8 * c + 3] + bcol[8 * c + 3]);
-            o[c].z = pack2(acc[8 * c + 4] + bcol[8 * c + 4], acc[8 * c + 5] + bcol[8 * c + 5]);
-            o[c].w = pack2(acc[8 * c + 6] + bcol[8 * c + 6], acc[8 * c + 7] + bcol[8 * c + 7]);
-        }
-#pragma unroll
-        for (int pr = 0; pr < kQxSK; ++pr)
-#pragma unroll
-            for (int c = 0; c < kW / 8; ++c) {
-                const int chunk = rank * (kW / 8) + c;
-                const uint32_t off = uint32_t(row) * 128u + (uint32_t(chunk ^ (row & 7)) << 4);
-                ptx::st_cluster_v4(ptx::mapa(ptx::smem_u32(sQ) + off, uint32_t(pr)), o[c]);
-            }
-        ptx::fence_proxy_async_cluster();
-        ptx::cluster_sync();
+        ptx::fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(q_full);
+        if (warp == 2 && lane == 0) ELA_TL_MARK(2);  // Q_i staged
         // phase-2 epilogue: q' chunks -> bf16 -> rows (m0 + row) * h + z
         __nv_bfloat16* dst_row = p.qp + (int64_t(m) * p.h + z) * p.d_m + col0;
         for (int c = 0; c < p.chunks; ++c) {
@@ -887,9 +857,10 @@ __global__ void __cluster_dims__(kQxSK, 1, 1) __launch_bounds__(kQxThreads, 1)
                 }
             }
         }
+        if (warp == 2 && lane == 0) ELA_TL_MARK(3);  // q' stores issued
     }
     ptx::tc_fence_before();
-    ptx::cluster_sync();
+    __syncthreads();
     ELA_TL_EXIT(kTlQexp);
     if (warp == 1) {
         ptx::tc_fence_after();
@@ -1096,6 +1067,15 @@ void launch_splitk(const GemmArgs& g, cudaStream_t st) {
     return launch_splitk_cfg<SK, false, false>(g, st);
 }
 
+// rows up to which the fused query expansion is used automatically (ELATTN_QEXP_ROWS overrides)
+int qexp_max_rows() {
+    static const int v = [] {
+        const char* e = getenv("ELATTN_QEXP_ROWS");
+        return e ? atoi(e) : 64;
+    }();
+    return v;
+}
+
 // fused query expansion for small batches (see tc_qexp_kernel); false = not applicable
 bool launch_qexp_fused(const void* Y, int M, const void* WqT, const float* bq, const void* Wk, void* qp, int h,
                        int d_m, int d_k, cudaStream_t st) {
@@ -1105,28 +1085,25 @@ bool launch_qexp_fused(const void* Y, int M, const void* WqT, const float* bq, c
     }();
     if (env == 0 || g_qexp_fused == 0) return false;
     const int items = int(ceil_div(M, kBM)) * h;
-    const int max_clusters = (num_sms() * 33) / 148;  // co-resident clusters of 4 (B200)
-    if (d_k != 64 || d_m % (128 * kQxSK) != 0 || d_m / kBK / kQxSK > QxSmem::kMaxKbp || items > max_clusters)
-        return false;
-    // measured faster than the two GEMMs only up to 64 rows (tools/probes/qexp_time.py: 8.4 vs
-    // 9.2-9.8 us at B <= 16, beam 4; 9.6 vs 9.4 at 128 rows): automatic use below that
-    if (g_qexp_fused < 0 && env < 0 && M > 64) return false;
-    if (!aligned16(Y) || !aligned16(WqT) || !aligned16(Wk) || !aligned16(qp)) return false;
+    if (d_k != 64 || d_m % 512 != 0 || 4 * items > 2 * num_sms()) return false;
+    // automatic use up to qexp_max_rows() rows (measured: tools/probes/qexp_time.py)
+    if (g_qexp_fused < 0 && env < 0 && M > qexp_max_rows()) return false;
+    if (bq == nullptr || !aligned16(Y) || !aligned16(WqT) || !aligned16(Wk) || !aligned16(qp) || !aligned16(bq)) return false;
     QxParams p{};
-    p.M = M, p.d_m = d_m, p.h = h, p.kbp = d_m / kBK / kQxSK, p.chunks = d_m / kQxSK / 128;
+    p.M = M, p.d_m = d_m, p.h = h, p.nkb = d_m / kBK, p.nks = int(ceil_div(d_m / kBK, kQxKbp)), p.chunks = d_m / 4 / 128;
     p.pdl = pdl_enabled() ? 1 : 0;
     p.bq = bq;
     p.qp = static_cast<__nv_bfloat16*>(qp);
     int zr = 0;
     // Y [M][d_m]: 4-D map (64 k, rows, 1, k-block); W_Q^T [h*64][d_m] likewise; W_K [h][d_m][64]: 3-D (k, d, head)
-    CUtensorMap ty = load_map(Y, d_m, 0, M, d_m, 1, kBM, p.kbp, &zr);
-    CUtensorMap twq = load_map(WqT, d_m, 0, h * 64, d_m, 1, 64, p.kbp, &zr);
+    CUtensorMap ty = load_map(Y, d_m, 0, M, d_m, 1, kBM, kQxKbp, &zr);
+    CUtensorMap twq = load_map(WqT, d_m, 0, h * 64, d_m, 1, 64, kQxKbp, &zr);
     const uint64_t kd[3] = {uint64_t(d_k), uint64_t(d_m), uint64_t(h)};
     const uint64_t ks[2] = {uint64_t(d_k) * 2, uint64_t(d_m) * d_k * 2};
     const uint32_t kbox[3] = {64, 128, 1};
     CUtensorMap twk = make_tmap_bf16(Wk, 3, kd, ks, kbox, 128);
     ELA_CHECK_CUDA(cudaFuncSetAttribute(tc_qexp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(QxSmem::kTotal)));
-    launch_ex(tc_qexp_kernel, dim3(items * kQxSK), dim3(kQxThreads), QxSmem::kTotal, st, 1, ty, twq, twk, p);
+    launch_ex(tc_qexp_kernel, dim3(items * 4), dim3(kQxThreads), QxSmem::kTotal, st, 1, ty, twq, twk, p);
     ELA_CHECK_LAUNCH();
     return true;
 }

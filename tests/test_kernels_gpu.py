@@ -453,8 +453,8 @@ def test_decode_ragged_schedules(B, rows, d_m):
 
 @pytest.mark.parametrize("R,d_m,h", [(128, 1024, 16), (256, 1024, 16), (77, 1024, 16), (200, 512, 8), (4, 1024, 16)])
 def test_fused_query_expansion(R, d_m, h):
-    """The fused small-batch query expansion (one launch: Q_i reduced over a cluster of 4
-    CTAs through DSMEM, all-gathered as bf16, then q' = Q_i.W_K,i^T) against torch fp32 of
+    """The fused small-batch query expansion (one launch: every CTA computes the bf16 Q_i
+    tile on the tensor cores, then its quarter of q' = Q_i.W_K,i^T) against torch fp32 of
     (bf16(Y.W_Q + b_Q))_i.W_K,i^T, against the two-GEMM path, and run-to-run identical."""
     import torch
 
