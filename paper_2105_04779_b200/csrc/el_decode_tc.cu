@@ -854,8 +854,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
                 xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 2));
                 // every value read from recv[sb] has reached a register (the shuffles above
-                // consumed them), so the peer may refill the buffer
-                if (lane == 0) ptx::mbar_arrive_remote(peer_recv_free0 + sb * 8);
+                // consumed them), so the peer may refill the buffer — for tile Gt + 2; none
+                // is sent past the schedule's end (so every remote operation into a CTA is
+                // awaited by it, and the kernel can end on an execution-only cluster barrier)
+                if (lane == 0 && Gt + 2 < G_total) ptx::mbar_arrive_remote(peer_recv_free0 + sb * 8);
                 uint32_t need = 0;
                 float alpha_a = 1.f, alpha_b = 1.f;
                 // lazy rescale: the reference max only moves when the tile max exceeds it
@@ -1153,7 +1155,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) ELA_TRACE(31, 0);  // all roles done
     if constexpr (TRACE)
         if (trace != nullptr && threadIdx.x == 0) trace[4096 + 2 * blockIdx.x + 1] = ptx::globaltimer();
-    ptx::cluster_sync();
+    // the peer stays alive until this CTA's DSMEM traffic into it has landed: every score
+    // exchange completes on a recv_full the peer waited on, and no recv_free arrive is sent
+    // past the schedule — execution-only barrier, the C / record stores drain at grid end
+    ptx::cluster_sync_relaxed();
     ELA_TL_EXIT(kTlDecode);
     if (warp == 1) {
         ptx::tc_fence_after();

@@ -103,6 +103,13 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+// Execution-only cluster barrier (no release/acquire of memory): for the end of a kernel
+// whose DSMEM traffic into each CTA is all tracked by mbarriers that CTA waits on before
+// arriving — every peer's incoming copies are then complete, and the CTA's own global stores
+// need not drain before the barrier (grid completion makes them visible to the next kernel).
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

@@ -612,7 +612,10 @@ __global__ void __launch_bounds__(kSkThreads, 1)
         if (warp == 2 && lane == 0) ELA_TL_MARK(3);  // stores issued
     }
     ptx::tc_fence_before();
-    ptx::cluster_sync();  // no CTA leaves while its partial columns are still in flight to a peer
+    // no CTA leaves while its partial columns are still in flight to a peer: each peer waited
+    // for all of its incoming columns (recv_full) before arriving, so an execution barrier is
+    // enough (a release would first drain this CTA's C stores, ~1 us)
+    ptx::cluster_sync_relaxed();
     ELA_TL_EXIT(kTlSplitK);
     if (warp == 1) {
         ptx::tc_fence_after();
