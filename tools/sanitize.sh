@@ -12,11 +12,11 @@ $CS --tool memcheck --leak-check no --report-api-errors no --print-limit 50 \
     -k "not full_size and not (garbage_workspace and (75 or 320))" > "$out/sanitize_memcheck.log" 2>&1
 echo "memcheck rc=$?"
 $CS --tool racecheck --racecheck-report all --print-limit 50 \
-    python -m pytest tests/test_kernels_gpu.py -q -x -k "decode_vs_torch and (64-32-512 or 16-77) or gemm_vs_torch and 128-128 or tf32x3 and 128-128 or splitk and 77-192 or ragged_schedules and 5-64" \
+    python -m pytest tests/test_kernels_gpu.py -q -x -k "decode_vs_torch and (64-32-512 or 16-77) or gemm_vs_torch and 128-128 or tf32x3 and 128-128 or splitk and 77-192 or ragged_schedules and 5-64 or fused_query_expansion and (4-1024 or 200-512)" \
     > "$out/sanitize_racecheck.log" 2>&1
 echo "racecheck rc=$?"
 $CS --tool synccheck --print-limit 50 \
-    python -m pytest tests/test_kernels_gpu.py -q -x -k "gemm_vs_torch and 128-128 or tf32x3 and 128-128 or splitk and 77-192" \
+    python -m pytest tests/test_kernels_gpu.py -q -x -k "gemm_vs_torch and 128-128 or tf32x3 and 128-128 or splitk and 77-192 or fused_query_expansion and (4-1024 or 200-512)" \
     > "$out/sanitize_synccheck.log" 2>&1
 echo "synccheck rc=$?"
 for f in memcheck racecheck synccheck; do echo "== $f"; tail -5 "$out/sanitize_$f.log"; done
