@@ -124,6 +124,16 @@ int elattn_gpu_el_attention_folded(elattn_gpu_params_t params, const void* qprim
 int elattn_gpu_el_attention_step(elattn_gpu_params_t params, const void* Y, const void* H,
                                  const int* n_per_input, int B, int x, int n, void* out,
                                  void* workspace, size_t workspace_bytes, elattn_stream_t stream);
+/*
+ * The same over SLOT-INDEXED states: input b attends over H[h_index[b]] of
+ * H [h_slots][n][d_m] (device h_index[B]; the hidden-state caches of decoder-only
+ * self-attention after a copy-on-fork reorder, elattn_gpu_cache_fork).  h_index = NULL
+ * is elattn_gpu_el_attention_step.  Errors as above; SHAPE (h_slots < 1 with h_index).
+ */
+int elattn_gpu_el_attention_step_indexed(elattn_gpu_params_t params, const void* Y, const void* H,
+                                         const int* n_per_input, const int* h_index, int h_slots, int B, int x,
+                                         int n, void* out, void* workspace, size_t workspace_bytes,
+                                         elattn_stream_t stream);
 
 /*
  * Stage (2) alone — the fused flash-style pass of el_attention_folded
@@ -190,6 +200,27 @@ int elattn_gpu_cache_append(void* cache, const void* Y, int* lengths, int lanes,
 int elattn_gpu_cache_gather(const void* src, const int* src_lengths, void* dst, int* dst_lengths,
                             const int* parent, int lanes_in, int lanes_out, int n_max, int d_m, int dtype,
                             int rows_hint, elattn_stream_t stream);
+/*
+ * Slot-indexed caches (copy on fork): lane i's history lives in slot lane_slot[i] of
+ * cache [layers][slots][n_max][d_m]; lengths stay per lane, [layers][lanes].
+ *   append_indexed: cache[lane_slot[i]][len[i]] = Y[i], ++len[i] (one layer's cache).
+ *   fork: gather_lanes (model.hpp:291-306) over the slot map — new lane i continues lane
+ *     parent[i]'s history.  The first new lane (lowest index) with a given parent takes
+ *     over the parent's slot (no copy); every further child of that parent gets a slot no
+ *     new lane owns and a copy of rows 0..len-1 in every layer.  So permute_lanes and
+ *     keep_lanes copy nothing and a beam reorder copies one history per duplicated parent.
+ *     Writes slot_out[lanes_out] and lengths_out[layers][lanes_out]; lanes_out <= slots;
+ *     an out-of-range parent gives the lane a free slot and length n_max + 1 (loud).
+ *     workspace: >= elattn_gpu_cache_fork_workspace(slots, lanes_in, lanes_out) bytes,
+ *     16-byte aligned.  Stream-ordered, graph-capturable.
+ */
+int elattn_gpu_cache_append_indexed(void* cache, const void* Y, int* lengths, const int* lane_slot, int lanes,
+                                    int n_max, int d_m, int dtype, elattn_stream_t stream);
+size_t elattn_gpu_cache_fork_workspace(int slots, int lanes_in, int lanes_out);
+int elattn_gpu_cache_fork(void* cache, int layers, int slots, int n_max, int d_m, int dtype,
+                          const int* lengths_in, int* lengths_out, const int* slot_in, int* slot_out,
+                          const int* parent, int lanes_in, int lanes_out, int rows_hint, void* workspace,
+                          size_t workspace_bytes, elattn_stream_t stream);
 /*
  * Whole-lane gather of fixed-size per-lane state (e.g. the K/V caches of the mixed form,
  * [R][h][t_max][d_k]): dst lane i = src lane parent[i], bytes_per_lane a multiple of 16;

@@ -262,11 +262,17 @@ class ElAttentionLayer:
         if shape is not None and tuple(t.shape) != tuple(shape):
             raise ShapeError(f"{what}: shape {tuple(t.shape)} != {tuple(shape)}")
 
-    def step(self, Y, H, n_per_input=None, out=None, stream=None):
+    def step(self, Y, H, n_per_input=None, out=None, stream=None, h_index=None):
+        """One EL cross-attention sub-layer (el_attention per lane, model.hpp:373-377) for
+        Y [B*x, d_m] over H [B, n, d_m]; with ``h_index`` (CUDA int32 [B]) input b attends
+        over H[h_index[b]] of H [slots, n, d_m] (slot-indexed caches)."""
         torch = _torch()
         if H.dim() != 3:
             raise ShapeError("H must be [B, n, d_m]")
-        B, n, d_m = H.shape
+        slots, n, d_m = H.shape
+        B = slots if h_index is None else h_index.numel()
+        if h_index is not None and (h_index.dtype != torch.int32 or not h_index.is_cuda):
+            raise ParamError("h_index must be a CUDA int32 tensor")
         if d_m != self.dev.d_m:
             raise ShapeError("el_attention: q/H width must equal d_m")
         if Y.dim() != 2 or Y.shape[1] != d_m or B < 1 or Y.shape[0] % B:
@@ -284,9 +290,14 @@ class ElAttentionLayer:
             npi = n_per_input.data_ptr()
         ws = self.workspace(B, x, n, stream)
         _record([out], stream)
-        capi.check(capi.lib().elattn_gpu_el_attention_step(
-            self.dev.handle, Y.data_ptr(), H.data_ptr(), npi or None, B, x, n, out.data_ptr(),
-            ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+        if h_index is None:
+            capi.check(capi.lib().elattn_gpu_el_attention_step(
+                self.dev.handle, Y.data_ptr(), H.data_ptr(), npi or None, B, x, n, out.data_ptr(),
+                ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+        else:
+            capi.check(capi.lib().elattn_gpu_el_attention_step_indexed(
+                self.dev.handle, Y.data_ptr(), H.data_ptr(), npi or None, h_index.data_ptr(), slots, B, x, n,
+                out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
         return out
 
     def build_el_query(self, Y, qprime=None, s=None, stream=None):
@@ -416,32 +427,55 @@ def _parent_tensor(parent, lanes: int):
 class HiddenStateCache:
     """Per-lane hidden-state caches for decoder-only EL self-attention (BASELINE config 4,
     the "hidden-state-only cache": each lane attends over its own history of layer inputs,
-    no per-head K/V).  Layer l keeps ``cache[l]`` [lanes, n_max, d_m] and device lengths
-    ``lengths[l]`` [lanes]; ``attend`` is the batched EL step with x = 1 over it.
-    ``gather(parent)`` is DecoderState::gather_lanes (model.hpp:291-306) on the device.
+    no per-head K/V).  Slot-indexed: layer l keeps ``cache[l]`` [slots, n_max, d_m], lane i's
+    history lives in slot ``lane_slot[i]``, and the device lengths ``lengths[l]`` [lanes]
+    are per lane; ``attend`` is the batched EL step with x = 1 reading through the slot map.
+    ``gather(parent)`` is DecoderState::gather_lanes (model.hpp:291-306) as a copy-on-fork on
+    the device (``elattn_gpu_cache_fork``): a lane that is its parent's first child keeps the
+    parent's slot, so permute / keep copy nothing and a beam reorder copies one history per
+    duplicated parent.  ``lane_view(l)`` returns the [lanes, n_max, d_m] view in lane order.
     """
 
-    def __init__(self, layers: int, lanes: int, n_max: int, d_m: int, dtype: int = DTYPE_BF16):
+    def __init__(self, layers: int, lanes: int, n_max: int, d_m: int, dtype: int = DTYPE_BF16,
+                 slots: Optional[int] = None):
         torch = _torch()
         self.dtype, self.lanes, self.n_max, self.d_m = dtype, lanes, n_max, d_m
-        self.cache = torch.zeros(layers, lanes, n_max, d_m, dtype=_tdtype(dtype), device="cuda")
+        self.slots = max(lanes, slots or lanes)
+        self.cache = torch.zeros(layers, self.slots, n_max, d_m, dtype=_tdtype(dtype), device="cuda")
         self.lengths = torch.zeros(layers, lanes, dtype=torch.int32, device="cuda")
-        self._spare = None
+        self.lane_slot = torch.arange(lanes, dtype=torch.int32, device="cuda")
+        self._spare = None  # (lengths, lane_slot) buffers the next fork writes
+        self._ws = None
+
+    def lane_view(self, layer: int):
+        """Layer ``layer``'s histories in lane order, [lanes, n_max, d_m] (a copy)."""
+        return self.cache[layer].index_select(0, self.lane_slot.long())
 
     def append(self, layer: int, Y, stream=None):
-        """cache[layer][l][len] = Y[l]; ++len (device side)."""
+        """cache[layer][lane_slot[i]][len[i]] = Y[i]; ++len[i] (device side)."""
         torch = _torch()
         if tuple(Y.shape) != (self.lanes, self.d_m) or Y.dtype != _tdtype(self.dtype):
             raise ShapeError("HiddenStateCache.append: Y must be [lanes, d_m] of the cache dtype")
         Y = Y.contiguous()
         st = stream if stream is not None else torch.cuda.current_stream()
-        capi.check(capi.lib().elattn_gpu_cache_append(self.cache[layer].data_ptr(), Y.data_ptr(),
-                                                      self.lengths[layer].data_ptr(), self.lanes, self.n_max,
-                                                      self.d_m, self.dtype, _stream_ptr(st)))
+        capi.check(capi.lib().elattn_gpu_cache_append_indexed(
+            self.cache[layer].data_ptr(), Y.data_ptr(), self.lengths[layer].data_ptr(), self.lane_slot.data_ptr(),
+            self.lanes, self.n_max, self.d_m, self.dtype, _stream_ptr(st)))
 
     def attend(self, layer_params: ElAttentionLayer, layer: int, Y, out=None, stream=None):
-        """EL self-attention of every lane's query row over its own cache."""
-        return layer_params.step(Y, self.cache[layer], self.lengths[layer], out=out, stream=stream)
+        """EL self-attention of every lane's query row over its own history."""
+        return layer_params.step(Y, self.cache[layer], self.lengths[layer], out=out, stream=stream,
+                                 h_index=self.lane_slot)
+
+    def _grow(self, slots: int, stream=None):
+        """More slots than lanes_out needs: a larger store, histories kept in their slots."""
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(st):
+            big = torch.zeros(self.cache.shape[0], slots, self.n_max, self.d_m, dtype=self.cache.dtype,
+                              device="cuda")
+            big[:, : self.slots].copy_(self.cache)
+        self.cache, self.slots = big, slots
 
     def gather(self, parent, rows_hint: Optional[int] = None, stream=None):
         """New lane i = old lane parent[i] in every layer (DecoderState::gather_lanes,
@@ -449,20 +483,27 @@ class HiddenStateCache:
         torch = _torch()
         parent = _parent_tensor(parent, self.lanes)
         lanes_out = parent.numel()
-        if self._spare is None or self._spare[0].shape[1] != lanes_out:
-            L = self.cache.shape[0]
-            self._spare = (torch.empty(L, lanes_out, self.n_max, self.d_m, dtype=self.cache.dtype, device="cuda"),
-                           torch.empty(L, lanes_out, dtype=torch.int32, device="cuda"))
-        dst, dlen = self._spare
+        if lanes_out > self.slots:
+            self._grow(lanes_out, stream)
+        L = self.cache.shape[0]
+        if self._spare is None or self._spare[1].numel() != lanes_out:
+            self._spare = (torch.empty(L, lanes_out, dtype=torch.int32, device="cuda"),
+                           torch.empty(lanes_out, dtype=torch.int32, device="cuda"))
+        need = capi.lib().elattn_gpu_cache_fork_workspace(self.slots, self.lanes, lanes_out)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        dlen, dslot = self._spare
         st = stream if stream is not None else torch.cuda.current_stream()
         hint = rows_hint if rows_hint is not None else self.n_max
-        for l in range(self.cache.shape[0]):
-            capi.check(capi.lib().elattn_gpu_cache_gather(
-                self.cache[l].data_ptr(), self.lengths[l].data_ptr(), dst[l].data_ptr(), dlen[l].data_ptr(),
-                parent.data_ptr(), self.lanes, lanes_out, self.n_max, self.d_m, self.dtype, hint,
-                _stream_ptr(st)))
-        self._spare = (self.cache, self.lengths)
-        self.cache, self.lengths = dst, dlen
+        capi.check(capi.lib().elattn_gpu_cache_fork(
+            self.cache.data_ptr(), L, self.slots, self.n_max, self.d_m, self.dtype, self.lengths.data_ptr(),
+            dlen.data_ptr(), self.lane_slot.data_ptr(), dslot.data_ptr(), parent.data_ptr(), self.lanes, lanes_out,
+            hint, self._ws.data_ptr(), self._ws.numel(), _stream_ptr(st)))
+        if self.lengths.shape[1] == lanes_out:
+            self._spare = (self.lengths, self.lane_slot)
+        else:
+            self._spare = None
+        self.lengths, self.lane_slot = dlen, dslot
         self.lanes = lanes_out
 
     def keep(self, mask, rows_hint: Optional[int] = None, stream=None):

@@ -26,6 +26,7 @@ EXPORTED_SYMBOLS = (
     "elattn_gpu_build_el_query",
     "elattn_gpu_el_attention_folded",
     "elattn_gpu_el_attention_step",
+    "elattn_gpu_el_attention_step_indexed",
     "elattn_gpu_el_attention_decode",
     "elattn_gpu_workspace_size",
     "elattn_gpu_decode_kernel_kind",
@@ -36,6 +37,9 @@ EXPORTED_SYMBOLS = (
     "elattn_gpu_decoder_kernels_per_run",
     "elattn_gpu_cache_append",
     "elattn_gpu_cache_gather",
+    "elattn_gpu_cache_append_indexed",
+    "elattn_gpu_cache_fork_workspace",
+    "elattn_gpu_cache_fork",
     "elattn_gpu_kv_append",
     "elattn_gpu_mixed_self_attention",
     "elattn_gpu_mixed_workspace_size",
@@ -104,6 +108,7 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.elattn_gpu_build_el_query.argtypes = [vp, vp, i32, vp, vp, vp, sz, vp]
     lib.elattn_gpu_el_attention_folded.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, sz, vp]
     lib.elattn_gpu_el_attention_step.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, sz, vp]
+    lib.elattn_gpu_el_attention_step_indexed.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, vp, sz, vp]
     lib.elattn_gpu_el_attention_decode.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp]
     lib.elattn_gpu_workspace_size.argtypes = [vp, i32, i32, i32]
     lib.elattn_gpu_workspace_size.restype = sz
@@ -117,6 +122,10 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.elattn_gpu_decoder_kernels_per_run.restype = i64
     lib.elattn_gpu_cache_append.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
     lib.elattn_gpu_cache_gather.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp]
+    lib.elattn_gpu_cache_append_indexed.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp]
+    lib.elattn_gpu_cache_fork_workspace.argtypes = [i32, i32, i32]
+    lib.elattn_gpu_cache_fork_workspace.restype = sz
+    lib.elattn_gpu_cache_fork.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, i32, vp, sz, vp]
     lib.elattn_gpu_kv_append.argtypes = [vp, vp, i32, vp, vp, i32, i32, vp]
     lib.elattn_gpu_mixed_self_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, i32, i32, vp, vp, sz, vp]
     lib.elattn_gpu_mixed_workspace_size.argtypes = [vp, i32, i32]
@@ -129,7 +138,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.elattn_gpu_mha_attention.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, sz, vp]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(lib, name)
-        if fn.restype is ctypes.c_int and name not in ("elattn_gpu_decode_kernel_kind",):
+        if fn.restype is ctypes.c_int and name not in ("elattn_gpu_decode_kernel_kind",
+                                                       "elattn_gpu_cache_fork_workspace"):
             fn.restype = i32
 
 

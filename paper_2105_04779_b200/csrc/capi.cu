@@ -304,13 +304,13 @@ struct Tf32H {
     int B = 0, n = 0;
 };
 Tf32H tf32_split_h(const elattn_gpu_params_s* p, Scratch& s, const float* H, const int* npi, int B, int n,
-                   cudaStream_t st) {
+                   cudaStream_t st, const int* h_index = nullptr) {
     Tf32H h;
     h.B = B, h.n = n;
     h.H = take_split(s, size_t(B) * n * p->d_m);
     h.HT = take_split(s, size_t(B) * p->d_m * pad32(n));
-    launch_tf32_split(H, int64_t(B) * n, p->d_m, p->d_m, h.H.hi, h.H.lo, npi, n, st);
-    launch_tf32_split_t(H, B, n, p->d_m, int(pad32(n)), npi, h.HT.hi, h.HT.lo, st);
+    launch_tf32_split(H, int64_t(B) * n, p->d_m, p->d_m, h.H.hi, h.H.lo, npi, n, st, h_index);
+    launch_tf32_split_t(H, B, n, p->d_m, int(pad32(n)), npi, h.HT.hi, h.HT.lo, st, h_index);
     return h;
 }
 
@@ -378,14 +378,16 @@ bool use_tc_decode(const elattn_gpu_params_s* p, int rows_per_input) {
 // (2) fused decode: C = softmax(q'.H^T / sqrt(d_k)) . H   (attention.hpp:272-280)
 // h_static: H is not written by any kernel of the stream while these kernels run (the
 // decoder step's graph), so the decode may start streaming it before its PDL wait
+// h_index (slot-indexed caches): input b reads H[h_index[b]] of h_slots blocks
 void decode(const elattn_gpu_params_s* p, const void* qp, const void* H, const int* npi, int B,
             int rows_per_input, int n, void* C, float* part, cudaStream_t st, float2* stats = nullptr,
-            bool h_static = false) {
+            bool h_static = false, const int* h_index = nullptr, int h_slots = 0) {
     const float scale = float(1.0 / std::sqrt(double(p->d_k)));
     if (use_tc_decode(p, rows_per_input))
-        launch_el_decode_tc(qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats, part, h_static);
+        launch_el_decode_tc(qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats, part, h_static, h_index,
+                            h_slots);
     else
-        launch_el_decode_simt(p->dtype, qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats);
+        launch_el_decode_simt(p->dtype, qp, H, npi, B, rows_per_input, n, p->d_m, scale, C, st, stats, h_index);
 }
 
 void check_handle(const elattn_gpu_params_s* p) {
@@ -600,16 +602,24 @@ int elattn_gpu_el_attention_decode(elattn_gpu_params_t p, const void* qprime, co
 int elattn_gpu_el_attention_step(elattn_gpu_params_t p, const void* Y, const void* H,
                                  const int* n_per_input, int B, int x, int n, void* out, void* ws,
                                  size_t ws_bytes, elattn_stream_t stream) {
+    return elattn_gpu_el_attention_step_indexed(p, Y, H, n_per_input, nullptr, 0, B, x, n, out, ws, ws_bytes,
+                                                stream);
+}
+
+int elattn_gpu_el_attention_step_indexed(elattn_gpu_params_t p, const void* Y, const void* H,
+                                         const int* n_per_input, const int* h_index, int h_slots, int B, int x,
+                                         int n, void* out, void* ws, size_t ws_bytes, elattn_stream_t stream) {
     return guarded([&] {
         check_handle(p);
         ELA_REQUIRE(B >= 1 && x >= 1, ELATTN_ERR_SHAPE, "el_attention_step: B and x must be >= 1");
         ELA_REQUIRE(n >= 1, ELATTN_ERR_STATE, "el_attention: empty context");
         ELA_REQUIRE(Y && H && out, ELATTN_ERR_PARAM, "el_attention_step: null buffer");
+        ELA_REQUIRE(h_index == nullptr || h_slots >= 1, ELATTN_ERR_SHAPE, "el_attention_step: h_slots must be >= 1");
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         const int64_t R = int64_t(B) * x;
         if (use_tf32_path(p) && al16p(Y) && al16p(H) && al16p(out)) {
             Scratch scratch(ws, ws_bytes, tf32_h_bytes(p, B, n) + tf32_layer_bytes(p, B, x, n), st);
-            const Tf32H hs = tf32_split_h(p, scratch, static_cast<const float*>(H), n_per_input, B, n, st);
+            const Tf32H hs = tf32_split_h(p, scratch, static_cast<const float*>(H), n_per_input, B, n, st, h_index);
             tf32_layer(p, scratch, static_cast<const float*>(Y), hs, n_per_input, x, static_cast<float*>(out), st);
             return;
         }
@@ -622,7 +632,7 @@ int elattn_gpu_el_attention_step(elattn_gpu_params_t p, const void* Y, const voi
         void* V = scratch.take(qb);
         float* part = static_cast<float*>(scratch.take(decode_scratch(p)));
         query_expansion(p, Y, R, Q, qp, st, /*need_Q=*/false);
-        decode(p, qp, H, n_per_input, B, x * p->h, n, C, part, st);
+        decode(p, qp, H, n_per_input, B, x * p->h, n, C, part, st, nullptr, false, h_index, h_slots);
         output_projection(p, C, R, V, out, st);
     });
 }
@@ -903,6 +913,40 @@ extern "C" int elattn_gpu_cache_append(void* cache, const void* Y, int* lengths,
         ELA_REQUIRE(lanes >= 1 && n_max >= 1 && d_m >= 1, ELATTN_ERR_SHAPE, "cache_append: bad shape");
         ELA_REQUIRE(dtype == ELATTN_DTYPE_F32 || dtype == ELATTN_DTYPE_BF16, ELATTN_ERR_PARAM, "unknown dtype");
         launch_cache_append(cache, Y, lengths, lanes, n_max, d_m, dtype, reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
+extern "C" int elattn_gpu_cache_append_indexed(void* cache, const void* Y, int* lengths, const int* lane_slot,
+                                               int lanes, int n_max, int d_m, int dtype, elattn_stream_t stream) {
+    return guarded([&] {
+        ELA_REQUIRE(cache && Y && lengths && lane_slot, ELATTN_ERR_PARAM, "cache_append: null buffer");
+        ELA_REQUIRE(lanes >= 1 && n_max >= 1 && d_m >= 1, ELATTN_ERR_SHAPE, "cache_append: bad shape");
+        ELA_REQUIRE(dtype == ELATTN_DTYPE_F32 || dtype == ELATTN_DTYPE_BF16, ELATTN_ERR_PARAM, "unknown dtype");
+        launch_cache_append(cache, Y, lengths, lanes, n_max, d_m, dtype, reinterpret_cast<cudaStream_t>(stream),
+                            lane_slot);
+    });
+}
+
+extern "C" size_t elattn_gpu_cache_fork_workspace(int slots, int lanes_in, int lanes_out) {
+    return cache_fork_workspace(slots, lanes_in, lanes_out);
+}
+
+extern "C" int elattn_gpu_cache_fork(void* cache, int layers, int slots, int n_max, int d_m, int dtype,
+                                     const int* lengths_in, int* lengths_out, const int* slot_in, int* slot_out,
+                                     const int* parent, int lanes_in, int lanes_out, int rows_hint, void* workspace,
+                                     size_t workspace_bytes, elattn_stream_t stream) {
+    return guarded([&] {
+        ELA_REQUIRE(cache && lengths_in && lengths_out && slot_in && slot_out && parent, ELATTN_ERR_PARAM,
+                    "cache_fork: null buffer");
+        ELA_REQUIRE(lengths_in != lengths_out && slot_in != slot_out, ELATTN_ERR_PARAM,
+                    "cache_fork: the lengths / slot maps in and out must differ");
+        ELA_REQUIRE(lanes_out >= 1, ELATTN_ERR_STATE, "gather_lanes: all lanes dropped");
+        ELA_REQUIRE(layers >= 1 && lanes_in >= 1 && slots >= 1 && n_max >= 1 && d_m >= 1, ELATTN_ERR_SHAPE,
+                    "cache_fork: bad shape");
+        ELA_REQUIRE(dtype == ELATTN_DTYPE_F32 || dtype == ELATTN_DTYPE_BF16, ELATTN_ERR_PARAM, "unknown dtype");
+        launch_cache_fork(cache, layers, slots, n_max, d_m, dtype, lengths_in, lengths_out, slot_in, slot_out, parent,
+                          lanes_in, lanes_out, rows_hint, workspace, workspace_bytes,
+                          reinterpret_cast<cudaStream_t>(stream));
     });
 }
 

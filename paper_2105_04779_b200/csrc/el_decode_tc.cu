@@ -186,6 +186,7 @@ struct SplitArgs {
     uint64_t h_pol;  // L2 policy of the H stream (evict-last when H fits in L2: the layers re-read it)
     int h_pre;       // H static across the stream's kernels (decoder step): tiles of the first segment
                      // loaded BEFORE the programmatic-dependent-launch wait (0 = after it)
+    const int* h_index;  // MASK builds: input b reads H[h_index[b]] (slot-indexed lane caches; null = H[b])
 };
 // RAGGED: the ragged schedules (T < 0) are compiled only into the MASK instantiations (the
 // ones launched with n_per_input); the production kernel keeps its schedule state minimal.
@@ -540,6 +541,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int b, j0, j1, Tb, kind;
             while (sc.next(b, j0, j1, Tb, kind)) {
                 const int T = j1 - j0;
+                // H block of this input (slot-indexed caches: a lane's history lives in its slot)
+                const int hb = (MASK && sa.h_index != nullptr) ? __ldg(sa.h_index + b / sa.vchunks) : b / sa.vchunks;
                 int nb = -1;  // input of the next segment (its q' is prefetched into L2)
                 {
                     Sched<MASK> pk = sc;
@@ -550,7 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const int j = j0 + jj, Gt = G + jj;
                     if (TRACE && tune.l2_ahead > 0 && j + tune.l2_ahead < Tb)
                         for (int c = 0; c < 2 * UNITS; ++c)
-                            ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, b / sa.vchunks);
+                            ptx::tma_prefetch_3d(&tm_h, dm_off + 64 * c, (j + tune.l2_ahead) * kNT, hb);
                     for (int u = 0; u < UNITS; ++u) {
                         const int g = Gt * UNITS + u, s = g % kRing;
                         if (Gt < n_pre) break;  // issued before the PDL wait
@@ -563,8 +566,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         // sibling virtual inputs (same H_b, running on neighbouring clusters)
                         // re-read the tile from L2: keep it there
                         const uint64_t pol = sa.h_pol;
-                        ptx::tma_load_3d(dst, &tm_h, &unit_full[s], col, j * kNT, b / sa.vchunks, pol);
-                        ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, b / sa.vchunks,
+                        ptx::tma_load_3d(dst, &tm_h, &unit_full[s], col, j * kNT, hb, pol);
+                        ptx::tma_load_3d(dst + kChunkBytes, &tm_h, &unit_full[s], col + 64, j * kNT, hb,
                                          pol);
                     }
                     if (jj == (T > kQPrefetchTiles ? T - kQPrefetchTiles : 0) && nb >= 0 && nb != b) {
@@ -1348,7 +1351,8 @@ constexpr int kRaggedSkMaxInputs = 8;  // ragged stream-K up to 8 inputs per clu
 
 template <int UNITS>
 void launch_units(const void* qp, const void* H, const int* npi, int B, int rows, int n_stride, int d_m,
-                  float scale_log2, void* ctx, cudaStream_t st, float2* stats, float* part, bool h_static) {
+                  float scale_log2, void* ctx, cudaStream_t st, float2* stats, float* part, bool h_static,
+                  const int* h_index, int h_slots) {
     // > 64 query rows per input: rows/64 virtual inputs of 64 rows each (q' and C rows are
     // contiguous per input, so virtual input v owns rows [64 v, 64 v + 64)); H_b is shared
     const int vchunks = rows > kRowsQ ? (rows + kRowsQ - 1) / kRowsQ : 1;
@@ -1360,7 +1364,7 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const uint64_t qstr[1] = {uint64_t(d_m) * 2};
     const uint32_t qbox[2] = {64, kRowsQ};
     CUtensorMap tq = make_tmap_bf16(qp, 2, qdims, qstr, qbox);
-    const uint64_t hdims[3] = {uint64_t(d_m), uint64_t(n_stride), uint64_t(B_h)};
+    const uint64_t hdims[3] = {uint64_t(d_m), uint64_t(n_stride), uint64_t(h_index ? h_slots : B_h)};
     const uint64_t hstr[2] = {uint64_t(d_m) * 2, uint64_t(n_stride) * d_m * 2};
     const uint32_t hbox[3] = {64, kNT, 1};
     CUtensorMap th = make_tmap_bf16(H, 3, hdims, hstr, hbox);
@@ -1371,7 +1375,7 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     CUtensorMap tc = make_tmap_bf16(ctx, 2, cdims, qstr, cbox, 64);
     // instrumented instantiation (trace hook, lookahead knobs) only when asked for
     const bool instr = g_decode_trace != nullptr || g_tuning.s_ahead != 4 || g_tuning.l2_ahead != 0;
-    const bool mask = npi != nullptr || n_stride % kNT != 0;
+    const bool mask = npi != nullptr || n_stride % kNT != 0 || h_index != nullptr;
     const bool r16 = rows <= 16 && !instr;  // one beam x <= 16 heads (vchunks == 1)
     auto kern = instr ? (mask ? el_decode_tc_kernel<UNITS, true, true> : el_decode_tc_kernel<UNITS, true, false>)
                 : r16 ? (mask ? el_decode_tc_kernel<UNITS, false, true, true> : el_decode_tc_kernel<UNITS, false, false, true>)
@@ -1382,6 +1386,7 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const int max_cl = num_sms_decode() / 2;
     int clusters;
     SplitArgs sa{};
+    sa.h_index = h_index;
     // Whole inputs strided over the clusters unless the last round would fill less than 60%
     // of the clusters: then stream-K (every input-segment transition costs a pipeline drain,
     // so splitting only pays when the tail is short; measured on B200 for B = 64..320).
@@ -1506,7 +1511,7 @@ bool el_decode_tc_supported(int rows_per_input, int d_m) {
 
 void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B, int rows_per_input,
                          int n_stride, int d_m, float scale, void* ctx, cudaStream_t st, float2* stats,
-                         float* part, bool h_static) {
+                         float* part, bool h_static, const int* h_index, int h_slots) {
     ELA_REQUIRE(el_decode_tc_supported(rows_per_input, d_m), ELATTN_ERR_UNSUPPORTED,
                 "tcgen05 decode: rows <= 512, d_m in {256, 512, 768, 1024}");
     ELA_REQUIRE((reinterpret_cast<uintptr_t>(qp) & 15) == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0 &&
@@ -1521,10 +1526,10 @@ void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, 
     }();
     (void)env_read;
     switch (d_m / 256) {
-        case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static);
-        case 2: return launch_units<2>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static);
-        case 3: return launch_units<3>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static);
-        default: return launch_units<4>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static);
+        case 1: return launch_units<1>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static, h_index, h_slots);
+        case 2: return launch_units<2>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static, h_index, h_slots);
+        case 3: return launch_units<3>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static, h_index, h_slots);
+        default: return launch_units<4>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2, ctx, st, stats, part, h_static, h_index, h_slots);
     }
 }
 

@@ -40,7 +40,7 @@ void launch_key_bias_scalars(int dtype, const void* Q, const float* bk, int R, i
 // with other score sources (mixed self-attention).
 void launch_el_decode_simt(int dtype, const void* qp, const void* H, const int* n_per_input,
                            int B, int rows_per_input, int n_stride, int d_m, float scale,
-                           void* ctx, cudaStream_t st, float2* stats = nullptr);
+                           void* ctx, cudaStream_t st, float2* stats = nullptr, const int* h_index = nullptr);
 
 // tcgen05 GEMM family (tc_gemm.cu: bf16 in, fp32 accumulate in TMEM, bf16 out), same
 // contract as launch_simt_gemm but requires K % 64 == 0, 16-byte aligned rows and
@@ -81,12 +81,14 @@ struct Tf32GemmArgs {
 bool tf32_gemm_supported(const Tf32GemmArgs& g);
 void launch_tf32_gemm(const Tf32GemmArgs& g, cudaStream_t st);
 // X [rows][cols] (row stride ld) -> hi, lo [rows][cols]; rows r with npi and
-// r % n_stride >= npi[r / n_stride] are zeroed.
+// r % n_stride >= npi[r / n_stride] are zeroed; h_index: output block b of n_stride rows
+// reads block h_index[b] of X (slot-indexed caches)
 void launch_tf32_split(const float* X, int64_t rows, int cols, int64_t ld, float* hi, float* lo, const int* npi,
-                       int n_stride, cudaStream_t st);
-// H [B][n][d_m] -> transposed hi/lo [B][d_m][n_pad], keys >= n_b (npi) or >= n zeroed
+                       int n_stride, cudaStream_t st, const int* h_index = nullptr);
+// H [B][n][d_m] -> transposed hi/lo [B][d_m][n_pad], keys >= n_b (npi) or >= n zeroed;
+// input b reads H[h_index[b]] when h_index is given
 void launch_tf32_split_t(const float* H, int B, int n, int d_m, int n_pad, const int* npi, float* hi, float* lo,
-                         cudaStream_t st);
+                         cudaStream_t st, const int* h_index = nullptr);
 // softmax over the first n_b of each score row (see tf32_gemm.cu) -> (P_hi, P_lo), stats
 void launch_tf32_softmax(const float* S, int64_t total_rows, int rows, int n_stride, int ld, const int* npi,
                          float scale, float* P_hi, float* P_lo, float2* stats, cudaStream_t st);
@@ -111,7 +113,12 @@ void launch_beam_topk(const float* lprobs, const float* live_lp, const float* pe
 void launch_lane_gather(const void* src, void* dst, const int* parent, int lanes_in, int lanes_out,
                         int64_t bytes_per_lane, cudaStream_t st);
 void launch_cache_append(void* cache, const void* Y, int* len, int lanes, int n_max, int d_m, int dtype,
-                         cudaStream_t st);
+                         cudaStream_t st, const int* lane_slot = nullptr);
+// slot-indexed caches: copy-on-fork reorder (see lane_cache.cu)
+size_t cache_fork_workspace(int slots, int lanes_in, int lanes_out);
+void launch_cache_fork(void* cache, int layers, int slots, int n_max, int d_m, int dtype, const int* len_in,
+                       int* len_out, const int* slot_in, int* slot_out, const int* parent, int lanes_in, int lanes_out,
+                       int rows_hint, void* ws, size_t ws_bytes, cudaStream_t st);
 void launch_cache_gather(const void* src, const int* src_len, void* dst, int* dst_len, const int* parent,
                          int lanes_in, int lanes_out, int n_max, int d_m, int dtype, int rows_hint,
                          cudaStream_t st);
@@ -132,6 +139,7 @@ bool el_decode_tc_supported(int rows_per_input, int d_m);
 size_t el_decode_tc_scratch_bytes(int d_m);
 void launch_el_decode_tc(const void* qp, const void* H, const int* n_per_input, int B,
                          int rows_per_input, int n_stride, int d_m, float scale, void* ctx,
-                         cudaStream_t st, float2* stats, float* part, bool h_static = false);
+                         cudaStream_t st, float2* stats, float* part, bool h_static = false,
+                         const int* h_index = nullptr, int h_slots = 0);
 
 }  // namespace elattn_gpu

@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
                                                              int d_m, float scale_log2,
                                                              T* __restrict__ ctx, float2* __restrict__ stats,
                                                              int splits, float* __restrict__ part_o,
-                                                             float2* __restrict__ part_ml) {
+                                                             float2* __restrict__ part_ml,
+                                                             const int* __restrict__ h_index) {
     extern __shared__ float smem[];
     // padded rows: q rows 16 banks apart (+16), H rows 4 apart land 16 banks apart (+4), so
     // the two half-warps of the score phase never collide
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(256) el_decode_simt_kernel(const T* __restrict
     float* s_m = s_l + kSimtRows;                    // [kSimtRows]
     const int b = blockIdx.y, r0 = blockIdx.x * kSimtRows, tid = threadIdx.x;
     const int n = n_per_input ? n_per_input[b] : n_stride;
-    const T* Hb = H + (int64_t)b * n_stride * d_m;
+    const T* Hb = H + (int64_t)(h_index ? h_index[b] : b) * n_stride * d_m;  // slot-indexed caches
     const int64_t row_base = (int64_t)b * rows_per_input + r0;
     const int nrows = min(kSimtRows, rows_per_input - r0);
 
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(256) simt_merge_kernel(const float* __restrict
 template <typename T, int CPT>
 static void launch_decode_cpt(const void* qp, const void* H, const int* npi, int B, int rows,
                               int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st,
-                              float2* stats) {
+                              float2* stats, const int* h_index) {
     const size_t smem =
         sizeof(float) * (size_t(kSimtRows) * (d_m + 16) + size_t(kSimtTile) * (d_m + 4) +
                          kSimtRows * kSimtTile + 3 * kSimtRows);
@@ -353,7 +354,8 @@ static void launch_decode_cpt(const void* qp, const void* H, const int* npi, int
     }
     dim3 grid(unsigned(ceil_div(rows, kSimtRows)), unsigned(B), unsigned(splits));
     kern<<<grid, 256, smem, st>>>(static_cast<const T*>(qp), static_cast<const T*>(H), npi, rows,
-                                  n_stride, d_m, scale_log2, static_cast<T*>(ctx), stats, splits, parts.o, parts.ml);
+                                  n_stride, d_m, scale_log2, static_cast<T*>(ctx), stats, splits, parts.o, parts.ml,
+                                  h_index);
     ELA_CHECK_LAUNCH();
     if (splits > 1) {
         simt_merge_kernel<T><<<unsigned(total_rows), 256, 0, st>>>(parts.o, parts.ml, splits, total_rows, rows, npi,
@@ -365,15 +367,15 @@ static void launch_decode_cpt(const void* qp, const void* H, const int* npi, int
 template <typename T>
 static void launch_decode_t(const void* qp, const void* H, const int* npi, int B, int rows,
                             int n_stride, int d_m, float scale_log2, void* ctx, cudaStream_t st,
-                            float2* stats) {
+                            float2* stats, const int* h_index) {
     const int cpt = int(ceil_div(d_m, 256));
     switch (cpt) {
-        case 1: return launch_decode_cpt<T, 1>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
-        case 2: return launch_decode_cpt<T, 2>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
-        case 3: return launch_decode_cpt<T, 3>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
-        case 4: return launch_decode_cpt<T, 4>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
-        case 5: return launch_decode_cpt<T, 5>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
-        case 6: return launch_decode_cpt<T, 6>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats);
+        case 1: return launch_decode_cpt<T, 1>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats, h_index);
+        case 2: return launch_decode_cpt<T, 2>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats, h_index);
+        case 3: return launch_decode_cpt<T, 3>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats, h_index);
+        case 4: return launch_decode_cpt<T, 4>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats, h_index);
+        case 5: return launch_decode_cpt<T, 5>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats, h_index);
+        case 6: return launch_decode_cpt<T, 6>(qp, H, npi, B, rows, n_stride, d_m, scale_log2, ctx, st, stats, h_index);
         default:
             throw Status{ELATTN_ERR_UNSUPPORTED, "SIMT decode supports d_m <= 1536"};
     }
@@ -381,14 +383,14 @@ static void launch_decode_t(const void* qp, const void* H, const int* npi, int B
 
 void launch_el_decode_simt(int dtype, const void* qp, const void* H, const int* n_per_input,
                            int B, int rows_per_input, int n_stride, int d_m, float scale,
-                           void* ctx, cudaStream_t st, float2* stats) {
+                           void* ctx, cudaStream_t st, float2* stats, const int* h_index) {
     const float scale_log2 = scale * 1.4426950408889634f;
     if (dtype == ELATTN_DTYPE_BF16)
         launch_decode_t<__nv_bfloat16>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m,
-                                       scale_log2, ctx, st, stats);
+                                       scale_log2, ctx, st, stats, h_index);
     else
         launch_decode_t<float>(qp, H, n_per_input, B, rows_per_input, n_stride, d_m, scale_log2,
-                               ctx, st, stats);
+                               ctx, st, stats, h_index);
 }
 
 }  // namespace elattn_gpu

@@ -385,14 +385,16 @@ void launch_tf32_gemm(const Tf32GemmArgs& g, cudaStream_t st) {
 // (npi and r % n_stride >= npi[r / n_stride]) are zeroed (ragged padding of H).
 __global__ void tf32_split_kernel(const float* __restrict__ X, int64_t rows, int cols, int64_t ld,
                                   float* __restrict__ hi, float* __restrict__ lo, const int* __restrict__ npi,
-                                  int n_stride) {
+                                  int n_stride, const int* __restrict__ h_index) {
     const int64_t total4 = rows * (cols / 4);
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total4; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / (cols / 4);
         const int c = int(e % (cols / 4)) * 4;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         const bool keep = npi == nullptr || int(r % n_stride) < npi[r / n_stride];
-        if (keep) v = *reinterpret_cast<const float4*>(X + r * ld + c);
+        // slot-indexed H: block b of the output reads block h_index[b] of X
+        const int64_t rs = h_index ? int64_t(h_index[r / n_stride]) * n_stride + r % n_stride : r;
+        if (keep) v = *reinterpret_cast<const float4*>(X + rs * ld + c);
         float4 h, l;
         h.x = tf32_hi(v.x), h.y = tf32_hi(v.y), h.z = tf32_hi(v.z), h.w = tf32_hi(v.w);
         l.x = v.x - h.x, l.y = v.y - h.y, l.z = v.z - h.z, l.w = v.w - h.w;
@@ -404,11 +406,12 @@ __global__ void tf32_split_kernel(const float* __restrict__ X, int64_t rows, int
 // H [B][n][d_m] -> (tf32(H^T), H^T - tf32(H^T)) [B][d_m][n_pad]: the K-major B operand of
 // C = P.H (keys = K).  Keys t >= n_b (ragged) or t >= n (padding up to n_pad) are zero.
 __global__ void tf32_split_t_kernel(const float* __restrict__ H, int n, int d_m, int n_pad,
-                                    const int* __restrict__ npi, float* __restrict__ hi, float* __restrict__ lo) {
+                                    const int* __restrict__ npi, float* __restrict__ hi, float* __restrict__ lo,
+                                    const int* __restrict__ h_index) {
     __shared__ float tile[32][33];
     const int b = blockIdx.z, t0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
     const int n_b = npi ? npi[b] : n;
-    const float* Hb = H + int64_t(b) * n * d_m;
+    const float* Hb = H + int64_t(h_index ? h_index[b] : b) * n * d_m;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int t = t0 + r, d = d0 + threadIdx.x;
         tile[r][threadIdx.x] = (t < n && t < n_b && d < d_m) ? Hb[int64_t(t) * d_m + d] : 0.f;
@@ -427,18 +430,18 @@ __global__ void tf32_split_t_kernel(const float* __restrict__ H, int n, int d_m,
 }
 
 void launch_tf32_split_t(const float* H, int B, int n, int d_m, int n_pad, const int* npi, float* hi, float* lo,
-                         cudaStream_t st) {
+                         cudaStream_t st, const int* h_index) {
     dim3 grid(unsigned((n_pad + 31) / 32), unsigned((d_m + 31) / 32), unsigned(B));
-    tf32_split_t_kernel<<<grid, dim3(32, 8), 0, st>>>(H, n, d_m, n_pad, npi, hi, lo);
+    tf32_split_t_kernel<<<grid, dim3(32, 8), 0, st>>>(H, n, d_m, n_pad, npi, hi, lo, h_index);
     ELA_CHECK_LAUNCH();
 }
 
 void launch_tf32_split(const float* X, int64_t rows, int cols, int64_t ld, float* hi, float* lo, const int* npi,
-                       int n_stride, cudaStream_t st) {
+                       int n_stride, cudaStream_t st, const int* h_index) {
     ELA_REQUIRE(cols % 4 == 0 && ld % 4 == 0, ELATTN_ERR_UNSUPPORTED, "tf32 split: cols must be a multiple of 4");
     const int64_t total4 = rows * (cols / 4);
     const int grid = int(std::min<int64_t>((total4 + 255) / 256, int64_t(num_sms_tf32()) * 8));
-    tf32_split_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(X, rows, cols, ld, hi, lo, npi, n_stride);
+    tf32_split_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(X, rows, cols, ld, hi, lo, npi, n_stride, h_index);
     ELA_CHECK_LAUNCH();
 }
 

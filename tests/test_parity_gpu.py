@@ -327,7 +327,7 @@ def test_hidden_state_cache_self_attention(gpu, dtype):
         cache.gather(parent, rows_hint=n_max)
         hist = [list(hist[q]) for q in parent]
         assert cache.lengths[0].cpu().tolist() == [len(hh) for hh in hist]
-        got = cache.cache[0].double().cpu().numpy()
+        got = cache.lane_view(0).double().cpu().numpy()
         for l in range(lanes):
             assert np.array_equal(got[l, :len(hist[l])], np.stack(hist[l]))
 
@@ -508,7 +508,7 @@ def test_lane_bookkeeping_on_device(gpu):
     for l in range(2):
         for i, pi in enumerate([1, 1, 3, 0, 2]):
             n = int(ref_l[l, pi])
-            assert torch.equal(hc.cache[l, i, :n], ref_c[l, pi, :n])
+            assert torch.equal(hc.lane_view(l)[i, :n], ref_c[l, pi, :n])
     hc.keep([True, False, True, True, False])
     assert hc.lanes == 3 and torch.equal(hc.lengths, ref_l[:, torch.tensor([1, 3, 0], device="cuda")])
     hc.permute([2, 0, 1])
@@ -528,6 +528,56 @@ def test_lane_bookkeeping_on_device(gpu):
     kv.gather(torch.tensor([0, 7], dtype=torch.int32, device="cuda"))  # device parent 7 is out of range
     torch.cuda.synchronize()
     assert torch.isnan(kv.K[1].float()).all() and torch.equal(kv.K[0], K0[3])
+
+
+@pytest.mark.parametrize("dtype", [1, 0])
+def test_hidden_state_cache_copy_on_fork(gpu, dtype):
+    """The slot-indexed cache's fork against a host mirror of gather_lanes (model.hpp:
+    291-306) over several reorders: random parents (repeats and drops), a permutation (no
+    slot changes hands... every lane keeps its parent's slot), an expansion past the slot
+    count (the store grows), an out-of-range device parent (loud length n_max + 1); and the
+    attention read through the slot map equals the step over a physically gathered H."""
+    import torch
+
+    E = gpu
+    L, lanes, n_max, d_m = 2, 6, 24, 256
+    td = torch.bfloat16 if dtype == 1 else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(5)
+    hc = E.HiddenStateCache(L, lanes, n_max, d_m, dtype)
+    hc.cache.copy_((torch.rand(hc.cache.shape, generator=g, device="cuda") * 2 - 1).to(td))
+    lens = torch.randint(1, n_max, (L, lanes), generator=g, device="cuda", dtype=torch.int32)
+    hc.lengths.copy_(lens)
+    mirror = [[hc.cache[l, i, : int(lens[l, i])].clone() for i in range(lanes)] for l in range(L)]
+    rng = np.random.default_rng(11)
+    plans = [list(rng.integers(0, lanes, lanes)), list(rng.permutation(lanes)), list(rng.integers(0, lanes, 4)),
+             [0, 1, 1, 2, 3, 3, 3, 0], list(rng.integers(0, 8, 8))]
+    for parent in plans:
+        slots_before = hc.lane_slot.clone()
+        hc.gather([int(p) for p in parent], rows_hint=n_max)
+        if sorted(parent) == list(range(len(parent))):  # permutation: histories change lanes, not slots
+            assert sorted(hc.lane_slot.tolist()) == sorted(slots_before.tolist())
+        mirror = [[mirror[l][int(p)] for p in parent] for l in range(L)]
+        assert hc.lanes == len(parent)
+        for l in range(L):
+            view = hc.lane_view(l)
+            for i in range(hc.lanes):
+                n = mirror[l][i].shape[0]
+                assert int(hc.lengths[l, i]) == n
+                assert torch.equal(view[i, :n], mirror[l][i])
+        assert len(set(hc.lane_slot.tolist())) == hc.lanes  # every lane owns its slot
+    # attention through the slot map == the step over the lane-ordered copy
+    p = E.AttentionParams.random(4, d_m, 64, E.Rng(3))
+    layer = E.ElAttentionLayer(p, dtype)
+    Y = (torch.rand((hc.lanes, d_m), generator=g, device="cuda") * 2 - 1).to(td)
+    got = hc.attend(layer, 1, Y)
+    want = layer.step(Y, hc.lane_view(1), hc.lengths[1].clone())
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    # out-of-range device parent: loud length, the other lanes intact
+    hc.gather(torch.tensor([1, 99], dtype=torch.int32, device="cuda"))
+    torch.cuda.synchronize()
+    assert int(hc.lengths[0, 1]) == n_max + 1 and int(hc.lengths[0, 0]) == mirror[0][1].shape[0]
+    assert torch.equal(hc.lane_view(0)[0, : mirror[0][1].shape[0]], mirror[0][1])
 
 
 def test_beam_candidates_errors_and_edges(gpu):

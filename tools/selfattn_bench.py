@@ -39,6 +39,11 @@ cache.cache.copy_((torch.rand(cache.cache.shape, generator=g, device="cuda") * 2
 Y = (torch.rand((lanes, d_m), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
 outs = [torch.empty_like(Y) for _ in range(2)]
 parent = torch.arange(lanes, device="cuda", dtype=torch.int32).view(a.B, a.beam).flip(1).reshape(-1)
+# a beam-search-like reorder: each lane continues a random beam of its own input (parents
+# repeat, some beams die) — copy-on-fork copies one history per extra child
+gp = torch.Generator().manual_seed(7)
+parent_beam = (torch.arange(a.B).view(a.B, 1) * a.beam + torch.randint(0, a.beam, (a.B, a.beam), generator=gp))
+parent_beam = parent_beam.reshape(-1).to(torch.int32).cuda()
 
 
 def timed(fn):
@@ -74,15 +79,20 @@ for n in a.n:
     def step_gather():
         cache.gather(parent, rows_hint=n)
 
+    def step_gather_beam():
+        cache.gather(parent_beam, rows_hint=n)
+
     ms_attn = timed(step_attn)
     cache.lengths.copy_(base + 1)
     ms_gather = timed(step_gather)
+    ms_gather_beam = timed(step_gather_beam)
     byt = L * lanes * n * d_m * 2  # every lane's history read once per layer
     print(json.dumps({"config": "GPT-2 medium decoder-only, hidden-state-only cache", "B": a.B, "beam": a.beam,
                       "lanes": lanes, "layers": L, "n": n, "attn_ms_per_step": ms_attn,
                       "tokens_per_s": lanes / (ms_attn / 1e3), "history_GBps": byt / (ms_attn / 1e3) / 1e9,
-                      "gather_ms_per_step": ms_gather,
-                      "gather_GBps": 2 * byt / (ms_gather / 1e3) / 1e9,
+                      "gather_ms_per_step": ms_gather, "gather_parent": "permutation (beams reversed)",
+                      "gather_beam_ms_per_step": ms_gather_beam,
+                      "gather_beam_copies": int(a.beam * a.B - sum(len(set(r)) for r in parent_beam.view(a.B, a.beam).tolist())),
                       "cache_GB": cache.cache.numel() * 2 / 1e9}), flush=True)
 
 # ---- the reference's decoder-only EL form: mixed self-attention (EL over the prefix shared
