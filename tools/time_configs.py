@@ -4,6 +4,7 @@ between CUDA events — device time, no host gaps.
 
     python tools/time_configs.py
 """
+import argparse
 import json
 import sys
 from pathlib import Path
@@ -12,6 +13,15 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch  # noqa: E402
 
 import paper_2105_04779_b200 as E  # noqa: E402
+from paper_2105_04779_b200 import capi  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--lib", default=None, help="library build to load (A/B runs)")
+ap.add_argument("--only", default=None, help="substring of the config name")
+ap.add_argument("--B", type=int, nargs="*", default=None, help="batch sizes (default: per config)")
+a = ap.parse_args()
+if a.lib:
+    capi.LIB_PATH = Path(a.lib).resolve()
 
 CONFIGS = [  # (name, d_m, h, x, n, B list)
     ("2 BART-large beam 4", 1024, 16, 4, 1024, [32, 64, 128, 320]),
@@ -21,7 +31,9 @@ CONFIGS = [  # (name, d_m, h, x, n, B list)
 L, REPS, HBM = 12, 10, 6545.6e9
 layers = [E.ElAttentionLayer(E.AttentionParams.random(16, 1024, 64, E.Rng(1 + l)), E.DTYPE_BF16) for l in range(L)]
 for name, d_m, h, x, n, Bs in CONFIGS:
-    for B in Bs:
+    if a.only and a.only not in name:
+        continue
+    for B in (a.B or Bs):
         g = torch.Generator(device="cuda").manual_seed(B)
         H = (torch.rand((B, n, d_m), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
         dec = E.DecoderStep(layers, H, B, x)
