@@ -1123,14 +1123,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         if (lane == 0) ptx::mbar_arrive(o_free);
                     }
                     uint2* body = reinterpret_cast<uint2*>(rec + kPartFloatsHdr + m * kPartFloatsUnit);
+                    // evict-last: the merge kernel re-reads the records right after this
+                    // kernel, and the H stream would otherwise push them out of L2
 #pragma unroll
                     for (int i4 = 0; i4 < 8; ++i4) {
-                        body[(0 * 8 + i4) * 128 + tid] =
-                            make_uint2(pack_bf16x2(__uint_as_float(lo[4 * i4]), __uint_as_float(lo[4 * i4 + 1])),
-                                       pack_bf16x2(__uint_as_float(lo[4 * i4 + 2]), __uint_as_float(lo[4 * i4 + 3])));
-                        body[(1 * 8 + i4) * 128 + tid] =
-                            make_uint2(pack_bf16x2(__uint_as_float(hi[4 * i4]), __uint_as_float(hi[4 * i4 + 1])),
-                                       pack_bf16x2(__uint_as_float(hi[4 * i4 + 2]), __uint_as_float(hi[4 * i4 + 3])));
+                        ptx::st_global_v2_hint(&body[(0 * 8 + i4) * 128 + tid],
+                                               pack_bf16x2(__uint_as_float(lo[4 * i4]), __uint_as_float(lo[4 * i4 + 1])),
+                                               pack_bf16x2(__uint_as_float(lo[4 * i4 + 2]), __uint_as_float(lo[4 * i4 + 3])),
+                                               ptx::kEvictLast);
+                        ptx::st_global_v2_hint(&body[(1 * 8 + i4) * 128 + tid],
+                                               pack_bf16x2(__uint_as_float(hi[4 * i4]), __uint_as_float(hi[4 * i4 + 1])),
+                                               pack_bf16x2(__uint_as_float(hi[4 * i4 + 2]), __uint_as_float(hi[4 * i4 + 3])),
+                                               ptx::kEvictLast);
                     }
                 }
             }
@@ -1257,6 +1261,18 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
     // The fragments of the first kPre segments do not depend on the weights: all of their
     // loads are issued before phase 1, so the merge costs ~one L2 round trip, not nseg + 1
     constexpr int kPer = 2 * 8 * 128 / 256, kPre = 4;
+    // the per-row maxima and sums first (phase 1 needs them before anything else), then
+    // the fragments
+    float ms[kMaxSegs], ls[kMaxSegs];
+    if (tid < 64) {
+#pragma unroll
+        for (int s = 0; s < kMaxSegs; ++s)
+            if (s < nseg) {
+                const float* r = rec_of(s);
+                ms[s] = __ldcg(r + tid);
+                ls[s] = __ldcg(r + 64 + tid);
+            }
+    }
     uint2 vp[kPre][kPer];
 #pragma unroll
     for (int s = 0; s < kPre; ++s)
@@ -1266,15 +1282,10 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
             for (int j = 0; j < kPer; ++j) vp[s][j] = __ldcg(body + tid + 256 * j);
         }
     if (tid < 64) {
-        float ms[kMaxSegs], ls[kMaxSegs], M = -INFINITY, L = 0.f;
+        float M = -INFINITY, L = 0.f;
 #pragma unroll
         for (int s = 0; s < kMaxSegs; ++s)
-            if (s < nseg) {
-                const float* r = rec_of(s);
-                ms[s] = __ldcg(r + tid);
-                ls[s] = __ldcg(r + 64 + tid);
-                M = fmaxf(M, ms[s]);
-            }
+            if (s < nseg) M = fmaxf(M, ms[s]);
 #pragma unroll
         for (int s = 0; s < kMaxSegs; ++s)
             if (s < nseg) {
@@ -1285,6 +1296,7 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
         s_inv[tid] = 1.f / L;
         if (stats != nullptr && rank == 0 && m == 0 && tid < vnrows(b, rows, vchunks))
             stats[vrow0(b, rows, vchunks) + tid] = make_float2(M * scale_log2, L);
+        if (tid == 0) ELA_TL_MARK(0);  // segment weights ready
     }
     __syncthreads();
     float4 acc[kPer];
@@ -1322,6 +1334,7 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
         tile[q0 + 1][d0 + 8] = __float2bfloat16_rn(acc[j].w * s_inv[q0 + 1]);
     }
     __syncthreads();
+    if (tid == 0) ELA_TL_MARK(1);  // merged tile staged
     const int dm_off = rank * (d_m / 2) + m * 128;
     const int r0 = vrow0(b, rows, vchunks);
     for (int e = tid; e < vnrows(b, rows, vchunks) * 16; e += 256) {
@@ -1329,6 +1342,7 @@ __global__ void __launch_bounds__(256) el_decode_merge_kernel(const float* __res
         *reinterpret_cast<uint4*>(ctx + (int64_t(r0) + q) * d_m + dm_off + 8 * v) =
             *reinterpret_cast<const uint4*>(&tile[q][8 * v]);
     }
+    if (tid == 0) ELA_TL_MARK(2);  // stores issued
     ELA_TL_EXIT(kTlMerge);
 }
 

@@ -245,6 +245,10 @@ __device__ __forceinline__ void bulk_wait_group() {
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
+// 8-byte global store with an L2 cache-policy hint
+__device__ __forceinline__ void st_global_v2_hint(void* p, uint32_t a, uint32_t b, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol) : "memory");
+}
 
 // Make generic-proxy smem writes visible to the async proxy (tcgen05.mma / TMA).
 __device__ __forceinline__ void fence_proxy_async_smem() {
