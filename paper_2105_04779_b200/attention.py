@@ -494,6 +494,7 @@ class HiddenStateCache:
             self._ws = torch.empty(need, dtype=torch.uint8, device="cuda")
         dlen, dslot = self._spare
         st = stream if stream is not None else torch.cuda.current_stream()
+        _record([self._ws, dlen, dslot, parent], stream)  # allocated on the current stream, used on `stream`
         hint = rows_hint if rows_hint is not None else self.n_max
         capi.check(capi.lib().elattn_gpu_cache_fork(
             self.cache.data_ptr(), L, self.slots, self.n_max, self.d_m, self.dtype, self.lengths.data_ptr(),
