@@ -34,9 +34,10 @@ __device__ unsigned tl_cap_;
 #define ELA_TL_EXIT(kind)                                                                             \
     do {                                                                                              \
         if (threadIdx.x == 0 && tl_buf_ != nullptr) {                                                 \
+            const unsigned long long tl_exit_ = ::elattn_gpu::ptx::globaltimer(); /* before the atomic */ \
             const unsigned i_ = atomicAdd(tl_cnt_, 1u);                                               \
             if (i_ < tl_cap_)                                                                         \
-                tl_buf_[i_] = ::elattn_gpu::TlRec{tl_entry_, tl_wait_, ::elattn_gpu::ptx::globaltimer(), \
+                tl_buf_[i_] = ::elattn_gpu::TlRec{tl_entry_, tl_wait_, tl_exit_,                        \
                                                   {tl_mark_[0], tl_mark_[1], tl_mark_[2], tl_mark_[3]}, \
                                                   unsigned(kind),                                     \
                                                   blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)}; \
