@@ -580,6 +580,31 @@ def test_hidden_state_cache_copy_on_fork(gpu, dtype):
     assert torch.equal(hc.lane_view(0)[0, : mirror[0][1].shape[0]], mirror[0][1])
 
 
+def test_hidden_state_cache_fork_many_lanes(gpu):
+    """Copy-on-fork plan over more lanes / slots than one CTA has threads (1300 lanes,
+    1500 slots: the plan kernel's strided scans), shrinking and growing lane counts."""
+    import torch
+
+    E = gpu
+    L, lanes, n_max, d_m = 1, 1300, 6, 256
+    g = torch.Generator(device="cuda").manual_seed(9)
+    hc = E.HiddenStateCache(L, lanes, n_max, d_m, E.DTYPE_BF16, slots=1500)
+    hc.cache.copy_((torch.rand(hc.cache.shape, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+    hc.lengths.copy_(torch.randint(1, n_max + 1, (L, lanes), generator=g, device="cuda", dtype=torch.int32))
+    view, lens = hc.lane_view(0).clone(), hc.lengths[0].clone()
+    rng = np.random.default_rng(4)
+    for lanes_out in (1300, 900, 1500):
+        parent = rng.integers(0, hc.lanes, lanes_out)
+        hc.gather([int(p) for p in parent])
+        idx = torch.from_numpy(parent).cuda().long()
+        view, lens = view[idx], lens[idx]
+        assert torch.equal(hc.lengths[0], lens)
+        got = hc.lane_view(0)
+        mask = torch.arange(n_max, device="cuda")[None, :] < lens[:, None].long()
+        assert torch.equal(got[mask], view[mask])
+        assert len(set(hc.lane_slot.tolist())) == hc.lanes
+
+
 def test_beam_candidates_errors_and_edges(gpu):
     """Reference-style errors at the boundary (k outside [1, 32], roots > lanes, shape
     mismatch) and edges: fewer finite candidates than k (parent -1 rows), V = 1, 256 lanes."""
