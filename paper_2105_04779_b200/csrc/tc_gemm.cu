@@ -640,16 +640,21 @@ __global__ void __launch_bounds__(kSkThreads, 1)
 // does, so the result is bit-identical to it.  Standalone (graph replay, beam 4): 7.0 us at
 // B <= 16 vs 9.1 for the two GEMMs; 8.3 vs 8.5 at B = 32, where the two-GEMM path is still
 // ahead inside the decoder step (the split-K Q GEMM spreads the 256 KB Y tile over 4 CTAs)
-constexpr int kQxThreads = 192, kQxKbp = 2, kQxStages = 3;
+// Four k-blocks per TMA box (64 KB Y / 32 KB W_Q boxes: a CTA's TMA ingress grows with the
+// box size, tools/probes/gemm_ingress_probe.cu) in two stages; the second W_K chunk buffer
+// is stage 0's memory, free once the Q_i accumulation has drained.
+constexpr int kQxThreads = 192, kQxKbp = 4, kQxStages = 2;
 struct QxSmem {
     static constexpr uint32_t kABytes = kBM * kBK * 2;  // Y: 128 rows x 64 k
     static constexpr uint32_t kBBytes = 64 * kBK * 2;   // W_Q,i: 64 rows x 64 k
     static constexpr uint32_t kStageBytes = kQxKbp * (kABytes + kBBytes);
+    static constexpr uint32_t kWkBytes = 128 * 64 * 2;           // one W_K chunk: 128 rows x 64 k
     static constexpr uint32_t kQOff = kQxStages * kStageBytes;  // Q_i bf16, 128 x 64, SW128 K-major
-    static constexpr uint32_t kWkOff = kQOff + kBM * 64 * 2;    // W_K chunks: 2 x (128 rows x 64 k)
-    static constexpr uint32_t kBarOff = kWkOff + 2 * 128 * 64 * 2;
+    static constexpr uint32_t kWkOff = kQOff + kBM * 64 * 2;    // W_K chunk buffer 0 (buffer 1: stage 0)
+    static constexpr uint32_t kBarOff = kWkOff + kWkBytes;
     static constexpr uint32_t kTotal = kBarOff + 256 + 1024;
     static_assert(kTotal <= 232448, "fused query expansion shared memory");
+    static_assert(kStageBytes >= kWkBytes, "W_K chunk buffer 1 lives in stage 0");
 };
 struct QxParams {
     int M, d_m, h, nkb, nks, chunks, pdl;  // chunks: 128-column q' chunks per CTA (d_m / 4 / 128)
@@ -711,10 +716,11 @@ __global__ void __launch_bounds__(kQxThreads, 1)
     const uint32_t tmem = *tmem_slot;
     const uint32_t tq = tmem, tp = tmem + 128;  // Q_i: 64 columns; q' chunks: 2 x 128 columns
     const int b_pre = p.pdl ? min(kQxStages, p.nks) : 0;
+    auto wk_buf = [&](int bi) { return bi == 0 ? sWk : smem; };  // buffer 1 = stage 0 (after phase 1)
     auto load_wk = [&](int c) {
         const int bi = c & 1;
-        ptx::mbar_arrive_expect_tx(&wk_full[bi], 128 * 64 * 2);
-        ptx::tma_load_3d(sWk + bi * 128 * 64 * 2, &tmWk, &wk_full[bi], 0, col0 + c * 128, z, ptx::kEvictLast);
+        ptx::mbar_arrive_expect_tx(&wk_full[bi], S::kWkBytes);
+        ptx::tma_load_3d(wk_buf(bi), &tmWk, &wk_full[bi], 0, col0 + c * 128, z, ptx::kEvictLast);
     };
     if (p.pdl) {
         ptx::griddep_launch_dependents();
@@ -724,7 +730,7 @@ __global__ void __launch_bounds__(kQxThreads, 1)
                 ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
                 ptx::tma_load_4d(stage_b(s), &tmWq, &full[s], 0, z * 64, 0, s * kQxKbp, ptx::kEvictLast);
             }
-            for (int c = 0; c < 2 && c < p.chunks; ++c) load_wk(c);
+            if (p.chunks > 0) load_wk(0);
         }
         __syncwarp();
         ptx::griddep_wait();
@@ -732,8 +738,7 @@ __global__ void __launch_bounds__(kQxThreads, 1)
     }
     if (warp == 0) {
         if (ptx::elect_one()) {
-            if (!p.pdl)
-                for (int c = 0; c < 2 && c < p.chunks; ++c) load_wk(c);
+            if (!p.pdl && p.chunks > 0) load_wk(0);
             for (int ks = 0; ks < p.nks; ++ks) {
                 const int s = ks % kQxStages;
                 ptx::mbar_wait(&empty[s], ((ks / kQxStages) & 1) ^ 1);
@@ -741,6 +746,11 @@ __global__ void __launch_bounds__(kQxThreads, 1)
                 if (!pre) ptx::mbar_arrive_expect_tx(&full[s], S::kStageBytes);
                 ptx::tma_load_4d(stage_a(s), &tmY, &full[s], 0, m0, 0, ks * kQxKbp, ptx::kEvictNormal);
                 if (!pre) ptx::tma_load_4d(stage_b(s), &tmWq, &full[s], 0, z * 64, 0, ks * kQxKbp, ptx::kEvictLast);
+            }
+            // chunk 1 goes to stage 0's memory once every phase-1 MMA has completed
+            if (p.chunks > 1) {
+                ptx::mbar_wait(acc_full, 0);
+                load_wk(1);
             }
             for (int c = 2; c < p.chunks; ++c) {
                 ptx::mbar_wait(&wk_empty[c & 1], ((c >> 1) - 1) & 1);
@@ -779,17 +789,16 @@ __global__ void __launch_bounds__(kQxThreads, 1)
         ptx::tc_fence_after();
         constexpr uint32_t idp = ptx::idesc_bf16(kBM, 128, 0, 0);
         const uint64_t aq = ptx::sdesc_sw128(ptx::smem_u32(sQ), 0, 1024);
-        const uint64_t bw = ptx::sdesc_sw128(ptx::smem_u32(sWk), 0, 1024);
         for (int c = 0; c < p.chunks; ++c) {
             const int bi = c & 1;
+            const uint64_t bw = ptx::sdesc_sw128(ptx::smem_u32(wk_buf(bi)), 0, 1024);
             ptx::mbar_wait(&wk_full[bi], (c >> 1) & 1);
             if (c >= 2) ptx::mbar_wait(&p_empty[bi], ((c >> 1) - 1) & 1);
             ptx::tc_fence_after();
             if (lane == 0) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    ptx::mma_bf16(tp + bi * 128, aq + uint64_t(2 * k),
-                                  bw + uint64_t((bi * 128 * 64 * 2) >> 4) + uint64_t(2 * k), idp, k != 0);
+                    ptx::mma_bf16(tp + bi * 128, aq + uint64_t(2 * k), bw + uint64_t(2 * k), idp, k != 0);
                 ptx::mma_commit(&wk_empty[bi]);
                 ptx::mma_commit(&p_full[bi]);
             }
@@ -1070,11 +1079,15 @@ void launch_splitk(const GemmArgs& g, cudaStream_t st) {
     return launch_splitk_cfg<SK, false, false>(g, st);
 }
 
-// rows up to which the fused query expansion is used automatically (ELATTN_QEXP_ROWS overrides)
+// Rows for which the fused query expansion is used automatically: M <= 64 and
+// 128 < M <= qexp_max_rows() (default 256; ELATTN_QEXP_ROWS overrides the bound).  Measured
+// in the 12-layer step (profiles/r02c_qexp_threshold.jsonl): B = 8 / 16 -1% / -1%, B = 48 /
+// 64 (two row tiles) -3% / -1.8%; at 65..128 rows (B = 24 / 32, one row tile, 64 CTAs) the
+// split-K Q GEMM + q' GEMM stay 0.4-0.5% ahead.
 int qexp_max_rows() {
     static const int v = [] {
         const char* e = getenv("ELATTN_QEXP_ROWS");
-        return e ? atoi(e) : 64;
+        return e ? atoi(e) : 256;
     }();
     return v;
 }
@@ -1089,8 +1102,7 @@ bool launch_qexp_fused(const void* Y, int M, const void* WqT, const float* bq, c
     if (env == 0 || g_qexp_fused == 0) return false;
     const int items = int(ceil_div(M, kBM)) * h;
     if (d_k != 64 || d_m % 512 != 0 || 4 * items > 2 * num_sms()) return false;
-    // automatic use up to qexp_max_rows() rows (measured: tools/probes/qexp_time.py)
-    if (g_qexp_fused < 0 && env < 0 && M > qexp_max_rows()) return false;
+    if (g_qexp_fused < 0 && env < 0 && (M > qexp_max_rows() || (M > 64 && M <= 128))) return false;
     if (bq == nullptr || !aligned16(Y) || !aligned16(WqT) || !aligned16(Wk) || !aligned16(qp) || !aligned16(bq)) return false;
     QxParams p{};
     p.M = M, p.d_m = d_m, p.h = h, p.nkb = d_m / kBK, p.nks = int(ceil_div(d_m / kBK, kQxKbp)), p.chunks = d_m / 4 / 128;
