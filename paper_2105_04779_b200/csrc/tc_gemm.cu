@@ -134,11 +134,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_tiles = p.Z * p.tiles_m * p.tiles_n;
     // z (head) fastest: the CTAs running concurrently touch the SAME rows r of the
     // head-interleaved layouts (q' / C rows r*h + i), so their row pieces land in the same
-    // DRAM pages; then n, so neighbouring CTAs share the A rows in L2
+    // DRAM pages; then n, so neighbouring CTAs share the A rows in L2.  Row blocks run LAST
+    // to FIRST: the first inputs' rows are written last and are still in L2 when the next
+    // kernel (the decode, reading q' input by input) starts with them
     auto tile_coords = [&](int t, int& z, int& m0, int& n0) {
         z = t % p.Z;
         const int r = t / p.Z;
-        m0 = (r / p.tiles_n) * (MT * kBM);
+        m0 = (p.tiles_m - 1 - r / p.tiles_n) * (MT * kBM);
         n0 = (r % p.tiles_n) * BN;
     };
 
