@@ -1001,7 +1001,7 @@ struct Cfg {
 
 // Block shape per GEMM (B200, 148 SMs):
 //   * N <= 64 (per-head V projection, N = d_k): 128 x 64 tiles, two m-subtiles per CTA
-//     sharing the weight slice when that still leaves one wave;
+//     sharing the weight slice beyond two waves of single tiles;
 //   * K <= 128 (q' expansion, write-bound): 128 x 256 tiles (128 x 128 for small M), one k-step;
 //   * otherwise (Y.W_Q, V.W_O): 128 x 128 tiles;
 // with two k-blocks per TMA box whenever K allows.
@@ -1010,7 +1010,10 @@ Cfg choose(const GemmArgs& g) {
     if (g.N <= 64) {
         c = {64, 1, 2};
         const int64_t tiles = ceil_div(g.M, kBM) * g.Z;
-        if (g.K >= 256 && tiles > num_sms()) c.mt = 2;
+        // two m-subtiles (halving the weight traffic) only beyond two waves of single tiles:
+        // up to two waves, one subtile per CTA keeps all 148 SMs streaming A (the decode's C,
+        // read from DRAM inside the step): B = 296 / 320 step -0.5% (80 -> 148 CTAs)
+        if (g.K >= 256 && tiles > 2 * num_sms()) c.mt = 2;
     } else if (g.K <= 128) {
         // write-bound q' expansion: 256-wide tiles, unless that leaves half the SMs idle
         // (small batches: 128-wide, measured 3.4 vs 4.3 us at B = 32, tools/time_gemms.py)
