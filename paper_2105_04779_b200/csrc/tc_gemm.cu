@@ -1046,10 +1046,15 @@ int choose_splitk(const GemmArgs& g) {
     const int sms = num_sms();
     const int64_t max_cl[3] = {sms / 2, (sms * 33) / 148, (sms * 15) / 148};
     const int sks[3] = {2, 4, 8};
-    // the widest split that keeps about 64 CTAs (measured best at B = 16..128, beam 4:
-    // tools/time_small_batch.py), else pairs while one wave of pairs holds the tiles
+    // the widest split whose clusters are all co-resident in one wave, at most ~64 CTAs —
+    // or up to one CTA per SM when every row tile is full (since the bulk-DSMEM exchange,
+    // SK = 4 on 128 CTAs beats pairs at B = 64, step -1%, but not at B = 48, whose second
+    // row tile is half empty: +0.7%; profiles/r02c_splitk_factor_sweep*.txt)
+    const bool full_rows = g.M % kBM == 0;
     for (int i = 2; i >= 0; --i)
-        if (ok(sks[i]) && tiles <= max_cl[i] && (tiles * sks[i] <= 64 || sks[i] == 2)) return sks[i];
+        if (ok(sks[i]) && tiles <= max_cl[i] &&
+            (tiles * sks[i] <= 64 || sks[i] == 2 || (full_rows && tiles * sks[i] <= sms)))
+            return sks[i];
     return 0;
 }
 
