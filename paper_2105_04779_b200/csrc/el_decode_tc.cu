@@ -1415,9 +1415,10 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     const int sched_mode = g_decode_sched_override ? g_decode_sched_override : sched_mode_env;
     // H's L2 policy: streamed once (evict-first) unless it fits in L2 with room to spare —
     // then every layer of a decoder step re-reads it from L2 (evict-last; measured 2% per
-    // step at B = 16, tools/time_small_batch.py); sibling virtual inputs (> 64 rows) share
-    // H_b across neighbouring clusters (evict-normal).
-    // ELATTN_DECODE_H_POLICY = auto | first | normal | last, ELATTN_DECODE_H_KEEP_MB (48)
+    // step at B = 16 and 1% at B = 32 (64 MB), worse from 80 MB: tools/time_small_batch.py,
+    // profiles/r02c_h_keep_sweep.txt); sibling virtual inputs (> 64 rows) share H_b across
+    // neighbouring clusters (evict-normal).
+    // ELATTN_DECODE_H_POLICY = auto | first | normal | last, ELATTN_DECODE_H_KEEP_MB (64)
     static const int h_pol_mode = [] {
         const char* e = getenv("ELATTN_DECODE_H_POLICY");
         const std::string v = e ? e : "";
@@ -1425,7 +1426,7 @@ void launch_units(const void* qp, const void* H, const int* npi, int B, int rows
     }();
     static const size_t h_keep_bytes = [] {
         const char* e = getenv("ELATTN_DECODE_H_KEEP_MB");
-        return size_t(e ? atoi(e) : 48) << 20;
+        return size_t(e ? atoi(e) : 64) << 20;
     }();
     const size_t h_bytes = size_t(B_h) * n_stride * d_m * 2;
     sa.h_pol = h_pol_mode == 1   ? ptx::kEvictFirst
